@@ -1,0 +1,28 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
+    config.addinivalue_line("markers", "slow: longer CPU cases")
+
+
+@pytest.fixture(scope="session")
+def orc():
+    from oracle.oracle import Oracle, build
+    build()
+    return Oracle("orc")
+
+
+@pytest.fixture(scope="session")
+def ref():
+    from oracle.oracle import Oracle, available
+    if not available("ref"):
+        pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
+    return Oracle("ref")
