@@ -11,6 +11,7 @@ import ctypes as C
 i8, u8, i32, u32, i64, u64, f64 = (C.c_int8, C.c_uint8, C.c_int32, C.c_uint32, C.c_int64,
                                    C.c_uint64, C.c_double)
 
+ABI_VERSION = 1
 MLOB_OK, MLOB_E_INVALID_ARGUMENT, MLOB_E_OUT_OF_RANGE, MLOB_E_LOGIC, MLOB_E_RUNTIME, MLOB_E_CUDA = range(6)
 
 # lob::MsgKind / Side (lob/types.hpp:8-22)

