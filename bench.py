@@ -1,0 +1,323 @@
+"""Throughput bench of the batched LOB environment step (BASELINE.json metric:
+LOB env-steps/sec at 1/2/4/8 B200, % of HBM roofline, CPU reference beside it).
+
+A "step" is one environment step of every env (bench::RandomStepHarness,
+bench/bench.hpp:53-70: random actions keyed (seed, BenchAction, env, step),
+auto-reset).  The unit of the metric is the message-level LOB step — one MBO
+message (agent or replay) through one env's book — counted exactly like the
+reference's messages_processed (env.hpp:233, bench.hpp:133-154).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload E|B|C]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
+  python bench.py --impl reference ...                    (the reference on the host cores)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "LOB env-steps/sec (1/2/4/8 B200) and % HBM roofline vs CPU reference"
+UNIT = "msg-steps/s"
+# Algorithmic bytes per message-level step, SURVEY.md §8(d) / DESIGN.md
+# ("Roofline"): book slots r+w, replay message read, env/agent state r+w,
+# outputs; per config.
+B_MSG = {"B": 171.4, "C": 169.1, "E": 169.1}
+HBM_FALLBACK = 6650.0
+
+
+def workload(name: str):
+    """BASELINE.json configs: unique-start synthetic stores
+    (an episode every 100 messages), 64 steps x 100 msgs, capacity 100."""
+    from paper_2511_02136_b200 import abi
+    ex = abi.agent_spec(abi.EXECUTOR)
+    mm = abi.agent_spec(abi.MARKET_MAKER)
+    n_envs, specs, label = {
+        "B": (4096, [ex], "B: 4096 envs, single execution agent"),
+        "C": (65536, [mm, ex], "C: 65536 envs, two-agent (market maker + execution)"),
+        "E": (1 << 20, [mm, ex], "E: 1M (2^20) envs, two-agent, env-sharded over the GPUs"),
+    }[name]
+    cfg = abi.env_config(specs, steps_per_episode=64, messages_per_step=100, start_stride_steps=1)
+    synth = abi.synth_config(n_messages=(n_envs + 64) * 100, state_sample_every=100)
+    return n_envs, cfg, synth, label
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_reference_run(n_envs_cap: int, steps: int, warmup: int, name: str):
+    """bench::run_throughput (bench.hpp:98-160) of the compiled reference
+    (oracle/_ref) on this host's cores, same workload, bounded env count."""
+    from oracle.oracle import Oracle, available, bench_run
+    if not available("ref"):
+        raise RuntimeError("oracle/_ref not built")
+    o = Oracle("ref")
+    n_envs, cfg, synth, label = workload(name)
+    n = min(n_envs, n_envs_cap)
+    from paper_2511_02136_b200 import abi
+    small = abi.synth_config(n_messages=(n + 64) * 100, state_sample_every=100)
+    store = o.synth(small, 0)   # the same stream's prefix: identical episodes 0..n
+    workers = os.cpu_count() or 1
+    row = bench_run(o, store, cfg, n, steps, warmup, workers, 0, 100, 1)
+    return row, workers, n, label
+
+
+def reference_arm(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    row, workers, n, label = cpu_reference_run(args.ref_envs, args.steps, args.warmup, args.workload)
+    v = row.messages_per_sec
+    sample = (f"{n} envs x {args.steps} timed steps (+{args.warmup} warm-up) of workload "
+              f"{args.workload}, bench::run_throughput with {workers} worker threads")
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * row.wall_seconds / max(1, args.steps), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+           "config": {"workload": label, "n_envs_sample": n, "messages_per_step": 100,
+                      "book_capacity": 100},
+           "env_steps_per_s": row.steps_per_sec,
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "reference",
+                            "sample": sample},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def gpu_arm(args) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_02136_b200 import abi
+    from paper_2511_02136_b200.env import DeviceStore, HostStore, MarketVecEnv
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local if world > 1 else 0
+    torch.cuda.set_device(dev)
+
+    n_total, cfg, synth, label = workload(args.workload)
+    if args.envs:
+        n_total = args.envs
+        synth.n_messages = (n_total + 64) * 100
+    per = n_total // world
+    base = rank * per
+    n_local = per if rank < world - 1 else n_total - base
+    t0 = time.time()
+    hs = HostStore.synth(synth, 0)
+    gen_s = time.time() - t0
+    store = DeviceStore(hs, dev)
+    del hs
+    venv = MarketVecEnv(store, cfg, seed=0, n_envs=n_local, n_envs_global=n_total,
+                        env_index_base=base, device=dev)
+    venv.reset_all()
+    stream = torch.cuda.ExternalStream(venv.stream, device=torch.device("cuda", dev))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    gstep = 0
+    for _ in range(args.warmup):
+        venv.step_random(0, gstep)
+        gstep += 1
+    venv.synchronize()
+    m0 = venv.messages_processed()
+    l0 = venv.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    with ClockSampler(dev) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            venv.step_random(0, gstep)
+            gstep += 1
+        ev1.record(stream)
+        ev1.synchronize()
+    launches = venv.launches - l0
+    venv.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    msgs = venv.messages_processed() - m0
+    # whole-job: max time over ranks, sum of messages
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    m = torch.tensor([msgs], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(m, op=dist.ReduceOp.SUM)
+    ms_max, msgs_all = float(t.item()), float(m.item())
+    value = msgs_all / (ms_max / 1e3)
+    env_steps = n_total * args.steps / (ms_max / 1e3)
+
+    # K4 + NCCL: episode statistics reduced across ranks (the only collective)
+    stats = torch.zeros(5 * cfg.n_specs, dtype=torch.float64, device="cuda")
+    venv.episode_stats_device(stats.data_ptr())
+    venv.synchronize()
+    if world > 1:
+        dist.all_reduce(stats)
+
+    # e2e through the public API with host buffers: pinned actions H2D, step,
+    # rewards + dones + observations D2H, every step
+    A = venv.n_agents
+    rng = np.random.default_rng(1234)
+    ar = np.array([abi.action_arity(cfg.specs[s]) for s in abi.flat_specs(cfg)])
+    acts = torch.from_numpy((rng.integers(0, 1 << 30, size=(n_local, A)) % ar).astype(np.int32))
+    acts = acts.pin_memory()
+    obs_bufs = [torch.empty((venv.n_streams(t), venv.obs_dim(t)), dtype=torch.float64).pin_memory()
+                for t in range(cfg.n_specs)]
+    rew = torch.empty((n_local, A), dtype=torch.float64).pin_memory()
+    dn = torch.empty((n_local, A), dtype=torch.uint8).pin_memory()
+    rs = torch.empty(max(venv.n_streams(t) for t in range(cfg.n_specs)), dtype=torch.uint8).pin_memory()
+    from paper_2511_02136_b200 import env as E
+    L = E.lib()
+    e_steps = max(3, min(args.steps, args.e2e_steps))
+    barrier()
+    w0 = time.perf_counter()
+    for _ in range(e_steps):
+        E._check(L.mlob_venv_set_actions(venv.h, acts.data_ptr(), 0))
+        venv.step()
+        E._check(L.mlob_venv_rewards(venv.h, rew.data_ptr()))
+        E._check(L.mlob_venv_dones(venv.h, dn.data_ptr()))
+        for ty in range(cfg.n_specs):
+            E._check(L.mlob_venv_gather(venv.h, ty, obs_bufs[ty].data_ptr(), rs.data_ptr()))
+    torch.cuda.synchronize()
+    e_wall = torch.tensor([time.perf_counter() - w0], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e_wall, op=dist.ReduceOp.MAX)
+    e_msgs = msgs_all / args.steps * e_steps  # same per-step message volume
+    h2d = acts.numel() * 4
+    d2h = rew.numel() * 8 + dn.numel() + sum(b.numel() * 8 for b in obs_bufs) + \
+        sum(venv.n_streams(t) for t in range(cfg.n_specs))
+    e2e_val = e_msgs / float(e_wall.item())
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peak, peak_kind = peaks()
+    bmsg = B_MSG.get(args.workload, 169.1)
+    per_launch_msgs = msgs / max(1, args.steps)          # this rank's launch
+    avg_launch_s = ms / 1e3 / max(1, launches)
+    achieved = bmsg * per_launch_msgs / avg_launch_s / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            prof = json.load(f)
+        traffic = prof["dram_bytes_per_msg"] * per_launch_msgs
+    except Exception:
+        pass
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+           "config": {"workload": label, "n_envs": n_total, "envs_per_gpu": n_local,
+                      "agents_per_env": A, "messages_per_step": cfg.messages_per_step,
+                      "steps_per_episode": cfg.steps_per_episode,
+                      "book_capacity": cfg.book_capacity, "parallelism": f"env-shard x{world}",
+                      "l2": "inputs larger than L2 (book state of all envs >> 126 MB)",
+                      "store_messages": int(synth.n_messages), "store_gen_s": round(gen_s, 2)},
+           "env_steps_per_s": env_steps,
+           "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                        "frac": achieved / peak, "traffic": traffic,
+                        "bytes_per_msg": bmsg, "peak_kind": peak_kind},
+           "gpu_launches": launches,
+           "clocks": clocks.summary(),
+           "episode_stats": {"episodes": float(stats[4].item())},
+           "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": d2h, "steps": e_steps}}
+    if world == 1 and not args.no_cpu:
+        try:
+            row, workers, n, _ = cpu_reference_run(args.ref_envs, args.cpu_steps, 2, args.workload)
+            out["cpu_baseline"] = {"value": row.messages_per_sec, "unit": UNIT, "cores": workers,
+                                   "kind": "reference",
+                                   "sample": f"{n} envs x {args.cpu_steps} timed steps (+2 warm-up), "
+                                             f"bench::run_throughput, {workers} threads, "
+                                             f"wall {row.wall_seconds:.2f}s"}
+        except Exception as e:  # reported, not fatal
+            out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                                   "sample": f"unavailable: {e}"}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--workload", default="E", choices=["B", "C", "E"])
+    p.add_argument("--envs", type=int, default=0, help="override the env count")
+    p.add_argument("--ref-envs", type=int, default=65536)
+    p.add_argument("--cpu-steps", type=int, default=8)
+    p.add_argument("--e2e-steps", type=int, default=10)
+    p.add_argument("--no-cpu", action="store_true")
+    args = p.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()
