@@ -1,0 +1,1256 @@
+// mlob_step.cuh — the warp-per-environment state machine (K1+K2+K3 device code).
+//
+// One warp owns one environment for a whole step:
+//   * the env's book is loaded from HBM into registers (SoA rows of 32 slots,
+//     lane l owns slots l, l+32, ...), processed, and stored back;
+//   * the step's replay slice is staged global->shared with cp.async.bulk
+//     (TMA bulk copy, mbarrier completion), overlapped with the book load and
+//     the agent-order generation;
+//   * every book operation is warp-cooperative: best price / oldest order by
+//     redux.sync min/max, order-id lookup by ballot, free-slot search by ballot;
+//   * step outcomes (rewards, infos, L2 top-D, observations) are computed in the
+//     same launch; terminal envs are reset in place (MarketVecEnv auto-reset).
+// The per-message loop is kept small (one copy shared by agent and replay
+// messages, runtime side, per-side code only in tiny scan primitives, agent
+// fill attribution deferred to a non-inlined routine): the v0 kernel was
+// instruction-cache bound (profiles/r1_v0_step_kernel_ncu.md).
+// Reference semantics followed (paths under /root/reference/proj/include/marlob):
+//   lob/book.hpp:65-220, env/env.hpp:143-503, agents/*.hpp, core/rng.hpp,
+//   ippo/rollout.hpp:290-318, bench/bench.hpp:53-70.
+// Compiled with --fmad=false so every double expression rounds exactly like
+// the reference's x86-64 build (no FMA contraction).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "mlob_dev.h"
+
+namespace mlob {
+
+#define FULLMASK 0xffffffffu
+
+// ---------------------------------------------------------------------------
+// core/rng.hpp:11-61
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += kGamma;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t key_fold(uint64_t h, uint64_t w) {
+  return splitmix64(h ^ (w + kGamma + (h << 6) + (h >> 2)));
+}
+struct Rng {
+  uint64_t s;
+  __device__ __forceinline__ uint64_t next() {
+    s += kGamma;
+    return splitmix64(s);
+  }
+  __device__ __forceinline__ uint64_t below(uint64_t n) { return next() % n; }
+  __device__ __forceinline__ bool coin() { return (next() & 1ull) != 0; }
+};
+enum : uint64_t { kRngShuffle = 1, kRngTaskDir = 2, kRngBenchAction = 7 };
+
+// ---------------------------------------------------------------------------
+// Book side held in registers: SPL rows of 32 slots (lane-major).
+// Empty slot: q == 0, p == side sentinel (bid INT_MIN, ask INT_MAX), st == ~0.
+// st = arrival_seq << 8 | trader_id, so a u32 min over st is a min over seq.
+template <int SPL>
+struct RegSide {
+  int32_t p_[SPL], q_[SPL];
+  uint32_t lo_[SPL], hi_[SPL], st_[SPL];
+  __device__ __forceinline__ int32_t P(int k) const { return p_[k]; }
+  __device__ __forceinline__ int32_t Q(int k) const { return q_[k]; }
+  __device__ __forceinline__ uint32_t LO(int k) const { return lo_[k]; }
+  __device__ __forceinline__ uint32_t HI(int k) const { return hi_[k]; }
+  __device__ __forceinline__ uint32_t ST(int k) const { return st_[k]; }
+  __device__ __forceinline__ void put(int k, int32_t p, int32_t q, uint32_t lo, uint32_t hi,
+                                      uint32_t st) {
+    p_[k] = p;
+    q_[k] = q;
+    lo_[k] = lo;
+    hi_[k] = hi;
+    st_[k] = st;
+  }
+  // dynamic-index access through select chains (no local memory)
+  __device__ __forceinline__ void get_pq(int k, int32_t& p, int32_t& q) const {
+    p = p_[0];
+    q = q_[0];
+#pragma unroll
+    for (int kk = 1; kk < SPL; ++kk)
+      if (k == kk) {
+        p = p_[kk];
+        q = q_[kk];
+      }
+  }
+  __device__ __forceinline__ void get_qid(int k, int32_t& q, uint32_t& lo, uint32_t& hi) const {
+    q = q_[0];
+    lo = lo_[0];
+    hi = hi_[0];
+#pragma unroll
+    for (int kk = 1; kk < SPL; ++kk)
+      if (k == kk) {
+        q = q_[kk];
+        lo = lo_[kk];
+        hi = hi_[kk];
+      }
+  }
+  __device__ __forceinline__ void set(int k, bool pred, int32_t p, int32_t q, uint32_t lo,
+                                      uint32_t hi, uint32_t st) {
+#pragma unroll
+    for (int kk = 0; kk < SPL; ++kk)
+      if (pred && k == kk) put(kk, p, q, lo, hi, st);
+  }
+  __device__ __forceinline__ void setq(int k, bool pred, int32_t q) {
+#pragma unroll
+    for (int kk = 0; kk < SPL; ++kk)
+      if (pred && k == kk) q_[kk] = q;
+  }
+  __device__ __forceinline__ void clear(int k, bool pred, int32_t empty_p) {
+#pragma unroll
+    for (int kk = 0; kk < SPL; ++kk)
+      if (pred && k == kk) {
+        p_[kk] = empty_p;
+        q_[kk] = 0;
+        st_[kk] = kEmptySt;
+      }
+  }
+};
+
+template <int S>
+__device__ __forceinline__ int32_t empty_price() {
+  return S == 0 ? INT_MIN : INT_MAX;
+}
+template <int S>
+__device__ __forceinline__ int32_t better_of(int32_t a, int32_t b) {
+  return S == 0 ? max(a, b) : min(a, b);
+}
+template <int S>
+__device__ __forceinline__ int32_t redux_best(int32_t v) {
+  return S == 0 ? __reduce_max_sync(FULLMASK, v) : __reduce_min_sync(FULLMASK, v);
+}
+
+// Per-agent per-step accumulators (fills of this step, env.hpp:222, 381-396).
+struct StepAcc {
+  double slip;     // slippage(fills, p_init, dir) accumulated in fill order
+  int64_t filled;  // Σ qty
+  int64_t sq[2];   // Σ qty by side (MM reward fallback beyond kFillLog fills)
+  int64_t spq[2];  // Σ price*qty by side
+  int32_t count;
+  int32_t _pad;
+};
+struct FillEnt {  // exact per-env fill log for the MM rewards (rewards.hpp:22-36)
+  int32_t price;
+  int32_t qty;
+  int32_t agent;
+  int32_t side;
+};
+struct L2Lvl {
+  int32_t price;
+  int32_t _pad;
+  int64_t qty;
+};
+
+struct WarpSmem {
+  DevMsg* chunk[2];
+  uint64_t* bar;  // 2 mbarriers
+  DevMsg* amsg;   // agent messages (<= 4 * A)
+  AgentRec* ag;
+  ActiveRec* act;
+  StepAcc* acc;
+  FillEnt* fills;
+  int32_t* scal;  // [0] fill-log count, [1] fill-log overflow
+  L2Lvl* l2;      // [2][obs_depth]
+  double* obs;    // staging, max_obs_dim
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  const uint32_t b = smem_u32(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// env.hpp:372-396 (attribute_trade -> apply_fill for the passive, then the
+// aggressor agent); executed by lane 0 only, in fill order.  Agent state is
+// not read inside the message loop, so the other lanes see it after the
+// loop's closing __syncwarp.
+__device__ __forceinline__ void attribute_fill(const DevCfg* cfg, WarpSmem sm, int32_t price,
+                                               int32_t qty, int ptrader, int atrader, int aside) {
+  for (int r = 0; r < 2; ++r) {
+    const int trader = r == 0 ? ptrader : atrader;
+    if (trader <= 0 || trader > cfg->n_agents) continue;
+    const int a = trader - 1;
+    const int side = r == 0 ? 1 - aside : aside;
+    const DevSpec& sp = cfg->specs[cfg->flat_spec[a]];
+    AgentRec& st = sm.ag[a];
+    StepAcc& ac = sm.acc[a];
+    const int64_t pq = static_cast<int64_t>(price) * qty;
+    if (side == MLOB_BID) {
+      st.inventory += qty;
+      st.cash -= pq;
+    } else {
+      st.inventory -= qty;
+      st.cash += pq;
+    }
+    st.filled_total += qty;
+    if (sp.type == MLOB_EXECUTOR) {
+      const bool task_side = (st.task_dir == MLOB_TASK_BUY) == (side == MLOB_BID);
+      if (task_side) st.task_remaining = max(static_cast<int64_t>(0), st.task_remaining - qty);
+    }
+    // slippage term, rewards.hpp:69-75: (sign * q) * (price - p_init)
+    const double sign = st.task_dir == MLOB_TASK_BUY ? 1.0 : -1.0;
+    ac.slip += sign * static_cast<double>(qty) * (static_cast<double>(price) - st.p_init);
+    ac.filled += qty;
+    ac.count += 1;
+    ac.sq[side] += qty;
+    ac.spq[side] += pq;
+    const int nf = sm.scal[0];
+    if (nf < kFillLog) {
+      sm.fills[nf] = FillEnt{price, qty, a, side};
+      sm.scal[0] = nf + 1;
+    } else {
+      sm.scal[1] = 1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <int SPL>
+struct WarpEnv {
+  using SideT = RegSide<SPL>;
+  SideT bid, ask;
+  const KParams& kp;
+  const DevCfg& cfg;
+  WarpSmem sm;
+  int lane;
+  uint64_t env, genv, seed;
+  // uniform state (identical in every lane)
+  int live0, live1;
+  int32_t best0, best1;
+  uint32_t next_seq;
+  int64_t mid_half, prev_mid_half, last_bid, last_ask, last_time;
+  double mbar;
+  uint64_t episode, msgs, cursor;
+  int64_t ep_finished;
+  int step;
+  bool terminal;
+  int64_t mid_sum, mid_count;
+  uint32_t n_trades;
+  uint32_t err;
+
+  __device__ WarpEnv(const KParams& p, const WarpSmem& s, uint64_t e, int ln)
+      : kp(p), cfg(p.cfg), sm(s), lane(ln), env(e) {
+    genv = kp.env_index ? kp.env_index[e] : kp.env_index_base + e;
+    seed = kp.env_seed ? kp.env_seed[e] : kp.seed;
+    err = 0;
+  }
+
+  template <int S>
+  __device__ __forceinline__ SideT& sd() {
+    if constexpr (S == 0)
+      return bid;
+    else
+      return ask;
+  }
+
+  // ---- HBM <-> registers --------------------------------------------------
+  __device__ __forceinline__ size_t row_index(int s, int k) const {
+    return ((env * 2 + static_cast<uint64_t>(s)) * SPL + static_cast<uint64_t>(k)) * kWarp + lane;
+  }
+  template <int S>
+  __device__ __forceinline__ void load_side(int hwm) {
+    SideT& d = sd<S>();
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      if (k * kWarp < hwm) {
+        const size_t i = row_index(S, k);
+        const uint2 id = kp.bk_id[i];
+        d.put(k, kp.bk_p[i], kp.bk_q[i], id.x, id.y, kp.bk_st[i]);
+      } else {
+        d.put(k, empty_price<S>(), 0, 0, 0, kEmptySt);
+      }
+    }
+  }
+  template <int S>
+  __device__ __forceinline__ int store_side() {
+    SideT& d = sd<S>();
+    int hwm = 0;
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      const uint32_t b = __ballot_sync(FULLMASK, d.Q(k) > 0);
+      if (b) hwm = k * kWarp + 32 - __clz(b);
+    }
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      if (k * kWarp < hwm) {
+        const size_t i = row_index(S, k);
+        kp.bk_p[i] = d.P(k);
+        kp.bk_q[i] = d.Q(k);
+        kp.bk_id[i] = make_uint2(d.LO(k), d.HI(k));
+        kp.bk_st[i] = d.ST(k);
+      }
+    }
+    return hwm;
+  }
+
+  __device__ void load_hdr() {
+    const EnvHdr& h = kp.hdr[env];
+    mid_half = h.mid_half;
+    prev_mid_half = h.prev_mid_half;
+    mbar = h.mbar;
+    last_bid = h.last_bid;
+    last_ask = h.last_ask;
+    last_time = h.last_time;
+    episode = h.episode;
+    msgs = h.msgs_processed;
+    cursor = h.cursor;
+    ep_finished = h.episodes_finished;
+    next_seq = h.next_seq;
+    step = h.step;
+    live0 = h.live[0];
+    live1 = h.live[1];
+    best0 = h.best[0];
+    best1 = h.best[1];
+    terminal = h.terminal != 0;
+    n_trades = h.n_trades;
+  }
+  __device__ void load_book() {
+    const EnvHdr& h = kp.hdr[env];
+    load_side<0>(h.hwm[0]);
+    load_side<1>(h.hwm[1]);
+  }
+  __device__ void store_all(uint8_t just_reset) {
+    const int h0 = store_side<0>();
+    const int h1 = store_side<1>();
+    if (lane == 0) {
+      EnvHdr h;
+      h.mid_half = mid_half;
+      h.prev_mid_half = prev_mid_half;
+      h.mbar = mbar;
+      h.last_bid = last_bid;
+      h.last_ask = last_ask;
+      h.last_time = last_time;
+      h.episode = episode;
+      h.msgs_processed = msgs;
+      h.cursor = cursor;
+      h.episodes_finished = ep_finished;
+      h.next_seq = next_seq;
+      h.step = step;
+      h.live[0] = static_cast<uint16_t>(live0);
+      h.live[1] = static_cast<uint16_t>(live1);
+      h.hwm[0] = static_cast<uint16_t>(h0);
+      h.hwm[1] = static_cast<uint16_t>(h1);
+      h.best[0] = best0;
+      h.best[1] = best1;
+      h.n_trades = n_trades;
+      h.terminal = terminal ? 1 : 0;
+      h.just_reset = just_reset;
+      h._pad8[0] = h._pad8[1] = 0;
+      h._pad64[0] = h._pad64[1] = 0;
+      kp.hdr[env] = h;
+      kp.just_reset[env] = just_reset;
+    }
+    const int A = cfg.n_agents;
+    const int words = A * static_cast<int>(sizeof(AgentRec) / 8);
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(sm.ag);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(kp.agents + env * A);
+    for (int i = lane; i < words; i += kWarp) dst[i] = src[i];
+    for (int a = 0; a < A; ++a) {
+      const int n = sm.ag[a].n_active;
+      if (lane < n) kp.active[(env * A + a) * kMaxActive + lane] = sm.act[a * kMaxActive + lane];
+    }
+    if (err && lane == 0) atomicOr(kp.error, err);
+  }
+  __device__ void load_agents() {
+    const int A = cfg.n_agents;
+    const int words = A * static_cast<int>(sizeof(AgentRec) / 8);
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(kp.agents + env * A);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(sm.ag);
+    for (int i = lane; i < words; i += kWarp) dst[i] = src[i];
+    __syncwarp();
+    for (int a = 0; a < A; ++a) {
+      const int n = sm.ag[a].n_active;
+      if (lane < n) sm.act[a * kMaxActive + lane] = kp.active[(env * A + a) * kMaxActive + lane];
+    }
+    __syncwarp();
+  }
+
+  // ---- per-side scan primitives (the only side-specialised hot code) ------
+  template <int S>
+  __device__ __forceinline__ int32_t side_best_t() {
+    SideT& d = sd<S>();
+    int32_t b = d.P(0);
+#pragma unroll
+    for (int k = 1; k < SPL; ++k) b = better_of<S>(b, d.P(k));
+    return redux_best<S>(b);
+  }
+  // lane-local oldest slot (min st) at `price`
+  template <int S>
+  __device__ __forceinline__ void scan_oldest_t(int32_t price, uint32_t& m, int& lk) {
+    SideT& d = sd<S>();
+    m = kEmptySt;
+    lk = 0;
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      const bool c = d.P(k) == price && d.ST(k) < m;
+      m = c ? d.ST(k) : m;
+      lk = c ? k : lk;
+    }
+  }
+  // lane-local id match: first matching row and match count
+  template <int S>
+  __device__ __forceinline__ void scan_id_t(uint32_t lo, uint32_t hi, int& nm, int& lk) {
+    SideT& d = sd<S>();
+    nm = 0;
+    lk = 0;
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      const bool c = d.Q(k) > 0 && d.LO(k) == lo && d.HI(k) == hi;
+      lk = (c && nm == 0) ? k : lk;
+      nm += c ? 1 : 0;
+    }
+  }
+  // lowest free position: (row, lane)
+  template <int S>
+  __device__ __forceinline__ void free_slot_t(int& pk, int& pl) {
+    SideT& d = sd<S>();
+    pk = -1;
+    pl = 0;
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      const uint32_t b = __ballot_sync(FULLMASK, d.Q(k) == 0);
+      if (pk < 0 && b) {
+        pk = k;
+        pl = __ffs(b) - 1;
+      }
+    }
+  }
+  __device__ __forceinline__ void slot_get_pq(int s, int k, int32_t& p, int32_t& q) const {
+    if (s)
+      ask.get_pq(k, p, q);
+    else
+      bid.get_pq(k, p, q);
+  }
+  __device__ __forceinline__ void slot_get_qid(int s, int k, int32_t& q, uint32_t& lo, uint32_t& hi) const {
+    if (s)
+      ask.get_qid(k, q, lo, hi);
+    else
+      bid.get_qid(k, q, lo, hi);
+  }
+  __device__ __forceinline__ void slot_setq(int s, int k, bool pred, int32_t q) {
+    if (s)
+      ask.setq(k, pred, q);
+    else
+      bid.setq(k, pred, q);
+  }
+  __device__ __forceinline__ void slot_clear(int s, int k, bool pred) {
+    if (s)
+      ask.clear(k, pred, INT_MAX);
+    else
+      bid.clear(k, pred, INT_MIN);
+  }
+
+  // Eviction on a full side (book.hpp:174-181): drop the newcomer unless it
+  // improves on the worst price, else remove the oldest order at the worst.
+  template <int S>
+  __device__ __forceinline__ bool evict_t(int32_t price) {
+    SideT& d = sd<S>();
+    int32_t lw = S == 0 ? INT_MAX : INT_MIN;
+#pragma unroll
+    for (int k = 0; k < SPL; ++k)
+      if (d.Q(k) > 0) lw = S == 0 ? min(lw, d.P(k)) : max(lw, d.P(k));
+    const int32_t worst = S == 0 ? __reduce_min_sync(FULLMASK, lw) : __reduce_max_sync(FULLMASK, lw);
+    const bool better = S == 0 ? price > worst : price < worst;
+    if (!better) return false;
+    uint32_t m;
+    int lk;
+    scan_oldest_t<S>(worst, m, lk);
+    const uint32_t g = __reduce_min_sync(FULLMASK, m);
+    const int owner = __ffs(__ballot_sync(FULLMASK, m == g)) - 1;
+    d.clear(lk, lane == owner, empty_price<S>());
+    return true;
+  }
+  // Duplicate live ids: the reference takes the first match in storage order
+  // (book.hpp:191-206; bids: lowest price then newest; asks: highest, newest).
+  template <int S>
+  __device__ __forceinline__ int dup_owner_t(uint32_t lo, uint32_t hi, int& lk) {
+    SideT& d = sd<S>();
+    int32_t kp_ = S == 0 ? INT_MAX : INT_MIN;
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      const bool c = d.Q(k) > 0 && d.LO(k) == lo && d.HI(k) == hi;
+      if (c) kp_ = S == 0 ? min(kp_, d.P(k)) : max(kp_, d.P(k));
+    }
+    const int32_t gp = S == 0 ? __reduce_min_sync(FULLMASK, kp_) : __reduce_max_sync(FULLMASK, kp_);
+    uint32_t ms = 0;
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      const bool c = d.Q(k) > 0 && d.LO(k) == lo && d.HI(k) == hi && d.P(k) == gp;
+      if (c && (!any || d.ST(k) > ms)) {
+        ms = d.ST(k);
+        lk = k;
+        any = true;
+      }
+    }
+    const uint32_t gs = __reduce_max_sync(FULLMASK, any ? ms : 0u);
+    return __ffs(__ballot_sync(FULLMASK, any && ms == gs)) - 1;
+  }
+
+  // ---- message handlers (runtime side) -------------------------------------
+  __device__ __forceinline__ void record_trade(int32_t price, int32_t qty, const DevMsg& m,
+                                               uint32_t lo, uint32_t hi, uint32_t st, int aside) {
+    if ((kp.flags & MLOB_VENV_RECORD_TRADES) && lane == 0 && n_trades < kp.trade_cap) {
+      mlob_trade t;
+      t.price = price;
+      t.quantity = qty;
+      t.time = m.time;
+      t.passive_order_id = (static_cast<uint64_t>(hi) << 32) | lo;
+      t.aggressor_order_id = m.order_id;
+      t.passive_trader_id = static_cast<int32_t>(st & 0xffu);
+      t.aggressor_trader_id = m.trader;
+      t.aggressor_side = static_cast<uint8_t>(aside);
+#pragma unroll
+      for (int i = 0; i < 7; ++i) t._pad[i] = 0;
+      kp.trades[env * kp.trade_cap + n_trades] = t;
+    }
+    ++n_trades;
+    const uint32_t pt = st & 0xffu;
+    if ((pt | static_cast<uint32_t>(m.trader)) && lane == 0)  // an agent is involved
+      attribute_fill(&cfg, sm, price, qty, static_cast<int>(pt), m.trader, aside);
+  }
+
+  // book.hpp:150-187 (process_new_limit + rest_order)
+  __device__ __forceinline__ void new_limit(const DevMsg& m) {
+    const int s = m.side, o = s ^ 1;
+    int32_t rem = m.qty;
+    const bool pass_ids = (kp.flags & MLOB_VENV_RECORD_TRADES) != 0;
+    while (rem > 0) {
+      const int lo_ = o ? live1 : live0;
+      const int32_t bp = o ? best1 : best0;
+      if (lo_ == 0 || (s == 0 ? bp > m.price : bp < m.price)) break;
+      uint32_t lm;
+      int lk;
+      if (o)
+        scan_oldest_t<1>(bp, lm, lk);
+      else
+        scan_oldest_t<0>(bp, lm, lk);
+      const uint32_t gst = __reduce_min_sync(FULLMASK, lm);
+      const int owner = __ffs(__ballot_sync(FULLMASK, lm == gst)) - 1;
+      int32_t q;
+      uint32_t idlo, idhi;
+      slot_get_qid(o, lk, q, idlo, idhi);
+      q = __shfl_sync(FULLMASK, q, owner);
+      if (pass_ids) {
+        idlo = __shfl_sync(FULLMASK, idlo, owner);
+        idhi = __shfl_sync(FULLMASK, idhi, owner);
+      }
+      const int32_t fill = min(rem, q);
+      const bool me = lane == owner;
+      rem -= fill;
+      if (fill == q) {
+        slot_clear(o, lk, me);
+        if (o) {
+          if (--live1 > 0) best1 = side_best_t<1>();
+        } else {
+          if (--live0 > 0) best0 = side_best_t<0>();
+        }
+      } else {
+        slot_setq(o, lk, me, q - fill);
+      }
+      record_trade(bp, fill, m, idlo, idhi, gst, s);
+    }
+    if (rem <= 0) return;
+    // rest_order
+    if ((s ? live1 : live0) == cfg.capacity) {
+      const bool ev = s ? evict_t<1>(m.price) : evict_t<0>(m.price);
+      if (!ev) return;  // newcomer dropped: no sequence number consumed
+      if (s)
+        --live1;
+      else
+        --live0;
+    }
+    const uint32_t seq = next_seq++;
+    if (seq >= kMaxSeq) err |= kErrSeqRange;
+    int pk, pl;
+    if (s)
+      free_slot_t<1>(pk, pl);
+    else
+      free_slot_t<0>(pk, pl);
+    const uint32_t st = (seq << 8) | static_cast<uint32_t>(m.trader & 0xff);
+    const uint32_t ilo = static_cast<uint32_t>(m.order_id), ihi = static_cast<uint32_t>(m.order_id >> 32);
+    if (s) {
+      ask.set(pk, lane == pl, m.price, rem, ilo, ihi, st);
+      best1 = ++live1 == 1 ? m.price : min(best1, m.price);
+    } else {
+      bid.set(pk, lane == pl, m.price, rem, ilo, ihi, st);
+      best0 = ++live0 == 1 ? m.price : max(best0, m.price);
+    }
+  }
+
+  // book.hpp:189-207 (reduce_order / remove_order); absent ids are no-ops.
+  __device__ __forceinline__ void by_id(const DevMsg& m, bool remove) {
+    const int s = m.side;
+    const uint32_t lo = static_cast<uint32_t>(m.order_id), hi = static_cast<uint32_t>(m.order_id >> 32);
+    int nm, lk;
+    if (s)
+      scan_id_t<1>(lo, hi, nm, lk);
+    else
+      scan_id_t<0>(lo, hi, nm, lk);
+    const uint32_t b = __ballot_sync(FULLMASK, nm > 0);
+    if (b == 0) return;
+    int owner = __ffs(b) - 1;
+    if (__reduce_add_sync(FULLMASK, static_cast<uint32_t>(nm)) != 1)
+      owner = s ? dup_owner_t<1>(lo, hi, lk) : dup_owner_t<0>(lo, hi, lk);
+    int32_t p, q;
+    slot_get_pq(s, lk, p, q);
+    p = __shfl_sync(FULLMASK, p, owner);
+    q = __shfl_sync(FULLMASK, q, owner);
+    const int32_t nq = remove ? 0 : q - min(q, m.qty);
+    const bool me = lane == owner;
+    if (nq == 0) {
+      slot_clear(s, lk, me);
+      if (s) {
+        if (--live1 > 0 && p == best1) best1 = side_best_t<1>();
+      } else {
+        if (--live0 > 0 && p == best0) best0 = side_best_t<0>();
+      }
+    } else {
+      slot_setq(s, lk, me, nq);
+    }
+  }
+
+  // book.hpp:65-86 + env.hpp:223-235
+  __device__ __forceinline__ void run_message(const DevMsg& m) {
+    if (m.kind == MLOB_NEW_LIMIT) {
+      if (m.qty > 0) new_limit(m);
+    } else if (m.kind <= MLOB_EXECUTE_VISIBLE) {
+      by_id(m, m.kind == MLOB_DELETE);
+    }
+    const bool hb = live0 > 0, ha = live1 > 0;
+    const int64_t b0 = best0, b1 = best1;
+    mid_half = hb ? (ha ? b0 + b1 : 2 * b0) : (ha ? 2 * b1 : mid_half);
+    mid_sum += mid_half;
+    ++mid_count;
+    last_time = m.time;
+  }
+
+  // Agent messages, then the replay slice staged in smem chunks (env.hpp:236-237).
+  __device__ void process_messages(int n_amsg, const DevMsg* slice) {
+    const int mps = cfg.mps;
+    const int total = n_amsg + mps;
+    const int nch = (mps + kChunk - 1) / kChunk;
+    const DevMsg* buf = sm.amsg;
+    int base = 0;  // index of buf[0] in the combined sequence
+    for (int i = 0; i < total; ++i) {
+      if (i >= n_amsg && (i - n_amsg) % kChunk == 0) {
+        const int c = (i - n_amsg) / kChunk;
+        if (c >= 1 && c + 1 < nch) {  // chunk c-1 consumed: refill its buffer with chunk c+1
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const int nb = (c + 1) & 1;
+            const int n2 = min(kChunk, mps - (c + 1) * kChunk);
+            bulk_copy(sm.chunk[nb], slice + (c + 1) * kChunk, static_cast<uint32_t>(n2 * sizeof(DevMsg)),
+                      &sm.bar[nb]);
+          }
+        }
+        bar_wait(&sm.bar[c & 1], static_cast<uint32_t>((c >> 1) & 1));
+        buf = sm.chunk[c & 1];
+        base = i;
+      }
+      const DevMsg m = buf[i - base];
+      run_message(m);
+    }
+    msgs += static_cast<uint64_t>(total);
+    __syncwarp();  // lane 0's agent updates become visible to the warp
+  }
+
+  // ---- agents (agents/actions.hpp, env.hpp:266-370) ----------------------
+  __device__ __forceinline__ void effective_tops(const DevSpec& p, int64_t& bid_, int64_t& ask_) const {
+    const int64_t mid_floor = mid_half >= 0 ? mid_half / 2 : (mid_half - 1) / 2;
+    const int64_t mid_ceil = (mid_half + 1) / 2;
+    bid_ = live0 > 0 ? static_cast<int64_t>(best0) : mid_floor - p.default_half_spread;
+    ask_ = live1 > 0 ? static_cast<int64_t>(best1) : mid_ceil + p.default_half_spread;
+    if (bid_ < 1) bid_ = 1;
+    if (ask_ <= bid_) ask_ = bid_ + 1;
+  }
+
+  struct Quotes {  // agents::QuoteList (actions.hpp:24-40), no dynamic indexing
+    int n;
+    int s0, s1;
+    int64_t p0, p1, q0, q1;
+    __device__ void push(int s, int64_t p, int64_t q) {
+      if (n == 0) {
+        s0 = s;
+        p0 = p;
+        q0 = q;
+      } else {
+        s1 = s;
+        p1 = p;
+        q1 = q;
+      }
+      ++n;
+    }
+    __device__ void finish_two_sided() {  // actions.hpp:47-56
+      if (n >= 1 && p0 < 1) p0 = 1;
+      if (n >= 2 && p1 < 1) p1 = 1;
+      if (n == 2) {
+        const bool a0 = s0 == MLOB_ASK;  // ask = items[0] if it is an ask, else items[1]
+        const int64_t bp = s0 == MLOB_BID ? p0 : p1;
+        const int64_t ap = a0 ? p0 : p1;
+        if (bp >= ap) {
+          if (a0)
+            p0 = bp + 1;
+          else
+            p1 = bp + 1;
+        }
+      }
+    }
+  };
+
+  __device__ void decode(int a, int id, Quotes& q) {
+    const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
+    const AgentRec& st = sm.ag[a];
+    int64_t bb, ba;
+    effective_tops(sp, bb, ba);
+    q.n = 0;
+    if (sp.type == MLOB_EXECUTOR) {  // env.hpp:302-311, actions.hpp:193-224
+      int64_t eb = bb, ea = ba;
+      if (st.task_dir == MLOB_TASK_BUY && live1 == 0) ea = max(static_cast<int64_t>(2), last_ask + 1);
+      if (st.task_dir == MLOB_TASK_SELL && live0 == 0) eb = max(static_cast<int64_t>(1), last_bid - 1);
+      const int pi = id % 4, mi = id / 4;
+      const int64_t spread = ea - eb;
+      int64_t price;
+      if (st.task_dir == MLOB_TASK_BUY)
+        price = pi == 0 ? ea : pi == 1 ? eb : pi == 2 ? eb - 1 : eb + spread / 2;
+      else
+        price = pi == 0 ? eb : pi == 1 ? ea : pi == 2 ? ea + 1 : ea - spread / 2;
+      int64_t qty = sp.order_size * (mi == 0 ? 1 : mi == 1 ? 2 : 5);
+      if (qty > st.task_remaining) qty = st.task_remaining;
+      if (qty > 0) q.push(st.task_dir == MLOB_TASK_BUY ? MLOB_BID : MLOB_ASK, price < 1 ? 1 : price, qty);
+    } else if (sp.type == MLOB_DIRECTIONAL) {  // actions.hpp:227-235
+      if (id == 1) q.push(MLOB_BID, bb < 1 ? 1 : bb, sp.order_size);
+      if (id == 2) q.push(MLOB_ASK, ba < 1 ? 1 : ba, sp.order_size);
+    } else if (sp.mm_space == MLOB_FIXED_QUANT) {  // actions.hpp:66-108
+      const int64_t br = sp.fixed_quant_from_mid ? (bb + ba) / 2 : bb;
+      const int64_t ar = sp.fixed_quant_from_mid ? (bb + ba + 1) / 2 : ba;
+      const int64_t sz = sp.order_size;
+      if (id != 0) {
+        const int64_t pb = id == 1 ? br - 2 : id == 2 ? br - 4 : id == 3 ? bb + 1 : id == 4 ? br - 2
+                         : id == 5 ? bb : id == 6 ? bb - 5 : bb + 1;
+        const int64_t pa = id == 1 ? ar + 2 : id == 2 ? ar + 4 : id == 3 ? ba - 1 : id == 4 ? ba
+                         : id == 5 ? ar + 2 : id == 6 ? ba - 1 : ba + 5;
+        q.push(MLOB_BID, pb, sz);
+        q.push(MLOB_ASK, pa, sz);
+      }
+      q.finish_two_sided();
+    } else if (sp.mm_space == MLOB_SPREAD_SKEW) {  // actions.hpp:128-140
+      const int64_t hs = sp.ss_half[id], sk = sp.ss_skew[id];
+      const int64_t bh = mid_half - 2 * hs + 2 * sk;
+      const int64_t ah = mid_half + 2 * hs + 2 * sk;
+      q.push(MLOB_BID, bh >= 0 ? bh / 2 : (bh - 1) / 2, sp.order_size);
+      q.push(MLOB_ASK, (ah + 1) / 2, sp.order_size);
+      q.finish_two_sided();
+    } else {  // AvSt, actions.hpp:151-178
+      const double gamma = sp.gamma[id];
+      const double rem = sp.horizon - static_cast<double>(step);
+      const double ttg = 0.0 < rem ? rem : 0.0;
+      const double mid_ticks = static_cast<double>(mid_half) / 2.0;
+      const double reservation =
+          mid_ticks - static_cast<double>(st.inventory) * gamma * sp.sigma * sp.sigma * ttg;
+      const double half_spread = 0.5 * (gamma * sp.sigma * sp.sigma * ttg + sp.avst_term[id]);
+      q.push(MLOB_BID, static_cast<int64_t>(floor(reservation - half_spread)), sp.order_size);
+      q.push(MLOB_ASK, static_cast<int64_t>(ceil(reservation + half_spread)), sp.order_size);
+      q.finish_two_sided();
+    }
+  }
+
+  __device__ __forceinline__ void push_amsg(int& n_amsg, int64_t time, uint64_t id, int64_t price,
+                                            int64_t qty, int kind, int side, int trader) {
+    if (lane == 0) {
+      DevMsg m;
+      m.time = time;
+      m.order_id = id;
+      m.price = static_cast<int32_t>(price);
+      m.qty = static_cast<int32_t>(qty);
+      m.kind = static_cast<uint8_t>(kind);
+      m.side = static_cast<uint8_t>(side);
+      m._pad = 0;
+      m.trader = trader;
+      sm.amsg[n_amsg] = m;
+    }
+    ++n_amsg;
+  }
+
+  // env.hpp:285-370: quotes -> Delete for stale active orders, NewLimit for
+  // quotes not already resting at the same (side, price).
+  __device__ void convert_action(int a, int64_t step_time, int& n_amsg) {
+    const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
+    AgentRec& st = sm.ag[a];
+    Quotes q;
+    q.n = 0;
+    q.s0 = q.s1 = 0;
+    q.p0 = q.p1 = q.q0 = q.q1 = 0;
+    if (kp.action_mode == kActDirect && kp.action_direct[env * cfg.n_agents + a].direct) {
+      const mlob_agent_action& da = kp.action_direct[env * cfg.n_agents + a];
+      q.n = da.n_quotes;
+      q.s0 = da.quotes[0].side;
+      q.p0 = da.quotes[0].price;
+      q.q0 = da.quotes[0].quantity;
+      q.s1 = da.quotes[1].side;
+      q.p1 = da.quotes[1].price;
+      q.q1 = da.quotes[1].quantity;
+      if (sp.type == MLOB_EXECUTOR) {
+        if (q.n >= 1 && q.q0 > st.task_remaining) q.q0 = st.task_remaining;
+        if (q.n >= 2 && q.q1 > st.task_remaining) q.q1 = st.task_remaining;
+        if (q.n == 1 && q.q0 <= 0) q.n = 0;
+      }
+    } else {
+      int id;
+      if (kp.action_mode == kActBench) {  // bench.hpp:57-60: one rng, one draw per agent in order
+        Rng r{key_fold(key_fold(key_fold(splitmix64(kp.bench_seed), kRngBenchAction), genv),
+                       kp.global_step)};
+        for (int b = 0; b < a; ++b) r.next();
+        id = static_cast<int>(r.below(static_cast<uint64_t>(sp.arity)));
+      } else if (kp.action_mode == kActDirect) {
+        id = kp.action_direct[env * cfg.n_agents + a].id;
+      } else {
+        id = kp.action_ids[env * cfg.n_agents + a];
+      }
+      if (id < 0 || id >= sp.arity) {
+        err |= kErrBadAction;
+        id = 0;
+      }
+      decode(a, id, q);
+    }
+    bool kept0 = false, kept1 = false;
+    const int na = st.n_active;
+    for (int i = 0; i < na; ++i) {
+      const ActiveRec ar = sm.act[a * kMaxActive + i];
+      const int side = static_cast<int>(ar.qty_side >> 31);
+      const bool r0 = q.n >= 1 && q.s0 == side && q.p0 == ar.price;
+      const bool r1 = q.n >= 2 && q.s1 == side && q.p1 == ar.price;
+      kept0 |= r0;
+      kept1 |= r1;
+      if (r0 || r1) continue;
+      push_amsg(n_amsg, step_time, ar.order_id, 0, 0, MLOB_DELETE, side, a + 1);
+    }
+    uint64_t nonce = st.nonce;
+    const uint64_t id_base = cfg.agent_id_base + static_cast<uint64_t>(a) * cfg.agent_id_range;
+    for (int j = 0; j < q.n; ++j) {
+      if (j == 0 ? kept0 : kept1) continue;
+      const int64_t pr = j == 0 ? q.p0 : q.p1, qt = j == 0 ? q.q0 : q.q1;
+      if (pr > INT_MAX - 1 || pr < INT_MIN + 1 || qt > INT_MAX || qt < INT_MIN) err |= kErrPriceRange;
+      push_amsg(n_amsg, step_time, id_base + nonce, pr, qt, MLOB_NEW_LIMIT, j == 0 ? q.s0 : q.s1, a + 1);
+      ++nonce;
+    }
+    __syncwarp();
+    if (lane == 0) st.nonce = nonce;
+  }
+
+  // ---- step outcomes -------------------------------------------------------
+  // Top-D aggregated levels per side, best-first (book.hpp:109-120, 209-220).
+  template <int S>
+  __device__ int l2_levels(L2Lvl* out) {
+    SideT& d = sd<S>();
+    const int D = cfg.obs_depth;
+    int n = 0;
+    int32_t prev = 0;
+    for (; n < D; ++n) {
+      int32_t lb = empty_price<S>();
+#pragma unroll
+      for (int k = 0; k < SPL; ++k) {
+        const bool ok = d.Q(k) > 0 && (n == 0 || (S == 0 ? d.P(k) < prev : d.P(k) > prev));
+        if (ok) lb = better_of<S>(lb, d.P(k));
+      }
+      const int32_t lvl = redux_best<S>(lb);
+      if (lvl == empty_price<S>()) break;
+      // per-lane sum < SPL * 2^31: reduce as 16-bit-split halves so the 32-bit
+      // redux.sync add cannot overflow
+      uint64_t s64 = 0;
+#pragma unroll
+      for (int k = 0; k < SPL; ++k)
+        if (d.P(k) == lvl) s64 += static_cast<uint32_t>(d.Q(k));
+      const uint32_t lo = __reduce_add_sync(FULLMASK, static_cast<uint32_t>(s64 & 0xffffu));
+      const uint32_t hi = __reduce_add_sync(FULLMASK, static_cast<uint32_t>(s64 >> 16));
+      const int64_t tot = static_cast<int64_t>(lo) + (static_cast<int64_t>(hi) << 16);
+      if (lane == 0) out[n] = L2Lvl{lvl, 0, tot};
+      prev = lvl;
+    }
+    __syncwarp();
+    return n;
+  }
+
+  // env.hpp:398-407: active orders per agent, book storage order.
+  __device__ void rebuild_active() {
+    const int A = cfg.n_agents;
+    for (int a = lane; a < A; a += kWarp) sm.ag[a].n_active = 0;
+    __syncwarp();
+    rebuild_side<0>();
+    rebuild_side<1>();
+  }
+  template <int S>
+  __device__ void rebuild_side() {
+    SideT& d = sd<S>();
+    uint32_t taken = 0;  // per-lane bitmask of consumed rows
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) cnt += (d.Q(k) > 0 && (d.ST(k) & 0xffu) != 0) ? 1 : 0;
+    const int total = __reduce_add_sync(FULLMASK, static_cast<uint32_t>(cnt));
+    for (int i = 0; i < total; ++i) {
+      // first in storage order: bids lowest price, asks highest; then newest seq
+      int32_t lp = S == 0 ? INT_MAX : INT_MIN;
+#pragma unroll
+      for (int k = 0; k < SPL; ++k)
+        if (d.Q(k) > 0 && (d.ST(k) & 0xffu) != 0 && !((taken >> k) & 1u))
+          lp = S == 0 ? min(lp, d.P(k)) : max(lp, d.P(k));
+      const int32_t gp = S == 0 ? __reduce_min_sync(FULLMASK, lp) : __reduce_max_sync(FULLMASK, lp);
+      uint32_t ms = 0;
+      int lk = 0;
+      bool any = false;
+#pragma unroll
+      for (int k = 0; k < SPL; ++k) {
+        const bool c = d.Q(k) > 0 && (d.ST(k) & 0xffu) != 0 && !((taken >> k) & 1u) && d.P(k) == gp;
+        if (c && (!any || d.ST(k) > ms)) {
+          ms = d.ST(k);
+          lk = k;
+          any = true;
+        }
+      }
+      const uint32_t gs = __reduce_max_sync(FULLMASK, any ? ms : 0u);
+      const int owner = __ffs(__ballot_sync(FULLMASK, any && ms == gs)) - 1;
+      if (lane == owner) taken |= 1u << lk;
+      int32_t q;
+      uint32_t lo, hi;
+      d.get_qid(lk, q, lo, hi);
+      q = __shfl_sync(FULLMASK, q, owner);
+      lo = __shfl_sync(FULLMASK, lo, owner);
+      hi = __shfl_sync(FULLMASK, hi, owner);
+      const int a = static_cast<int>(gs & 0xffu) - 1;
+      if (a >= cfg.n_agents) {
+        err |= kErrBadTrader;
+        continue;
+      }
+      const int n = sm.ag[a].n_active;
+      if (n >= kMaxActive) {
+        err |= kErrActiveOverflow;
+        continue;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        sm.act[a * kMaxActive + n] =
+            ActiveRec{(static_cast<uint64_t>(hi) << 32) | lo, gp,
+                      static_cast<uint32_t>(q) | (static_cast<uint32_t>(S) << 31)};
+        sm.ag[a].n_active = n + 1;
+      }
+      __syncwarp();
+    }
+  }
+
+  // env.hpp:435-443
+  __device__ double reference_price(const DevSpec& sp, const AgentRec& st) const {
+    if (sp.ref_price == MLOB_REF_MID || st.inventory == 0) return static_cast<double>(mid_half) / 2.0;
+    if (st.inventory > 0) return static_cast<double>(live0 > 0 ? static_cast<int64_t>(best0) : last_bid);
+    return static_cast<double>(live1 > 0 ? static_cast<int64_t>(best1) : last_ask);
+  }
+
+  // env.hpp:445-464 (also accumulates slippage_total); lane 0 writes.
+  __device__ void fill_info(int a) {
+    const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
+    AgentRec& st = sm.ag[a];
+    const StepAcc& ac = sm.acc[a];
+    mlob_agent_info info;
+    info.inventory = st.inventory;
+    info.cash = st.cash;
+    info.portfolio_value =
+        static_cast<double>(st.inventory) * reference_price(sp, st) + static_cast<double>(st.cash);
+    info.slippage_step = sp.type == MLOB_EXECUTOR ? ac.slip : 0.0;
+    const double total = st.slippage_total + info.slippage_step;
+    info.slippage_total = total;
+    info.task_remaining = st.task_remaining;
+    info.step_filled = ac.filled;
+    info.step_fill_count = ac.count;
+    info._pad = 0;
+    __syncwarp();
+    if (lane == 0) {
+      st.slippage_total = total;
+      kp.infos[env * cfg.n_agents + a] = info;
+    }
+    __syncwarp();
+  }
+
+  // env.hpp:409-433 + rewards.hpp
+  __device__ double compute_reward(int a) {
+    const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
+    const AgentRec& st = sm.ag[a];
+    const StepAcc& ac = sm.acc[a];
+    double r = 0.0;
+    if (sp.reward == MLOB_REWARD_EXEC) {
+      r = -ac.slip;
+      if (terminal && st.task_remaining > 0)
+        r -= sp.unfilled_penalty_coef * static_cast<double>(st.task_remaining) * st.p_init;
+    } else {
+      double pb = 0.0, ps = 0.0;
+      const int nf = sm.scal[0];
+      if (!sm.scal[1]) {
+        for (int i = 0; i < nf; ++i) {
+          const FillEnt f = sm.fills[i];
+          if (f.agent == a && f.side == MLOB_BID)
+            pb += (mbar - static_cast<double>(f.price)) * static_cast<double>(f.qty);
+        }
+        for (int i = 0; i < nf; ++i) {
+          const FillEnt f = sm.fills[i];
+          if (f.agent == a && f.side == MLOB_ASK)
+            ps += (static_cast<double>(f.price) - mbar) * static_cast<double>(f.qty);
+        }
+      } else {
+        // exact-rational fallback beyond kFillLog fills in one env-step
+        pb = mbar * static_cast<double>(ac.sq[0]) - static_cast<double>(ac.spq[0]);
+        ps = static_cast<double>(ac.spq[1]) - mbar * static_cast<double>(ac.sq[1]);
+      }
+      if (sp.reward == MLOB_REWARD_BUYSELL) {
+        r = pb + ps;
+      } else {
+        const double mid = static_cast<double>(mid_half) / 2.0;
+        const double prev = static_cast<double>(prev_mid_half) / 2.0;
+        const double psi_inv = static_cast<double>(st.inventory) * (mid - prev);
+        r = pb + ps + psi_inv - (1.0 - sp.lambda) * (0.0 < psi_inv ? psi_inv : 0.0);
+      }
+      if (sp.quadratic_penalty) {
+        const double frac = static_cast<double>(st.inventory) / static_cast<double>(sp.inventory_cap);
+        r -= sp.rho * frac * frac;
+      }
+    }
+    return r * sp.reward_scale;
+  }
+
+  __device__ static double fmin_ref(double a, double x) { return x < a ? x : a; }  // std::min(a, x)
+  __device__ static double qty_feature(int64_t q, int64_t order_size) {
+    return static_cast<double>(q) / static_cast<double>(q + (order_size > 1 ? order_size : 1));
+  }
+  __device__ static double offset_feature(int64_t own, int64_t touch, bool bid_side) {
+    if (own < 0 || touch < 0) return -1.0;
+    const double off = static_cast<double>(bid_side ? touch - own : own - touch);
+    const double lo = -16.0 < off ? off : -16.0;
+    return lo < 16.0 ? lo : 16.0;
+  }
+
+  // env.hpp:466-503, observations.hpp:42-148; features staged in smem by lane
+  // 0 then written by lanes (coalesced).
+  __device__ void build_observation(int a, const L2Lvl* l2b, int nb, const L2Lvl* l2a, int na) {
+    const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
+    const AgentRec& st = sm.ag[a];
+    const int dim = sp.obs_dim;
+    if (lane == 0) {
+      const int64_t bb = live0 > 0 ? best0 : -1;
+      const int64_t ba = live1 > 0 ? best1 : -1;
+      const double time_frac = static_cast<double>(step) / static_cast<double>(cfg.steps_per_episode);
+      int64_t bq = 0, aq = 0;
+      for (int i = 0; i < nb; ++i) bq += l2b[i].qty;
+      for (int i = 0; i < na; ++i) aq += l2a[i].qty;
+      const double imb = bq + aq == 0 ? 0.0 : static_cast<double>(bq - aq) / static_cast<double>(bq + aq);
+      const double spread = (bb < 0 || ba < 0) ? 0.0 : fmin_ref(32.0, static_cast<double>(ba - bb));
+      int64_t own_bid = -1, own_ask = -1;
+      for (int i = 0; i < st.n_active; ++i) {
+        const ActiveRec ar = sm.act[a * kMaxActive + i];
+        if ((ar.qty_side >> 31) == 0)
+          own_bid = own_bid < 0 ? ar.price : max(own_bid, static_cast<int64_t>(ar.price));
+        else
+          own_ask = own_ask < 0 ? ar.price : min(own_ask, static_cast<int64_t>(ar.price));
+      }
+      const double dmid = static_cast<double>(mid_half - prev_mid_half) / 2.0;
+      double* out = sm.obs;
+      if (sp.type == MLOB_EXECUTOR) {
+        const int dir = st.task_dir == MLOB_TASK_BUY ? 1 : -1;
+        out[0] = static_cast<double>(st.task_remaining) /
+                 static_cast<double>(sp.task_size > 1 ? sp.task_size : 1);
+        out[1] = time_frac;
+        out[2] = static_cast<double>(dir);
+        out[3] = spread;
+        out[4] = dmid;
+        out[5] = static_cast<double>(mid_half) / 2.0 - st.p_init;
+        out[6] = imb;
+        out[7] = nb > 0 ? qty_feature(l2b[0].qty, sp.order_size) : 0.0;
+        out[8] = na > 0 ? qty_feature(l2a[0].qty, sp.order_size) : 0.0;
+        const bool buy = dir > 0;
+        out[9] = offset_feature(buy ? own_bid : own_ask, buy ? bb : ba, buy);
+        for (int j = 10; j < dim; ++j) out[j] = 0.0;  // MMFull-sized executor obs
+      } else {
+        const int64_t cs = sp.inventory_cap * static_cast<int64_t>(st.p_init);
+        out[0] = static_cast<double>(st.inventory) / static_cast<double>(sp.inventory_cap);
+        out[1] = static_cast<double>(st.cash) / static_cast<double>(cs > 1 ? cs : 1);
+        out[2] = spread;
+        out[3] = dmid;
+        out[4] = imb;
+        out[5] = time_frac;
+        out[6] = offset_feature(own_bid, bb, true);
+        out[7] = offset_feature(own_ask, ba, false);
+        if (sp.obs_space == MLOB_OBS_MM_FULL) {
+          int k = 8;
+          const int levels = (dim - 8) / 4;
+          for (int d = 0; d < levels; ++d) {
+            const bool hb = d < nb, ha = d < na;
+            out[k++] = hb ? fmin_ref(32.0, static_cast<double>(bb - l2b[d].price)) : -1.0;
+            out[k++] = hb ? qty_feature(l2b[d].qty, sp.order_size) : 0.0;
+            out[k++] = ha ? fmin_ref(32.0, static_cast<double>(l2a[d].price - ba)) : -1.0;
+            out[k++] = ha ? qty_feature(l2a[d].qty, sp.order_size) : 0.0;
+          }
+        } else if (sp.obs_space == MLOB_OBS_EXEC) {
+          out[8] = 0.0;  // the reference leaves these two zero-initialised
+          out[9] = 0.0;
+        }
+      }
+    }
+    __syncwarp();
+    const int t = cfg.flat_spec[a];
+    const int kk = a - cfg.specs[t].flat_offset;
+    double* dst = kp.obs[t] + (env * static_cast<uint64_t>(cfg.specs[t].count) + kk) * dim;
+    for (int j = lane; j < dim; j += kWarp) dst[j] = sm.obs[j];
+    __syncwarp();
+  }
+
+  __device__ void outcomes(bool write_rewards) {
+    L2Lvl* l2b = sm.l2;
+    L2Lvl* l2a = sm.l2 + cfg.obs_depth;
+    const int nb = l2_levels<0>(l2b);
+    const int na = l2_levels<1>(l2a);
+    for (int a = 0; a < cfg.n_agents; ++a) {
+      if (write_rewards) {
+        const double r = compute_reward(a);
+        if (lane == 0) {
+          kp.rewards[env * cfg.n_agents + a] = r;
+          kp.dones[env * cfg.n_agents + a] = terminal ? 1 : 0;
+        }
+      }
+      fill_info(a);
+      build_observation(a, l2b, nb, l2a, na);
+    }
+  }
+
+  __device__ void clear_step_acc() {
+    const int A = cfg.n_agents;
+    for (int i = lane; i < A; i += kWarp) sm.acc[i] = StepAcc{0.0, 0, {0, 0}, {0, 0}, 0, 0};
+    if (lane == 0) {
+      sm.scal[0] = 0;
+      sm.scal[1] = 0;
+    }
+    __syncwarp();
+  }
+
+  // ---- reset (env.hpp:143-192, book.hpp:41-60) ---------------------------
+  __device__ bool reset(uint64_t ep, bool write_rewards) {
+    const EpState es = kp.ep_state[ep];
+    if (!es.valid) {
+      err |= kErrMissingState;
+      return false;
+    }
+    if (static_cast<int>(es.nb) > cfg.capacity || static_cast<int>(es.na) > cfg.capacity) {
+      err |= kErrTooDeep;
+      return false;
+    }
+    episode = ep;
+    const DevLevel* lv = kp.levels + es.level_offset;
+    init_side<0>(lv, es.nb, cfg.synth_id_base, 0);
+    init_side<1>(lv + es.nb, es.na, cfg.synth_id_base + es.nb, es.nb);
+    next_seq = es.nb + es.na;
+    live0 = static_cast<int>(es.nb);
+    live1 = static_cast<int>(es.na);
+    best0 = es.nb ? lv[0].price : 0;
+    best1 = es.na ? lv[es.nb].price : 0;
+    {
+      const bool hb = live0 > 0, ha = live1 > 0;
+      const int64_t b0 = best0, b1 = best1;
+      mid_half = hb ? (ha ? b0 + b1 : 2 * b0) : (ha ? 2 * b1 : cfg.fallback_mid_half);
+    }
+    prev_mid_half = mid_half;
+    mbar = static_cast<double>(mid_half) / 2.0;
+    last_bid = live0 > 0 ? static_cast<int64_t>(best0) : mid_half / 2 - 1;
+    last_ask = live1 > 0 ? static_cast<int64_t>(best1) : (mid_half + 1) / 2 + 1;
+    step = 0;
+    terminal = false;
+    n_trades = 0;
+    const int A = cfg.n_agents;
+    for (int a = 0; a < A; ++a) {
+      const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
+      AgentRec st;
+      st.inventory = 0;
+      st.cash = 0;
+      st.filled_total = 0;
+      st.slippage_total = 0.0;
+      st.nonce = 0;
+      st.n_active = 0;
+      st.p_init = static_cast<double>(mid_half) / 2.0;
+      st.task_dir = sm.ag[a].task_dir;
+      if (sp.type == MLOB_EXECUTOR) {
+        uint64_t h = splitmix64(seed);
+        h = key_fold(h, genv);
+        h = key_fold(h, ep);
+        h = key_fold(h, 0);
+        h = key_fold(h, kRngTaskDir);
+        h = key_fold(h, static_cast<uint64_t>(a));
+        Rng r{h};
+        st.task_dir = r.coin() ? MLOB_TASK_BUY : MLOB_TASK_SELL;
+        st.task_remaining = sp.task_size;
+      } else {
+        st.task_remaining = 0;
+      }
+      __syncwarp();
+      if (lane == 0) sm.ag[a] = st;
+    }
+    __syncwarp();
+    clear_step_acc();
+    for (int a = 0; a < A && write_rewards; ++a)
+      if (lane == 0) {
+        kp.rewards[env * A + a] = 0.0;
+        kp.dones[env * A + a] = 0;
+      }
+    outcomes(false);
+    return true;
+  }
+
+  template <int S>
+  __device__ void init_side(const DevLevel* lv, uint32_t n, uint64_t id_base, uint32_t seq_base) {
+    SideT& d = sd<S>();
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      const uint32_t i = static_cast<uint32_t>(k * kWarp + lane);
+      if (i < n) {
+        const uint64_t id = id_base + i;
+        d.put(k, lv[i].price, lv[i].qty, static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32),
+              (seq_base + i) << 8);
+      } else {
+        d.put(k, empty_price<S>(), 0, 0, 0, kEmptySt);
+      }
+    }
+  }
+
+  __device__ uint64_t episode_for(uint64_t k) const {  // rollout.hpp:286-288
+    const uint64_t i = (genv + k * kp.n_envs_global) % kp.pool_len;
+    return kp.pool ? kp.pool[i] : i;
+  }
+};
+
+}  // namespace mlob
