@@ -28,8 +28,8 @@ __device__ WarpSmem carve(char* base, const DevCfg& c) {
   const int chunk = c.mps < kChunk ? c.mps : kChunk;
   const int nbuf = c.mps > kChunk ? 2 : 1;
   char* p = base;
-  s.chunk[0] = reinterpret_cast<DevMsg*>(p);
-  s.chunk[1] = nbuf == 2 ? s.chunk[0] + chunk : s.chunk[0];
+  s.chunk0 = reinterpret_cast<DevMsg*>(p);
+  s.chunk1 = nbuf == 2 ? s.chunk0 + chunk : s.chunk0;
   p += static_cast<size_t>(nbuf) * chunk * sizeof(DevMsg);
   s.bar = reinterpret_cast<uint64_t*>(p);
   p += 16;
@@ -78,10 +78,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp, MLOB_MIN_BLOCKS)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.bar[1])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int c = 0; c < 2 && c < n_chunks; ++c)
-      bulk_copy(sm.chunk[c], slice + c * kChunk,
+      bulk_copy(c ? sm.chunk1 : sm.chunk0, slice + c * kChunk,
                 static_cast<uint32_t>(min(kChunk, mps - c * kChunk) * sizeof(DevMsg)), &sm.bar[c]);
   }
-  w.load_book();
   w.load_agents();
   w.clear_step_acc();
   const int64_t step_time = mps > 0 ? slice[0].time : w.last_time + 1;
@@ -107,6 +106,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp, MLOB_MIN_BLOCKS)
     }
   }
   __syncwarp();
+  // book registers are loaded only now: nothing above needs them (tops are in
+  // the header) and they must not be live across the modulo subroutine calls
+  w.load_book();
 
   // (3) + (4): agent messages, then the replay slice
   w.prev_mid_half = w.mid_half;
@@ -124,6 +126,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp, MLOB_MIN_BLOCKS)
   w.rebuild_active();
   ++w.step;
   w.terminal = w.step >= cfg.steps_per_episode;
+  w.snapshot();
+  w.store_book();  // book registers dead from here on (no calls below see them live)
   w.outcomes(true);
 
   uint8_t just_reset = 0;
@@ -145,9 +149,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp, MLOB_MIN_BLOCKS)
     ++w.ep_finished;
     const uint64_t ep = w.episode_for(w.cursor);
     ++w.cursor;
-    if (w.reset(ep, false)) just_reset = 1;
+    if (w.reset(ep, false)) {
+      just_reset = 1;
+      w.snapshot();
+      w.store_book();
+      w.outcomes(false);
+    }
   }
-  w.store_all(just_reset);
+  w.store_state(just_reset);
 }
 
 // K3: MarketEnv::reset for every env (reset_all / reset_envs).
@@ -163,9 +172,16 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp)
   WarpEnv<SPL> w(kp, sm, env, lane);
   w.load_hdr();  // keeps last_time / messages_processed across resets
   w.load_agents();
-  w.reset(kp.reset_episodes[env], true);
+  w.load_book();
+  if (w.reset(kp.reset_episodes[env], true)) {
+    w.snapshot();
+    w.store_book();
+    w.outcomes(false);
+  } else {
+    w.store_book();
+  }
   w.cursor = 1;
-  w.store_all(1);
+  w.store_state(1);
 }
 
 // K4: per-type episode-stat sums over this handle's envs (for the NCCL

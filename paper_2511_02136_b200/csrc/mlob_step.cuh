@@ -157,7 +157,8 @@ struct L2Lvl {
 };
 
 struct WarpSmem {
-  DevMsg* chunk[2];
+  DevMsg* chunk0;  // replay chunk buffers (no array: keeps WarpEnv promotable to registers)
+  DevMsg* chunk1;
   uint64_t* bar;  // 2 mbarriers
   DevMsg* amsg;   // agent messages (<= 4 * A)
   AgentRec* ag;
@@ -196,14 +197,15 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
 // aggressor agent); executed by lane 0 only, in fill order.  Agent state is
 // not read inside the message loop, so the other lanes see it after the
 // loop's closing __syncwarp.
-__device__ __forceinline__ void attribute_fill(const DevCfg* cfg, WarpSmem sm, int32_t price,
-                                               int32_t qty, int ptrader, int atrader, int aside) {
+__device__ __forceinline__ void attribute_fill(int n_agents, const DevCfg& cfg, WarpSmem sm,
+                                               int32_t price, int32_t qty, int ptrader, int atrader,
+                                               int aside) {
   for (int r = 0; r < 2; ++r) {
     const int trader = r == 0 ? ptrader : atrader;
-    if (trader <= 0 || trader > cfg->n_agents) continue;
+    if (trader <= 0 || trader > n_agents) continue;
     const int a = trader - 1;
     const int side = r == 0 ? 1 - aside : aside;
-    const DevSpec& sp = cfg->specs[cfg->flat_spec[a]];
+    const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
     AgentRec& st = sm.ag[a];
     StepAcc& ac = sm.acc[a];
     const int64_t pq = static_cast<int64_t>(price) * qty;
@@ -259,12 +261,19 @@ struct WarpEnv {
   int64_t mid_sum, mid_count;
   uint32_t n_trades;
   uint32_t err;
+  int capacity;        // cached kernel params (avoid generic loads of param space)
+  bool rec_trades;
+  int n_agents;
+  int nb_l2, na_l2;    // L2 levels staged in smem by snapshot()
 
   __device__ WarpEnv(const KParams& p, const WarpSmem& s, uint64_t e, int ln)
       : kp(p), cfg(p.cfg), sm(s), lane(ln), env(e) {
     genv = kp.env_index ? kp.env_index[e] : kp.env_index_base + e;
     seed = kp.env_seed ? kp.env_seed[e] : kp.seed;
     err = 0;
+    capacity = p.cfg.capacity;
+    rec_trades = (p.flags & MLOB_VENV_RECORD_TRADES) != 0;
+    n_agents = p.cfg.n_agents;
   }
 
   template <int S>
@@ -315,7 +324,7 @@ struct WarpEnv {
     return hwm;
   }
 
-  __device__ void load_hdr() {
+  __device__ __forceinline__ void load_hdr() {
     const EnvHdr& h = kp.hdr[env];
     mid_half = h.mid_half;
     prev_mid_half = h.prev_mid_half;
@@ -336,14 +345,18 @@ struct WarpEnv {
     terminal = h.terminal != 0;
     n_trades = h.n_trades;
   }
-  __device__ void load_book() {
+  __device__ __forceinline__ void load_book() {
     const EnvHdr& h = kp.hdr[env];
     load_side<0>(h.hwm[0]);
     load_side<1>(h.hwm[1]);
   }
-  __device__ void store_all(uint8_t just_reset) {
-    const int h0 = store_side<0>();
-    const int h1 = store_side<1>();
+  int hwm0, hwm1;
+  __device__ __forceinline__ void store_book() {
+    hwm0 = store_side<0>();
+    hwm1 = store_side<1>();
+  }
+  __device__ __forceinline__ void store_state(uint8_t just_reset) {
+    const int h0 = hwm0, h1 = hwm1;
     if (lane == 0) {
       EnvHdr h;
       h.mid_half = mid_half;
@@ -383,7 +396,7 @@ struct WarpEnv {
     }
     if (err && lane == 0) atomicOr(kp.error, err);
   }
-  __device__ void load_agents() {
+  __device__ __forceinline__ void load_agents() {
     const int A = cfg.n_agents;
     const int words = A * static_cast<int>(sizeof(AgentRec) / 8);
     const uint64_t* src = reinterpret_cast<const uint64_t*>(kp.agents + env * A);
@@ -522,7 +535,7 @@ struct WarpEnv {
   // ---- message handlers (runtime side) -------------------------------------
   __device__ __forceinline__ void record_trade(int32_t price, int32_t qty, const DevMsg& m,
                                                uint32_t lo, uint32_t hi, uint32_t st, int aside) {
-    if ((kp.flags & MLOB_VENV_RECORD_TRADES) && lane == 0 && n_trades < kp.trade_cap) {
+    if (rec_trades && lane == 0 && n_trades < kp.trade_cap) {
       mlob_trade t;
       t.price = price;
       t.quantity = qty;
@@ -539,14 +552,14 @@ struct WarpEnv {
     ++n_trades;
     const uint32_t pt = st & 0xffu;
     if ((pt | static_cast<uint32_t>(m.trader)) && lane == 0)  // an agent is involved
-      attribute_fill(&cfg, sm, price, qty, static_cast<int>(pt), m.trader, aside);
+      attribute_fill(n_agents, cfg, sm, price, qty, static_cast<int>(pt), m.trader, aside);
   }
 
   // book.hpp:150-187 (process_new_limit + rest_order)
   __device__ __forceinline__ void new_limit(const DevMsg& m) {
     const int s = m.side, o = s ^ 1;
     int32_t rem = m.qty;
-    const bool pass_ids = (kp.flags & MLOB_VENV_RECORD_TRADES) != 0;
+    const bool pass_ids = rec_trades;
     while (rem > 0) {
       const int lo_ = o ? live1 : live0;
       const int32_t bp = o ? best1 : best0;
@@ -584,7 +597,7 @@ struct WarpEnv {
     }
     if (rem <= 0) return;
     // rest_order
-    if ((s ? live1 : live0) == cfg.capacity) {
+    if ((s ? live1 : live0) == capacity) {
       const bool ev = s ? evict_t<1>(m.price) : evict_t<0>(m.price);
       if (!ev) return;  // newcomer dropped: no sequence number consumed
       if (s)
@@ -658,7 +671,7 @@ struct WarpEnv {
   }
 
   // Agent messages, then the replay slice staged in smem chunks (env.hpp:236-237).
-  __device__ void process_messages(int n_amsg, const DevMsg* slice) {
+  __device__ __forceinline__ void process_messages(int n_amsg, const DevMsg* slice) {
     const int mps = cfg.mps;
     const int total = n_amsg + mps;
     const int nch = (mps + kChunk - 1) / kChunk;
@@ -673,12 +686,12 @@ struct WarpEnv {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             const int nb = (c + 1) & 1;
             const int n2 = min(kChunk, mps - (c + 1) * kChunk);
-            bulk_copy(sm.chunk[nb], slice + (c + 1) * kChunk, static_cast<uint32_t>(n2 * sizeof(DevMsg)),
+            bulk_copy(nb ? sm.chunk1 : sm.chunk0, slice + (c + 1) * kChunk, static_cast<uint32_t>(n2 * sizeof(DevMsg)),
                       &sm.bar[nb]);
           }
         }
         bar_wait(&sm.bar[c & 1], static_cast<uint32_t>((c >> 1) & 1));
-        buf = sm.chunk[c & 1];
+        buf = (c & 1) ? sm.chunk1 : sm.chunk0;
         base = i;
       }
       const DevMsg m = buf[i - base];
@@ -731,7 +744,7 @@ struct WarpEnv {
     }
   };
 
-  __device__ void decode(int a, int id, Quotes& q) {
+  __device__ __forceinline__ void decode(int a, int id, Quotes& q) {
     const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
     const AgentRec& st = sm.ag[a];
     int64_t bb, ba;
@@ -807,7 +820,7 @@ struct WarpEnv {
 
   // env.hpp:285-370: quotes -> Delete for stale active orders, NewLimit for
   // quotes not already resting at the same (side, price).
-  __device__ void convert_action(int a, int64_t step_time, int& n_amsg) {
+  __device__ __forceinline__ void convert_action(int a, int64_t step_time, int& n_amsg) {
     const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
     AgentRec& st = sm.ag[a];
     Quotes q;
@@ -874,7 +887,7 @@ struct WarpEnv {
   // ---- step outcomes -------------------------------------------------------
   // Top-D aggregated levels per side, best-first (book.hpp:109-120, 209-220).
   template <int S>
-  __device__ int l2_levels(L2Lvl* out) {
+  __device__ __forceinline__ int l2_levels(L2Lvl* out) {
     SideT& d = sd<S>();
     const int D = cfg.obs_depth;
     int n = 0;
@@ -905,7 +918,7 @@ struct WarpEnv {
   }
 
   // env.hpp:398-407: active orders per agent, book storage order.
-  __device__ void rebuild_active() {
+  __device__ __forceinline__ void rebuild_active() {
     const int A = cfg.n_agents;
     for (int a = lane; a < A; a += kWarp) sm.ag[a].n_active = 0;
     __syncwarp();
@@ -913,7 +926,7 @@ struct WarpEnv {
     rebuild_side<1>();
   }
   template <int S>
-  __device__ void rebuild_side() {
+  __device__ __forceinline__ void rebuild_side() {
     SideT& d = sd<S>();
     uint32_t taken = 0;  // per-lane bitmask of consumed rows
     int cnt = 0;
@@ -971,14 +984,14 @@ struct WarpEnv {
   }
 
   // env.hpp:435-443
-  __device__ double reference_price(const DevSpec& sp, const AgentRec& st) const {
+  __device__ __forceinline__ double reference_price(const DevSpec& sp, const AgentRec& st) const {
     if (sp.ref_price == MLOB_REF_MID || st.inventory == 0) return static_cast<double>(mid_half) / 2.0;
     if (st.inventory > 0) return static_cast<double>(live0 > 0 ? static_cast<int64_t>(best0) : last_bid);
     return static_cast<double>(live1 > 0 ? static_cast<int64_t>(best1) : last_ask);
   }
 
   // env.hpp:445-464 (also accumulates slippage_total); lane 0 writes.
-  __device__ void fill_info(int a) {
+  __device__ __forceinline__ void fill_info(int a) {
     const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
     AgentRec& st = sm.ag[a];
     const StepAcc& ac = sm.acc[a];
@@ -1003,7 +1016,7 @@ struct WarpEnv {
   }
 
   // env.hpp:409-433 + rewards.hpp
-  __device__ double compute_reward(int a) {
+  __device__ __forceinline__ double compute_reward(int a) {
     const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
     const AgentRec& st = sm.ag[a];
     const StepAcc& ac = sm.acc[a];
@@ -1060,7 +1073,7 @@ struct WarpEnv {
 
   // env.hpp:466-503, observations.hpp:42-148; features staged in smem by lane
   // 0 then written by lanes (coalesced).
-  __device__ void build_observation(int a, const L2Lvl* l2b, int nb, const L2Lvl* l2a, int na) {
+  __device__ __forceinline__ void build_observation(int a, const L2Lvl* l2b, int nb, const L2Lvl* l2a, int na) {
     const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
     const AgentRec& st = sm.ag[a];
     const int dim = sp.obs_dim;
@@ -1132,11 +1145,20 @@ struct WarpEnv {
     __syncwarp();
   }
 
-  __device__ void outcomes(bool write_rewards) {
-    L2Lvl* l2b = sm.l2;
-    L2Lvl* l2a = sm.l2 + cfg.obs_depth;
-    const int nb = l2_levels<0>(l2b);
-    const int na = l2_levels<1>(l2a);
+  // Book-dependent part of the step outcomes: L2 top-D into smem.  After this
+  // (and rebuild_active) the book registers can be stored and released, so no
+  // book register is live across the double-division / 64-bit-modulo
+  // subroutine calls of the reward/observation code (they forced the book
+  // through local memory in v1).
+  __device__ __forceinline__ void snapshot() {
+    nb_l2 = l2_levels<0>(sm.l2);
+    na_l2 = l2_levels<1>(sm.l2 + cfg.obs_depth);
+  }
+
+  __device__ __forceinline__ void outcomes(bool write_rewards) {
+    const L2Lvl* l2b = sm.l2;
+    const L2Lvl* l2a = sm.l2 + cfg.obs_depth;
+    const int nb = nb_l2, na = na_l2;
     for (int a = 0; a < cfg.n_agents; ++a) {
       if (write_rewards) {
         const double r = compute_reward(a);
@@ -1150,7 +1172,7 @@ struct WarpEnv {
     }
   }
 
-  __device__ void clear_step_acc() {
+  __device__ __forceinline__ void clear_step_acc() {
     const int A = cfg.n_agents;
     for (int i = lane; i < A; i += kWarp) sm.acc[i] = StepAcc{0.0, 0, {0, 0}, {0, 0}, 0, 0};
     if (lane == 0) {
@@ -1161,7 +1183,7 @@ struct WarpEnv {
   }
 
   // ---- reset (env.hpp:143-192, book.hpp:41-60) ---------------------------
-  __device__ bool reset(uint64_t ep, bool write_rewards) {
+  __device__ __forceinline__ bool reset(uint64_t ep, bool write_rewards) {
     const EpState es = kp.ep_state[ep];
     if (!es.valid) {
       err |= kErrMissingState;
@@ -1227,12 +1249,11 @@ struct WarpEnv {
         kp.rewards[env * A + a] = 0.0;
         kp.dones[env * A + a] = 0;
       }
-    outcomes(false);
-    return true;
+    return true;  // caller: snapshot(), store_book(), outcomes(false)
   }
 
   template <int S>
-  __device__ void init_side(const DevLevel* lv, uint32_t n, uint64_t id_base, uint32_t seq_base) {
+  __device__ __forceinline__ void init_side(const DevLevel* lv, uint32_t n, uint64_t id_base, uint32_t seq_base) {
     SideT& d = sd<S>();
 #pragma unroll
     for (int k = 0; k < SPL; ++k) {
@@ -1247,7 +1268,7 @@ struct WarpEnv {
     }
   }
 
-  __device__ uint64_t episode_for(uint64_t k) const {  // rollout.hpp:286-288
+  __device__ __forceinline__ uint64_t episode_for(uint64_t k) const {  // rollout.hpp:286-288
     const uint64_t i = (genv + k * kp.n_envs_global) % kp.pool_len;
     return kp.pool ? kp.pool[i] : i;
   }
