@@ -153,6 +153,7 @@ struct KParams {
   uint32_t trade_cap;
   uint32_t fill_overflows_unused;
   unsigned long long* fill_overflow;  // count of env-steps whose MM fill log overflowed
+  unsigned long long* ticket;         // persistent step kernel: next-env ticket counter
   // env identity / episode pool
   const uint64_t* env_seed;   // optional
   const uint64_t* env_index;  // optional

@@ -56,107 +56,152 @@ constexpr int kWarpsPerBlock = 4;
 #define MLOB_MIN_BLOCKS 4
 #endif
 
-// K1+K2: one environment step per warp (MarketEnv::step, env.hpp:194-254,
-// + MarketVecEnv::step_one auto-reset, rollout.hpp:290-318).
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// K1+K2: persistent warps, one environment step per warp per iteration
+// (MarketEnv::step, env.hpp:194-254, + MarketVecEnv::step_one auto-reset,
+// rollout.hpp:290-318).  While env e is processed, the next env's first
+// replay chunk is already in flight (cp.async.bulk) and its header, agent
+// records and book rows are prefetched into L2.
 template <int SPL>
 __global__ void __launch_bounds__(kWarpsPerBlock * kWarp, MLOB_MIN_BLOCKS)
     step_kernel(const __grid_constant__ KParams kp) {
   extern __shared__ __align__(128) char smem[];
   const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
-  const uint64_t env = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + warp;
-  if (env >= kp.n_envs) return;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarpsPerBlock;
+  // dynamic work distribution: the first env of each warp is static, later
+  // ones come from a global ticket counter (fetched one env ahead so the next
+  // env's data can be prefetched); kp.ticket is zeroed before each launch.
+  const uint64_t first = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + warp;
+  if (first >= kp.n_envs) return;
+  const auto ticket = [&]() -> uint64_t {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(kp.ticket, 1ull);
+    return stride + __shfl_sync(FULLMASK, t, 0);
+  };
   const DevCfg& cfg = kp.cfg;
   WarpSmem sm = carve(smem + warp * warp_smem_bytes(cfg), cfg);
-  WarpEnv<SPL> w(kp, sm, env, lane);
-  w.load_hdr();
-
+  WarpEnv<SPL> w(kp, sm, first, lane);
   const int mps = cfg.mps;
-  const DevMsg* slice = kp.msgs + kp.ep_start[w.episode] + static_cast<uint64_t>(w.step) * mps;
-  const int n_chunks = (mps + kChunk - 1) / kChunk;
-  if (mps > 0 && lane == 0) {
+  const int nch = (mps + kChunk - 1) / kChunk;
+  const int A = cfg.n_agents;
+  if (lane == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.bar[0])));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.bar[1])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int c = 0; c < 2 && c < n_chunks; ++c)
-      bulk_copy(c ? sm.chunk1 : sm.chunk0, slice + c * kChunk,
-                static_cast<uint32_t>(min(kChunk, mps - c * kChunk) * sizeof(DevMsg)), &sm.bar[c]);
   }
-  w.load_agents();
-  w.clear_step_acc();
-  const int64_t step_time = mps > 0 ? slice[0].time : w.last_time + 1;
-
-  // (1) actions -> agent messages, (2) Fisher-Yates (rng.hpp:63-71)
-  int n_amsg = 0;
-  for (int a = 0; a < cfg.n_agents; ++a) w.convert_action(a, step_time, n_amsg);
   __syncwarp();
-  if (n_amsg >= 2 && lane == 0) {
-    uint64_t h = splitmix64(w.seed);
-    h = key_fold(h, w.genv);
-    h = key_fold(h, w.episode);
-    h = key_fold(h, static_cast<uint64_t>(w.step));
-    h = key_fold(h, kRngShuffle);
-    Rng r{h};
-    for (int i = n_amsg - 1; i > 0; --i) {
-      const int j = static_cast<int>(r.below(static_cast<uint64_t>(i + 1)));
-      if (i != j) {
-        const DevMsg t = sm.amsg[i];
-        sm.amsg[i] = sm.amsg[j];
-        sm.amsg[j] = t;
+  const auto slice_of = [&](uint64_t e) {
+    const EnvHdr& h = kp.hdr[e];
+    return kp.msgs + kp.ep_start[h.episode] + static_cast<uint64_t>(h.step) * mps;
+  };
+  if (mps > 0) w.stage(slice_of(first), min(kChunk, mps));
+
+  uint64_t nenv = MLOB_PERSIST ? ticket() : kp.n_envs;
+  for (uint64_t env = first; env < kp.n_envs;) {
+    w.bind(env);
+    w.load_hdr();
+    const DevMsg* slice = kp.msgs + kp.ep_start[w.episode] + static_cast<uint64_t>(w.step) * mps;
+    if (nch >= 2) w.stage(slice + kChunk, min(kChunk, mps - kChunk));
+    const bool has_next = nenv < kp.n_envs;
+    const DevMsg* next_slice = nullptr;
+    if (has_next) {
+      next_slice = mps > 0 ? slice_of(nenv) : nullptr;
+#if MLOB_PREFETCH
+      const EnvHdr& nh = kp.hdr[nenv];
+      if (lane == 0) prefetch_l2(&nh);
+      if (lane < A) prefetch_l2(kp.agents + nenv * A + lane);
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+#pragma unroll
+        for (int k = 0; k < SPL; ++k)
+          if (k * kWarp < (s ? nh.hwm[1] : nh.hwm[0])) {
+            const size_t i = ((nenv * 2 + s) * SPL + k) * kWarp + lane;
+            prefetch_l2(kp.bk_p + i);
+            prefetch_l2(kp.bk_q + i);
+            prefetch_l2(kp.bk_id + i);
+            prefetch_l2(kp.bk_st + i);
+          }
+#endif
+    }
+    w.load_agents();
+    w.clear_step_acc();
+    const int64_t step_time = mps > 0 ? slice[0].time : w.last_time + 1;
+
+    // (1) actions -> agent messages, (2) Fisher-Yates (rng.hpp:63-71)
+    int n_amsg = 0;
+    for (int a = 0; a < A; ++a) w.convert_action(a, step_time, n_amsg);
+    __syncwarp();
+    if (n_amsg >= 2 && lane == 0) {
+      uint64_t h = splitmix64(w.seed);
+      h = key_fold(h, w.genv);
+      h = key_fold(h, w.episode);
+      h = key_fold(h, static_cast<uint64_t>(w.step));
+      h = key_fold(h, kRngShuffle);
+      Rng r{h};
+      for (int i = n_amsg - 1; i > 0; --i) {
+        const int j = static_cast<int>(r.below(static_cast<uint64_t>(i + 1)));
+        if (i != j) {
+          const DevMsg t = sm.amsg[i];
+          sm.amsg[i] = sm.amsg[j];
+          sm.amsg[j] = t;
+        }
       }
     }
-  }
-  __syncwarp();
-  // book registers are loaded only now: nothing above needs them (tops are in
-  // the header) and they must not be live across the modulo subroutine calls
-  w.load_book();
+    __syncwarp();
+    // book registers are loaded only now: nothing above needs them (tops are
+    // in the header) and they must not be live across subroutine calls
+    w.load_book();
 
-  // (3) + (4): agent messages, then the replay slice
-  w.prev_mid_half = w.mid_half;
-  w.mid_sum = 0;
-  w.mid_count = 0;
-  w.n_trades = 0;
-  w.process_messages(n_amsg, slice);
-  if (w.live0 > 0) w.last_bid = w.best0;
-  if (w.live1 > 0) w.last_ask = w.best1;
+    // (3) + (4): agent messages, then the replay slice
+    w.prev_mid_half = w.mid_half;
+    w.mid_sum = 0;
+    w.mid_count = 0;
+    w.n_trades = 0;
+    w.process_messages(n_amsg, slice);
+    if (has_next && mps > 0) w.stage(next_slice, min(kChunk, mps));  // overlaps the outcomes
+    if (w.live0 > 0) w.last_bid = w.best0;
+    if (w.live1 > 0) w.last_ask = w.best1;
 
-  // (5) outcomes
-  w.mbar = w.mid_count > 0 ? static_cast<double>(w.mid_sum) / (2.0 * static_cast<double>(w.mid_count))
-                           : static_cast<double>(w.prev_mid_half) / 2.0;
-  if (sm.scal[1] && lane == 0) atomicAdd(kp.fill_overflow, 1ull);
-  w.rebuild_active();
-  ++w.step;
-  w.terminal = w.step >= cfg.steps_per_episode;
-  w.snapshot();
-  w.store_book();  // book registers dead from here on (no calls below see them live)
-  w.outcomes(true);
-
-  uint8_t just_reset = 0;
-  if (w.terminal && (kp.flags & MLOB_VENV_AUTO_RESET)) {
-    const int A = cfg.n_agents;
-    if (lane == 0)
-      for (int a = 0; a < A; ++a) {  // rollout.hpp:300-313
-        const mlob_agent_info& info = kp.infos[env * A + a];
-        const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
-        const size_t slot = env * A + a;
-        kp.t_pv[slot] += info.portfolio_value;
-        kp.t_slip[slot] += info.slippage_total;
-        kp.t_comp[slot] += sp.type == MLOB_EXECUTOR
-                               ? 1.0 - static_cast<double>(info.task_remaining) /
-                                           static_cast<double>(sp.task_size)
-                               : 0.0;
-        kp.t_inv[slot] += static_cast<double>(info.inventory) * static_cast<double>(info.inventory);
-      }
-    ++w.ep_finished;
-    const uint64_t ep = w.episode_for(w.cursor);
-    ++w.cursor;
-    if (w.reset(ep, false)) {
-      just_reset = 1;
+    // (5) outcomes
+    w.mbar = w.mid_count > 0 ? static_cast<double>(w.mid_sum) / (2.0 * static_cast<double>(w.mid_count))
+                             : static_cast<double>(w.prev_mid_half) / 2.0;
+    if (sm.scal[1] && lane == 0) atomicAdd(kp.fill_overflow, 1ull);
+    w.rebuild_active();
+    ++w.step;
+    w.terminal = w.step >= cfg.steps_per_episode;
+    uint8_t just_reset = 0;
+    for (int pass = 0;; ++pass) {  // pass 1: the auto-reset env's fresh outputs
       w.snapshot();
-      w.store_book();
-      w.outcomes(false);
+      w.store_book();  // book registers dead from here on
+      w.outcomes(pass == 0);
+      if (pass > 0 || !(w.terminal && (kp.flags & MLOB_VENV_AUTO_RESET))) break;
+      if (lane == 0)
+        for (int a = 0; a < A; ++a) {  // rollout.hpp:300-313
+          const mlob_agent_info& info = kp.infos[env * A + a];
+          const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
+          const size_t slot = env * A + a;
+          kp.t_pv[slot] += info.portfolio_value;
+          kp.t_slip[slot] += info.slippage_total;
+          kp.t_comp[slot] += sp.type == MLOB_EXECUTOR
+                                 ? 1.0 - static_cast<double>(info.task_remaining) /
+                                             static_cast<double>(sp.task_size)
+                                 : 0.0;
+          kp.t_inv[slot] += static_cast<double>(info.inventory) * static_cast<double>(info.inventory);
+        }
+      ++w.ep_finished;
+      const uint64_t ep = w.episode_for(w.cursor);
+      ++w.cursor;
+      if (!w.reset(ep, false)) break;
+      just_reset = 1;
     }
+    w.store_state(just_reset);
+    env = nenv;
+    if (has_next) nenv = ticket();
   }
-  w.store_state(just_reset);
+  w.report_errors();
 }
 
 // K3: MarketEnv::reset for every env (reset_all / reset_envs).
@@ -182,6 +227,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp)
   }
   w.cursor = 1;
   w.store_state(1);
+  w.report_errors();
 }
 
 // K4: per-type episode-stat sums over this handle's envs (for the NCCL
@@ -240,7 +286,16 @@ static cudaError_t launch_step_t(const KParams& kp, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(step_kernel<SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sm));
   if (e != cudaSuccess) return e;
-  const unsigned blocks = static_cast<unsigned>((kp.n_envs + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  // persistent grid: every SM filled to its occupancy limit, warps loop over envs
+  int dev = 0, n_sm = 0, per_sm = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<SPL>, kWarpsPerBlock * kWarp,
+                                                         sm)) != cudaSuccess)
+    return e;
+  const uint64_t need = (kp.n_envs + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const uint64_t cap = static_cast<uint64_t>(n_sm) * (per_sm > 0 ? per_sm : 1);
+  const unsigned blocks = static_cast<unsigned>(MLOB_PERSIST ? (need < cap ? need : cap) : need);
   step_kernel<SPL><<<blocks, kWarpsPerBlock * kWarp, sm, s>>>(kp);
   return cudaGetLastError();
 }

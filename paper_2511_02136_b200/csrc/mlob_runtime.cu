@@ -137,6 +137,7 @@ struct mlob_venv {
   uint64_t* d_reset_eps = nullptr;
   uint32_t* d_error = nullptr;
   unsigned long long* d_scratch = nullptr;
+  unsigned long long* d_ticket = nullptr;
 
   template <class T>
   T* alloc(size_t n, const char* what) {
@@ -182,6 +183,7 @@ struct mlob_venv {
     k.trades = d_trades;
     k.trade_cap = trade_cap;
     k.fill_overflow = d_fill_overflow;
+    k.ticket = d_ticket;
     k.env_seed = d_env_seed;
     k.env_index = d_env_index;
     k.seed = seed;
@@ -658,6 +660,7 @@ mlob_status mlob_venv_create(const mlob_venv_desc* desc, mlob_venv** out) {
     if (v->trade_cap) v->d_trades = v->alloc<mlob_trade>(n * v->trade_cap, "trades");
     v->d_fill_overflow = v->alloc<unsigned long long>(1, "fill_overflow");
     v->d_scratch = v->alloc<unsigned long long>(8, "scratch");
+    v->d_ticket = v->alloc<unsigned long long>(1, "ticket");
     v->d_reset_eps = v->alloc<uint64_t>(n, "reset_eps");
     v->d_error = v->alloc<uint32_t>(1, "error");
     if (desc->env_seeds) {
@@ -770,6 +773,7 @@ static void do_step(mlob_venv* v, int mode, uint64_t bench_seed, uint64_t global
   kp.action_mode = mode;
   kp.bench_seed = bench_seed;
   kp.global_step = global_step;
+  cuda_check(cudaMemsetAsync(v->d_ticket, 0, sizeof(unsigned long long), v->stream), "ticket reset");
   cuda_check(launch_step(kp, v->spl, v->stream), "step kernel");
   ++v->launches;
   for (auto& s : v->steps) {

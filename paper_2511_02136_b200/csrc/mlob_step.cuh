@@ -28,6 +28,16 @@
 
 #include "mlob_dev.h"
 
+#ifndef MLOB_LDS_ASM
+#define MLOB_LDS_ASM 1
+#endif
+#ifndef MLOB_PERSIST  // persistent warps + ticketed envs: measured slower (r1 notes)
+#define MLOB_PERSIST 0
+#endif
+#ifndef MLOB_PREFETCH
+#define MLOB_PREFETCH 1
+#endif
+
 namespace mlob {
 
 #define FULLMASK 0xffffffffu
@@ -51,7 +61,18 @@ struct Rng {
     s += kGamma;
     return splitmix64(s);
   }
-  __device__ __forceinline__ uint64_t below(uint64_t n) { return next() % n; }
+  // next() % n, computed without the 64-bit modulo subroutine call when n < 2^16:
+  // x mod n = ((hi mod n) * (2^32 mod n) + lo mod n) mod n, all in 32 bits.
+  __device__ __forceinline__ uint64_t below(uint64_t n) {
+    const uint64_t x = next();
+    if (n <= 0xffffu) {
+      const uint32_t m = static_cast<uint32_t>(n);
+      const uint32_t hi = static_cast<uint32_t>(x >> 32), lo = static_cast<uint32_t>(x);
+      const uint32_t p32 = (0xffffffffu % m + 1u) % m;
+      return ((hi % m) * p32 + lo % m) % m;
+    }
+    return x % n;
+  }
   __device__ __forceinline__ bool coin() { return (next() & 1ull) != 0; }
 };
 enum : uint64_t { kRngShuffle = 1, kRngTaskDir = 2, kRngBenchAction = 7 };
@@ -174,6 +195,25 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// 32-byte message record from shared memory (explicit ld.shared: the generic
+// pointer would otherwise compile to a generic LD).
+__device__ __forceinline__ DevMsg lds_msg(const DevMsg* p) {
+  uint4 a, b;
+  const uint32_t s = smem_u32(p);
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "r"(s));
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4+16];" : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "r"(s));
+  DevMsg m;
+  m.time = static_cast<int64_t>((static_cast<uint64_t>(a.y) << 32) | a.x);
+  m.order_id = (static_cast<uint64_t>(a.w) << 32) | a.z;
+  m.price = static_cast<int32_t>(b.x);
+  m.qty = static_cast<int32_t>(b.y);
+  m.kind = static_cast<uint8_t>(b.z & 0xffu);
+  m.side = static_cast<uint8_t>((b.z >> 8) & 0xffu);
+  m._pad = 0;
+  m.trader = static_cast<int32_t>(b.w);
+  return m;
+}
+
 __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   const uint32_t b = smem_u32(bar);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
@@ -268,12 +308,17 @@ struct WarpEnv {
 
   __device__ WarpEnv(const KParams& p, const WarpSmem& s, uint64_t e, int ln)
       : kp(p), cfg(p.cfg), sm(s), lane(ln), env(e) {
-    genv = kp.env_index ? kp.env_index[e] : kp.env_index_base + e;
-    seed = kp.env_seed ? kp.env_seed[e] : kp.seed;
+    bind(e);
     err = 0;
     capacity = p.cfg.capacity;
     rec_trades = (p.flags & MLOB_VENV_RECORD_TRADES) != 0;
     n_agents = p.cfg.n_agents;
+  }
+
+  __device__ __forceinline__ void bind(uint64_t e) {
+    env = e;
+    genv = kp.env_index ? kp.env_index[e] : kp.env_index_base + e;
+    seed = kp.env_seed ? kp.env_seed[e] : kp.seed;
   }
 
   template <int S>
@@ -351,6 +396,25 @@ struct WarpEnv {
     load_side<1>(h.hwm[1]);
   }
   int hwm0, hwm1;
+  // chunk stager: copy #q goes to buffer q & 1 and completes phase (q >> 1) & 1
+  // of that buffer's mbarrier.  Copies run ahead of consumption by <= 2.
+  uint32_t q_issued = 0, q_consumed = 0;
+  __device__ __forceinline__ void stage(const DevMsg* src, int n) {
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const int b = q_issued & 1;
+      bulk_copy(b ? sm.chunk1 : sm.chunk0, src, static_cast<uint32_t>(n * sizeof(DevMsg)),
+                b ? &sm.bar[1] : &sm.bar[0]);
+    }
+    ++q_issued;
+  }
+  __device__ __forceinline__ const DevMsg* staged() {
+    const int b = q_consumed & 1;
+    bar_wait(b ? &sm.bar[1] : &sm.bar[0], (q_consumed >> 1) & 1);
+    ++q_consumed;
+    return b ? sm.chunk1 : sm.chunk0;
+  }
   __device__ __forceinline__ void store_book() {
     hwm0 = store_side<0>();
     hwm1 = store_side<1>();
@@ -394,6 +458,8 @@ struct WarpEnv {
       const int n = sm.ag[a].n_active;
       if (lane < n) kp.active[(env * A + a) * kMaxActive + lane] = sm.act[a * kMaxActive + lane];
     }
+  }
+  __device__ __forceinline__ void report_errors() {
     if (err && lane == 0) atomicOr(kp.error, err);
   }
   __device__ __forceinline__ void load_agents() {
@@ -671,33 +737,29 @@ struct WarpEnv {
   }
 
   // Agent messages, then the replay slice staged in smem chunks (env.hpp:236-237).
+  // Chunk 0 (and 1) of this env were staged before the call; chunk c+2 is
+  // staged once chunk c is consumed.
   __device__ __forceinline__ void process_messages(int n_amsg, const DevMsg* slice) {
     const int mps = cfg.mps;
-    const int total = n_amsg + mps;
     const int nch = (mps + kChunk - 1) / kChunk;
-    const DevMsg* buf = sm.amsg;
-    int base = 0;  // index of buf[0] in the combined sequence
-    for (int i = 0; i < total; ++i) {
-      if (i >= n_amsg && (i - n_amsg) % kChunk == 0) {
-        const int c = (i - n_amsg) / kChunk;
-        if (c >= 1 && c + 1 < nch) {  // chunk c-1 consumed: refill its buffer with chunk c+1
-          __syncwarp();
-          if (lane == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            const int nb = (c + 1) & 1;
-            const int n2 = min(kChunk, mps - (c + 1) * kChunk);
-            bulk_copy(nb ? sm.chunk1 : sm.chunk0, slice + (c + 1) * kChunk, static_cast<uint32_t>(n2 * sizeof(DevMsg)),
-                      &sm.bar[nb]);
-          }
-        }
-        bar_wait(&sm.bar[c & 1], static_cast<uint32_t>((c >> 1) & 1));
-        buf = (c & 1) ? sm.chunk1 : sm.chunk0;
-        base = i;
+    for (int seg = -1; seg < nch; ++seg) {
+      const DevMsg* buf;
+      int n;
+      if (seg < 0) {
+        buf = sm.amsg;
+        n = n_amsg;
+      } else {
+        buf = staged();
+        n = min(kChunk, mps - seg * kChunk);
       }
-      const DevMsg m = buf[i - base];
-      run_message(m);
+#if MLOB_LDS_ASM
+      for (int i = 0; i < n; ++i) run_message(lds_msg(buf + i));
+#else
+      for (int i = 0; i < n; ++i) run_message(buf[i]);
+#endif
+      if (seg >= 0 && seg + 2 < nch) stage(slice + (seg + 2) * kChunk, min(kChunk, mps - (seg + 2) * kChunk));
     }
-    msgs += static_cast<uint64_t>(total);
+    msgs += static_cast<uint64_t>(n_amsg + mps);
     __syncwarp();  // lane 0's agent updates become visible to the warp
   }
 

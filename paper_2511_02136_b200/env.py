@@ -26,7 +26,7 @@ from .abi import (AgentAction, AgentInfo, AgentState, EnvConfig, EnvScalars, Epi
                   Message, RestingOrder, SynthConfig, Trade, VenvDesc)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmlob.so")
+LIB_PATH = os.environ.get("MLOB_LIB") or os.path.join(HERE, "libmlob.so")
 
 _EXC = {abi.MLOB_E_INVALID_ARGUMENT: ValueError, abi.MLOB_E_OUT_OF_RANGE: IndexError,
         abi.MLOB_E_LOGIC: RuntimeError, abi.MLOB_E_RUNTIME: RuntimeError,
