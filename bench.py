@@ -155,9 +155,13 @@ def gpu_arm(args) -> None:
     torch.cuda.set_device(dev)
 
     n_total, cfg, synth, label = workload(args.workload)
+    if args.mps:
+        cfg.messages_per_step = args.mps
+        synth.n_messages = (n_total + 64) * args.mps
+        synth.state_sample_every = args.mps
     if args.envs:
         n_total = args.envs
-        synth.n_messages = (n_total + 64) * 100
+        synth.n_messages = (n_total + 64) * cfg.messages_per_step
     per = n_total // world
     base = rank * per
     n_local = per if rank < world - 1 else n_total - base
@@ -306,6 +310,7 @@ def main():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--workload", default="E", choices=["B", "C", "E"])
     p.add_argument("--envs", type=int, default=0, help="override the env count")
+    p.add_argument("--mps", type=int, default=0, help="override messages per step (diagnostics)")
     p.add_argument("--ref-envs", type=int, default=65536)
     p.add_argument("--cpu-steps", type=int, default=8)
     p.add_argument("--e2e-steps", type=int, default=10)

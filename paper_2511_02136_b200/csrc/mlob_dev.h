@@ -64,7 +64,7 @@ struct DevSpec {
 
 struct DevCfg {
   int32_t steps_per_episode, mps, capacity, obs_depth;
-  int32_t n_specs, n_agents, max_obs_dim, _pad;
+  int32_t n_specs, n_agents, max_obs_dim, full_l2;  // full_l2: some agent uses MMFull levels
   int64_t fallback_mid_half;
   uint64_t synth_id_base, agent_id_base, agent_id_range;
   uint8_t flat_spec[kMaxAgents];

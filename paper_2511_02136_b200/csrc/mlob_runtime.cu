@@ -551,6 +551,7 @@ static void build_devcfg(mlob_venv& v) {
     }
     for (int k = 0; k < sp.count; ++k) d.flat_spec[a++] = static_cast<uint8_t>(s);
     maxdim = std::max(maxdim, ds.obs_dim);
+    if (sp.obs_space == MLOB_OBS_MM_FULL) d.full_l2 = 1;
   }
   d.n_agents = a;
   d.max_obs_dim = maxdim;

@@ -171,6 +171,15 @@ struct FillEnt {  // exact per-env fill log for the MM rewards (rewards.hpp:22-3
   int32_t agent;
   int32_t side;
 };
+struct ActTmp {  // one agent-owned resting order, rebuild_active scratch (fits a DevMsg slot)
+  int32_t price;
+  uint32_t st;
+  uint32_t lo, hi;
+  int32_t qty;
+  int32_t _pad;
+};
+static_assert(sizeof(ActTmp) <= sizeof(DevMsg), "ActTmp reuses the agent-message smem");
+
 struct L2Lvl {
   int32_t price;
   int32_t _pad;
@@ -305,6 +314,8 @@ struct WarpEnv {
   bool rec_trades;
   int n_agents;
   int nb_l2, na_l2;    // L2 levels staged in smem by snapshot()
+  int64_t topq0, topq1;  // level-0 aggregated qty per side
+  int64_t sumq0, sumq1;  // Σ qty over the top-D levels per side
 
   __device__ WarpEnv(const KParams& p, const WarpSmem& s, uint64_t e, int ln)
       : kp(p), cfg(p.cfg), sm(s), lane(ln), env(e) {
@@ -979,70 +990,73 @@ struct WarpEnv {
     return n;
   }
 
-  // env.hpp:398-407: active orders per agent, book storage order.
+  // env.hpp:398-407: active orders per agent, book storage order.  Agent
+  // slots are compacted into smem by ballot rank, then lane 0 sorts the few
+  // entries into storage order (bids worst->best, then asks) and deals them
+  // out to the agents.
   __device__ __forceinline__ void rebuild_active() {
     const int A = cfg.n_agents;
-    for (int a = lane; a < A; a += kWarp) sm.ag[a].n_active = 0;
+    ActTmp* tmp = reinterpret_cast<ActTmp*>(sm.amsg);  // agent messages are consumed
+    const int cap = 4 * A + 4;                          // DevMsg slots = ActTmp slots
+    int base = 0;
+    base = compact_side<0>(tmp, base, cap);
+    const int nbid = base;
+    base = compact_side<1>(tmp, base, cap);
     __syncwarp();
-    rebuild_side<0>();
-    rebuild_side<1>();
-  }
-  template <int S>
-  __device__ __forceinline__ void rebuild_side() {
-    SideT& d = sd<S>();
-    uint32_t taken = 0;  // per-lane bitmask of consumed rows
-    int cnt = 0;
-#pragma unroll
-    for (int k = 0; k < SPL; ++k) cnt += (d.Q(k) > 0 && (d.ST(k) & 0xffu) != 0) ? 1 : 0;
-    const int total = __reduce_add_sync(FULLMASK, static_cast<uint32_t>(cnt));
-    for (int i = 0; i < total; ++i) {
-      // first in storage order: bids lowest price, asks highest; then newest seq
-      int32_t lp = S == 0 ? INT_MAX : INT_MIN;
-#pragma unroll
-      for (int k = 0; k < SPL; ++k)
-        if (d.Q(k) > 0 && (d.ST(k) & 0xffu) != 0 && !((taken >> k) & 1u))
-          lp = S == 0 ? min(lp, d.P(k)) : max(lp, d.P(k));
-      const int32_t gp = S == 0 ? __reduce_min_sync(FULLMASK, lp) : __reduce_max_sync(FULLMASK, lp);
-      uint32_t ms = 0;
-      int lk = 0;
-      bool any = false;
-#pragma unroll
-      for (int k = 0; k < SPL; ++k) {
-        const bool c = d.Q(k) > 0 && (d.ST(k) & 0xffu) != 0 && !((taken >> k) & 1u) && d.P(k) == gp;
-        if (c && (!any || d.ST(k) > ms)) {
-          ms = d.ST(k);
-          lk = k;
-          any = true;
+    if (lane == 0) {
+      for (int a = 0; a < A; ++a) sm.ag[a].n_active = 0;
+      const int total = base < cap ? base : cap;
+      if (base > cap) err |= kErrActiveOverflow;
+      // insertion sort each side into storage order: bids (price asc, seq desc),
+      // asks (price desc, seq desc)
+      for (int i = 1; i < total; ++i) {
+        const ActTmp x = tmp[i];
+        const bool bid = i < nbid;
+        int j = i - 1;
+        const int lo = bid ? 0 : nbid;
+        while (j >= lo) {
+          const ActTmp y = tmp[j];
+          const bool after = y.price != x.price ? (bid ? y.price > x.price : y.price < x.price)
+                                                : (y.st >> 8) < (x.st >> 8);
+          if (!after) break;
+          tmp[j + 1] = y;
+          --j;
         }
+        tmp[j + 1] = x;
       }
-      const uint32_t gs = __reduce_max_sync(FULLMASK, any ? ms : 0u);
-      const int owner = __ffs(__ballot_sync(FULLMASK, any && ms == gs)) - 1;
-      if (lane == owner) taken |= 1u << lk;
-      int32_t q;
-      uint32_t lo, hi;
-      d.get_qid(lk, q, lo, hi);
-      q = __shfl_sync(FULLMASK, q, owner);
-      lo = __shfl_sync(FULLMASK, lo, owner);
-      hi = __shfl_sync(FULLMASK, hi, owner);
-      const int a = static_cast<int>(gs & 0xffu) - 1;
-      if (a >= cfg.n_agents) {
-        err |= kErrBadTrader;
-        continue;
-      }
-      const int n = sm.ag[a].n_active;
-      if (n >= kMaxActive) {
-        err |= kErrActiveOverflow;
-        continue;
-      }
-      __syncwarp();
-      if (lane == 0) {
+      for (int i = 0; i < total; ++i) {
+        const ActTmp x = tmp[i];
+        const int a = static_cast<int>(x.st & 0xffu) - 1;
+        if (a >= A) {
+          err |= kErrBadTrader;
+          continue;
+        }
+        const int n = sm.ag[a].n_active;
+        if (n >= kMaxActive) {
+          err |= kErrActiveOverflow;
+          continue;
+        }
         sm.act[a * kMaxActive + n] =
-            ActiveRec{(static_cast<uint64_t>(hi) << 32) | lo, gp,
-                      static_cast<uint32_t>(q) | (static_cast<uint32_t>(S) << 31)};
+            ActiveRec{(static_cast<uint64_t>(x.hi) << 32) | x.lo, x.price,
+                      static_cast<uint32_t>(x.qty) | (static_cast<uint32_t>(i >= nbid) << 31)};
         sm.ag[a].n_active = n + 1;
       }
-      __syncwarp();
     }
+    __syncwarp();
+  }
+  template <int S>
+  __device__ __forceinline__ int compact_side(ActTmp* tmp, int base, int cap) {
+    SideT& d = sd<S>();
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      const bool is_ag = d.Q(k) > 0 && (d.ST(k) & 0xffu) != 0;
+      const uint32_t b = __ballot_sync(FULLMASK, is_ag);
+      if (b == 0) continue;
+      const int pos = base + __popc(b & ((1u << lane) - 1u));
+      if (is_ag && pos < cap) tmp[pos] = ActTmp{d.P(k), d.ST(k), d.LO(k), d.HI(k), d.Q(k), 0};
+      base += __popc(b);
+    }
+    return base;
   }
 
   // env.hpp:435-443
@@ -1143,9 +1157,7 @@ struct WarpEnv {
       const int64_t bb = live0 > 0 ? best0 : -1;
       const int64_t ba = live1 > 0 ? best1 : -1;
       const double time_frac = static_cast<double>(step) / static_cast<double>(cfg.steps_per_episode);
-      int64_t bq = 0, aq = 0;
-      for (int i = 0; i < nb; ++i) bq += l2b[i].qty;
-      for (int i = 0; i < na; ++i) aq += l2a[i].qty;
+      const int64_t bq = sumq0, aq = sumq1;
       const double imb = bq + aq == 0 ? 0.0 : static_cast<double>(bq - aq) / static_cast<double>(bq + aq);
       const double spread = (bb < 0 || ba < 0) ? 0.0 : fmin_ref(32.0, static_cast<double>(ba - bb));
       int64_t own_bid = -1, own_ask = -1;
@@ -1168,8 +1180,8 @@ struct WarpEnv {
         out[4] = dmid;
         out[5] = static_cast<double>(mid_half) / 2.0 - st.p_init;
         out[6] = imb;
-        out[7] = nb > 0 ? qty_feature(l2b[0].qty, sp.order_size) : 0.0;
-        out[8] = na > 0 ? qty_feature(l2a[0].qty, sp.order_size) : 0.0;
+        out[7] = nb > 0 ? qty_feature(topq0, sp.order_size) : 0.0;
+        out[8] = na > 0 ? qty_feature(topq1, sp.order_size) : 0.0;
         const bool buy = dir > 0;
         out[9] = offset_feature(buy ? own_bid : own_ask, buy ? bb : ba, buy);
         for (int j = 10; j < dim; ++j) out[j] = 0.0;  // MMFull-sized executor obs
@@ -1213,8 +1225,70 @@ struct WarpEnv {
   // subroutine calls of the reward/observation code (they forced the book
   // through local memory in v1).
   __device__ __forceinline__ void snapshot() {
+    if (!cfg.full_l2 && summarize_l2<0>() && summarize_l2<1>()) return;
     nb_l2 = l2_levels<0>(sm.l2);
     na_l2 = l2_levels<1>(sm.l2 + cfg.obs_depth);
+    sumq0 = sumq1 = topq0 = topq1 = 0;
+    for (int i = 0; i < nb_l2; ++i) sumq0 += sm.l2[i].qty;
+    for (int i = 0; i < na_l2; ++i) sumq1 += sm.l2[cfg.obs_depth + i].qty;
+    topq0 = nb_l2 > 0 ? sm.l2[0].qty : 0;
+    topq1 = na_l2 > 0 ? sm.l2[cfg.obs_depth].qty : 0;
+  }
+
+  // Warp-sum of a per-lane value < 2^36 (16-bit split keeps redux.sync exact).
+  __device__ __forceinline__ int64_t warp_sum64(uint64_t v) {
+    const uint32_t lo = __reduce_add_sync(FULLMASK, static_cast<uint32_t>(v & 0xffffu));
+    const uint32_t hi = __reduce_add_sync(FULLMASK, static_cast<uint32_t>(v >> 16));
+    return static_cast<int64_t>(lo) + (static_cast<int64_t>(hi) << 16);
+  }
+
+  // Observation inputs without materialising the levels (MMBasic/Exec spaces):
+  // the distinct prices within 32 ticks of the touch form one bitmask; if the
+  // window holds the top D levels (or the whole side), the level count, the
+  // top-D quantity and the touch quantity follow from two masked sums.
+  template <int S>
+  __device__ __forceinline__ bool summarize_l2() {
+    SideT& d = sd<S>();
+    const int live = S ? live1 : live0;
+    const int32_t best = S ? best1 : best0;
+    if (live == 0) {
+      (S ? na_l2 : nb_l2) = 0;
+      (S ? sumq1 : sumq0) = 0;
+      (S ? topq1 : topq0) = 0;
+      return true;
+    }
+    uint32_t m = 0;
+    bool far = false;
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      if (d.Q(k) > 0) {
+        const uint32_t off = static_cast<uint32_t>(S == 0 ? best - d.P(k) : d.P(k) - best);
+        if (off < 32)
+          m |= 1u << off;
+        else
+          far = true;
+      }
+    }
+    const uint32_t mask = __reduce_or_sync(FULLMASK, m);
+    const int D = cfg.obs_depth;
+    const int nl = __popc(mask);
+    if (nl < D && __any_sync(FULLMASK, far)) return false;  // levels beyond the window: slow path
+    const int n = nl < D ? nl : D;
+    uint32_t mm = mask;
+    for (int i = 1; i < n; ++i) mm &= mm - 1;
+    const uint32_t cut = static_cast<uint32_t>(__ffs(mm) - 1);  // offset of the n-th level
+    uint64_t sa = 0, st = 0;
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      const uint32_t off = static_cast<uint32_t>(S == 0 ? best - d.P(k) : d.P(k) - best);
+      const uint32_t q = d.Q(k) > 0 ? static_cast<uint32_t>(d.Q(k)) : 0u;
+      sa += off <= cut ? q : 0u;
+      st += off == 0 ? q : 0u;
+    }
+    (S ? na_l2 : nb_l2) = n;
+    (S ? sumq1 : sumq0) = warp_sum64(sa);
+    (S ? topq1 : topq0) = warp_sum64(st);
+    return true;
   }
 
   __device__ __forceinline__ void outcomes(bool write_rewards) {
