@@ -118,7 +118,7 @@ enum DevError : uint32_t {
   kErrBadTrader = 1u << 6,      // replay trader_id names a non-existent agent
 };
 
-struct KParams {
+struct __align__(16) KParams {
   // store (read-only, shared by every handle on the device)
   const DevMsg* msgs;
   const uint64_t* ep_start;
@@ -154,6 +154,7 @@ struct KParams {
   uint32_t fill_overflows_unused;
   unsigned long long* fill_overflow;  // count of env-steps whose MM fill log overflowed
   unsigned long long* ticket;         // persistent step kernel: next-env ticket counter
+  long long* timing;                  // MLOB_PHASE_TIMING builds: [env][16] clock64 stamps
   // env identity / episode pool
   const uint64_t* env_seed;   // optional
   const uint64_t* env_index;  // optional
@@ -162,7 +163,7 @@ struct KParams {
   uint64_t pool_len, n_envs_global, n_envs;
   const uint64_t* reset_episodes;  // reset kernel: per-env episode
   uint32_t* error;
-  DevCfg cfg;
+  const DevCfg* cfg;  // device copy; staged into shared memory by each block
 };
 
 }  // namespace mlob

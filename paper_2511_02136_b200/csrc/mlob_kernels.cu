@@ -56,6 +56,18 @@ constexpr int kWarpsPerBlock = 4;
 #define MLOB_MIN_BLOCKS 4
 #endif
 
+#ifdef MLOB_PHASE_TIMING
+#define PHASE(i)                                                               \
+  do {                                                                         \
+    __syncwarp();                                                              \
+    if (lane == 0 && kp.timing) kp.timing[env * 16 + (i)] = clock64();         \
+  } while (0)
+#else
+#define PHASE(i) \
+  do {           \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -65,10 +77,33 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 // rollout.hpp:290-318).  While env e is processed, the next env's first
 // replay chunk is already in flight (cp.async.bulk) and its header, agent
 // records and book rows are prefetched into L2.
+// Kernel parameters and the env config are staged into shared memory once
+// per block: reading them through a reference to the __grid_constant__
+// parameter compiled to slow generic loads (profiles/r1 phase timing).
+struct StagedParams {
+  KParams kp;
+  DevCfg cfg;
+};
+__device__ __forceinline__ void stage_params(StagedParams& sp, const KParams& kp) {
+  const int4* a = reinterpret_cast<const int4*>(&kp);
+  int4* d = reinterpret_cast<int4*>(&sp.kp);
+  for (int i = threadIdx.x; i < static_cast<int>(sizeof(KParams) / 16); i += blockDim.x) d[i] = a[i];
+  const int n_specs = kp.cfg->n_specs;
+  const int bytes = static_cast<int>(offsetof(DevCfg, specs) + n_specs * sizeof(DevSpec));
+  const int4* c = reinterpret_cast<const int4*>(kp.cfg);
+  int4* dc = reinterpret_cast<int4*>(&sp.cfg);
+  for (int i = threadIdx.x; i < (bytes + 15) / 16; i += blockDim.x) dc[i] = c[i];
+  __syncthreads();
+}
+static_assert(sizeof(KParams) % 16 == 0, "KParams must be int4-copyable");
+
 template <int SPL>
 __global__ void __launch_bounds__(kWarpsPerBlock * kWarp, MLOB_MIN_BLOCKS)
-    step_kernel(const __grid_constant__ KParams kp) {
+    step_kernel(const __grid_constant__ KParams kparam) {
   extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(16) StagedParams sp_;
+  stage_params(sp_, kparam);
+  const KParams& kp = sp_.kp;
   const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarpsPerBlock;
   // dynamic work distribution: the first env of each warp is static, later
@@ -81,9 +116,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp, MLOB_MIN_BLOCKS)
     if (lane == 0) t = atomicAdd(kp.ticket, 1ull);
     return stride + __shfl_sync(FULLMASK, t, 0);
   };
-  const DevCfg& cfg = kp.cfg;
+  const DevCfg& cfg = sp_.cfg;
   WarpSmem sm = carve(smem + warp * warp_smem_bytes(cfg), cfg);
-  WarpEnv<SPL> w(kp, sm, first, lane);
+  WarpEnv<SPL> w(kp, cfg, sm, first, lane);
   const int mps = cfg.mps;
   const int nch = (mps + kChunk - 1) / kChunk;
   const int A = cfg.n_agents;
@@ -102,6 +137,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp, MLOB_MIN_BLOCKS)
   uint64_t nenv = MLOB_PERSIST ? ticket() : kp.n_envs;
   for (uint64_t env = first; env < kp.n_envs;) {
     w.bind(env);
+    PHASE(0);
     w.load_hdr();
     const DevMsg* slice = kp.msgs + kp.ep_start[w.episode] + static_cast<uint64_t>(w.step) * mps;
     if (nch >= 2) w.stage(slice + kChunk, min(kChunk, mps - kChunk));
@@ -129,6 +165,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp, MLOB_MIN_BLOCKS)
     w.load_agents();
     w.clear_step_acc();
     const int64_t step_time = mps > 0 ? slice[0].time : w.last_time + 1;
+    PHASE(1);
 
     // (1) actions -> agent messages, (2) Fisher-Yates (rng.hpp:63-71)
     int n_amsg = 0;
@@ -151,6 +188,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp, MLOB_MIN_BLOCKS)
       }
     }
     __syncwarp();
+    PHASE(2);
     // book registers are loaded only now: nothing above needs them (tops are
     // in the header) and they must not be live across subroutine calls
     w.load_book();
@@ -160,7 +198,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp, MLOB_MIN_BLOCKS)
     w.mid_sum = 0;
     w.mid_count = 0;
     w.n_trades = 0;
+    PHASE(3);
     w.process_messages(n_amsg, slice);
+    PHASE(4);
     if (has_next && mps > 0) w.stage(next_slice, min(kChunk, mps));  // overlaps the outcomes
     if (w.live0 > 0) w.last_bid = w.best0;
     if (w.live1 > 0) w.last_ask = w.best1;
@@ -170,13 +210,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp, MLOB_MIN_BLOCKS)
                              : static_cast<double>(w.prev_mid_half) / 2.0;
     if (sm.scal[1] && lane == 0) atomicAdd(kp.fill_overflow, 1ull);
     w.rebuild_active();
+    PHASE(5);
     ++w.step;
     w.terminal = w.step >= cfg.steps_per_episode;
     uint8_t just_reset = 0;
     for (int pass = 0;; ++pass) {  // pass 1: the auto-reset env's fresh outputs
       w.snapshot();
+      if (pass == 0) PHASE(6);
       w.store_book();  // book registers dead from here on
+      if (pass == 0) PHASE(7);
       w.outcomes(pass == 0);
+      if (pass == 0) PHASE(8);
       if (pass > 0 || !(w.terminal && (kp.flags & MLOB_VENV_AUTO_RESET))) break;
       if (lane == 0)
         for (int a = 0; a < A; ++a) {  // rollout.hpp:300-313
@@ -198,6 +242,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp, MLOB_MIN_BLOCKS)
       just_reset = 1;
     }
     w.store_state(just_reset);
+    PHASE(9);
     env = nenv;
     if (has_next) nenv = ticket();
   }
@@ -207,14 +252,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp, MLOB_MIN_BLOCKS)
 // K3: MarketEnv::reset for every env (reset_all / reset_envs).
 template <int SPL>
 __global__ void __launch_bounds__(kWarpsPerBlock * kWarp)
-    reset_kernel(const __grid_constant__ KParams kp) {
+    reset_kernel(const __grid_constant__ KParams kparam) {
   extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(16) StagedParams sp_;
+  stage_params(sp_, kparam);
+  const KParams& kp = sp_.kp;
   const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
   const uint64_t env = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + warp;
   if (env >= kp.n_envs) return;
-  const DevCfg& cfg = kp.cfg;
+  const DevCfg& cfg = sp_.cfg;
   WarpSmem sm = carve(smem + warp * warp_smem_bytes(cfg), cfg);
-  WarpEnv<SPL> w(kp, sm, env, lane);
+  WarpEnv<SPL> w(kp, cfg, sm, env, lane);
   w.load_hdr();  // keeps last_time / messages_processed across resets
   w.load_agents();
   w.load_book();
@@ -234,7 +282,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp)
 // all-reduce), 5 doubles per type: pv, slip, completion, inv², episodes.
 __global__ void stats_kernel(const __grid_constant__ KParams kp, double* out) {
   const int t = blockIdx.y;
-  const DevCfg& cfg = kp.cfg;
+  const DevCfg& cfg = *kp.cfg;
   const int A = cfg.n_agents;
   const int cnt = cfg.specs[t].count, off = cfg.specs[t].flat_offset;
   double s[5] = {0, 0, 0, 0, 0};
@@ -273,7 +321,7 @@ __global__ void clear_finished_kernel(EnvHdr* hdr, uint64_t n) {
 // ---------------------------------------------------------------------------
 // host-side launchers
 
-size_t step_smem_bytes(const DevCfg& c) { return warp_smem_bytes(c) * kWarpsPerBlock; }
+size_t step_smem_bytes(const DevCfg& c) { return warp_smem_bytes(c) * kWarpsPerBlock; }  // dynamic part
 
 static unsigned grid_for(uint64_t n) {
   const uint64_t b = (n + 255) / 256;
@@ -281,8 +329,8 @@ static unsigned grid_for(uint64_t n) {
 }
 
 template <int SPL>
-static cudaError_t launch_step_t(const KParams& kp, cudaStream_t s) {
-  const size_t sm = step_smem_bytes(kp.cfg);
+static cudaError_t launch_step_t(const KParams& kp, const DevCfg& cfg, cudaStream_t s) {
+  const size_t sm = step_smem_bytes(cfg);
   cudaError_t e = cudaFuncSetAttribute(step_kernel<SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sm));
   if (e != cudaSuccess) return e;
@@ -301,8 +349,8 @@ static cudaError_t launch_step_t(const KParams& kp, cudaStream_t s) {
 }
 
 template <int SPL>
-static cudaError_t launch_reset_t(const KParams& kp, cudaStream_t s) {
-  const size_t sm = step_smem_bytes(kp.cfg);
+static cudaError_t launch_reset_t(const KParams& kp, const DevCfg& cfg, cudaStream_t s) {
+  const size_t sm = step_smem_bytes(cfg);
   cudaError_t e = cudaFuncSetAttribute(reset_kernel<SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sm));
   if (e != cudaSuccess) return e;
@@ -320,30 +368,30 @@ int slots_per_lane(int capacity) {
   return -1;
 }
 
-cudaError_t launch_step(const KParams& kp, int spl, cudaStream_t s) {
+cudaError_t launch_step(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s) {
   switch (spl) {
-    case 1: return launch_step_t<1>(kp, s);
-    case 2: return launch_step_t<2>(kp, s);
-    case 4: return launch_step_t<4>(kp, s);
-    case 8: return launch_step_t<8>(kp, s);
+    case 1: return launch_step_t<1>(kp, cfg, s);
+    case 2: return launch_step_t<2>(kp, cfg, s);
+    case 4: return launch_step_t<4>(kp, cfg, s);
+    case 8: return launch_step_t<8>(kp, cfg, s);
   }
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_reset(const KParams& kp, int spl, cudaStream_t s) {
+cudaError_t launch_reset(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s) {
   switch (spl) {
-    case 1: return launch_reset_t<1>(kp, s);
-    case 2: return launch_reset_t<2>(kp, s);
-    case 4: return launch_reset_t<4>(kp, s);
-    case 8: return launch_reset_t<8>(kp, s);
+    case 1: return launch_reset_t<1>(kp, cfg, s);
+    case 2: return launch_reset_t<2>(kp, cfg, s);
+    case 4: return launch_reset_t<4>(kp, cfg, s);
+    case 8: return launch_reset_t<8>(kp, cfg, s);
   }
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_stats(const KParams& kp, double* out, cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double) * 5 * kp.cfg.n_specs, s);
+cudaError_t launch_stats(const KParams& kp, const DevCfg& cfg, double* out, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double) * 5 * cfg.n_specs, s);
   if (e != cudaSuccess) return e;
-  stats_kernel<<<dim3(grid_for(kp.n_envs), kp.cfg.n_specs), 256, 0, s>>>(kp, out);
+  stats_kernel<<<dim3(grid_for(kp.n_envs), cfg.n_specs), 256, 0, s>>>(kp, out);
   return cudaGetLastError();
 }
 

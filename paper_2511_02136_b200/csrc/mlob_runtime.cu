@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -17,9 +18,9 @@
 namespace mlob {
 size_t step_smem_bytes(const DevCfg& c);
 int slots_per_lane(int capacity);
-cudaError_t launch_step(const KParams& kp, int spl, cudaStream_t s);
-cudaError_t launch_reset(const KParams& kp, int spl, cudaStream_t s);
-cudaError_t launch_stats(const KParams& kp, double* out, cudaStream_t s);
+cudaError_t launch_step(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s);
+cudaError_t launch_reset(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s);
+cudaError_t launch_stats(const KParams& kp, const DevCfg& cfg, double* out, cudaStream_t s);
 cudaError_t launch_sum_msgs(const EnvHdr* hdr, uint64_t n, unsigned long long* out, cudaStream_t s);
 cudaError_t launch_clear_finished(EnvHdr* hdr, uint64_t n, cudaStream_t s);
 }  // namespace mlob
@@ -138,6 +139,8 @@ struct mlob_venv {
   uint32_t* d_error = nullptr;
   unsigned long long* d_scratch = nullptr;
   unsigned long long* d_ticket = nullptr;
+  long long* d_timing = nullptr;
+  DevCfg* d_cfg = nullptr;
 
   template <class T>
   T* alloc(size_t n, const char* what) {
@@ -184,6 +187,7 @@ struct mlob_venv {
     k.trade_cap = trade_cap;
     k.fill_overflow = d_fill_overflow;
     k.ticket = d_ticket;
+    k.timing = d_timing;
     k.env_seed = d_env_seed;
     k.env_index = d_env_index;
     k.seed = seed;
@@ -194,7 +198,7 @@ struct mlob_venv {
     k.n_envs = n_envs;
     k.reset_episodes = d_reset_eps;
     k.error = d_error;
-    k.cfg = dcfg;
+    k.cfg = d_cfg;
     return k;
   }
 
@@ -634,6 +638,8 @@ mlob_status mlob_venv_create(const mlob_venv_desc* desc, mlob_venv** out) {
     }
     const uint64_t n = v->n_envs;
     const uint64_t slots = n * 2 * v->spl * kWarp;
+    v->d_cfg = v->alloc<DevCfg>(1, "cfg");
+    cuda_check(cudaMemcpy(v->d_cfg, &v->dcfg, sizeof(DevCfg), cudaMemcpyHostToDevice), "H2D cfg");
     v->d_ep_start = v->alloc<uint64_t>(v->starts.size(), "ep_start");
     v->d_ep_state = v->alloc<EpState>(v->ep_state.size(), "ep_state");
     cuda_check(cudaMemcpy(v->d_ep_start, v->starts.data(), v->starts.size() * 8, cudaMemcpyHostToDevice), "H2D");
@@ -662,6 +668,7 @@ mlob_status mlob_venv_create(const mlob_venv_desc* desc, mlob_venv** out) {
     v->d_fill_overflow = v->alloc<unsigned long long>(1, "fill_overflow");
     v->d_scratch = v->alloc<unsigned long long>(8, "scratch");
     v->d_ticket = v->alloc<unsigned long long>(1, "ticket");
+    if (std::getenv("MLOB_TIMING")) v->d_timing = v->alloc<long long>(n * 16, "timing");
     v->d_reset_eps = v->alloc<uint64_t>(n, "reset_eps");
     v->d_error = v->alloc<uint32_t>(1, "error");
     if (desc->env_seeds) {
@@ -699,7 +706,7 @@ static void do_reset(mlob_venv* v, const std::vector<uint64_t>& eps) {
              "H2D");
   cuda_check(cudaStreamSynchronize(v->stream), "sync");  // eps is a host temporary
   const KParams kp = v->params();
-  cuda_check(launch_reset(kp, v->spl, v->stream), "reset kernel");
+  cuda_check(launch_reset(kp, v->dcfg, v->spl, v->stream), "reset kernel");
   ++v->launches;
   std::fill(v->steps.begin(), v->steps.end(), 0);
 }
@@ -775,7 +782,7 @@ static void do_step(mlob_venv* v, int mode, uint64_t bench_seed, uint64_t global
   kp.bench_seed = bench_seed;
   kp.global_step = global_step;
   cuda_check(cudaMemsetAsync(v->d_ticket, 0, sizeof(unsigned long long), v->stream), "ticket reset");
-  cuda_check(launch_step(kp, v->spl, v->stream), "step kernel");
+  cuda_check(launch_step(kp, v->dcfg, v->spl, v->stream), "step kernel");
   ++v->launches;
   for (auto& s : v->steps) {
     ++s;
@@ -892,7 +899,7 @@ mlob_status mlob_venv_episode_stats(mlob_venv* v, int type, mlob_episode_stats* 
 mlob_status mlob_venv_episode_stats_device(mlob_venv* v, double* out_device) {
   return guarded([&] {
     v->set_device();
-    cuda_check(launch_stats(v->params(), out_device, v->stream), "stats kernel");
+    cuda_check(launch_stats(v->params(), v->dcfg, out_device, v->stream), "stats kernel");
     ++v->launches;
   });
 }
@@ -1012,6 +1019,13 @@ mlob_status mlob_venv_read_trades(mlob_venv* v, uint64_t env, mlob_trade* out, u
                                std::to_string(v->trade_cap));
     const uint64_t n = std::min<uint64_t>(h.n_trades, cap);
     if (n) d2h(v, out, v->d_trades + env * v->trade_cap, n);
+  });
+}
+
+mlob_status mlob_venv_read_timing(mlob_venv* v, long long* out) {
+  return guarded([&] {
+    if (!v->d_timing) fail(MLOB_E_LOGIC, "timing buffer not allocated (set MLOB_TIMING)");
+    d2h(v, out, v->d_timing, v->n_envs * 16);
   });
 }
 

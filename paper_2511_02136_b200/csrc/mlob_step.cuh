@@ -317,13 +317,13 @@ struct WarpEnv {
   int64_t topq0, topq1;  // level-0 aggregated qty per side
   int64_t sumq0, sumq1;  // Σ qty over the top-D levels per side
 
-  __device__ WarpEnv(const KParams& p, const WarpSmem& s, uint64_t e, int ln)
-      : kp(p), cfg(p.cfg), sm(s), lane(ln), env(e) {
+  __device__ WarpEnv(const KParams& p, const DevCfg& c, const WarpSmem& s, uint64_t e, int ln)
+      : kp(p), cfg(c), sm(s), lane(ln), env(e) {
     bind(e);
     err = 0;
-    capacity = p.cfg.capacity;
+    capacity = c.capacity;
     rec_trades = (p.flags & MLOB_VENV_RECORD_TRADES) != 0;
-    n_agents = p.cfg.n_agents;
+    n_agents = c.n_agents;
   }
 
   __device__ __forceinline__ void bind(uint64_t e) {
