@@ -701,7 +701,7 @@ struct WarpEnv {
   }
 
   // book.hpp:189-207 (reduce_order / remove_order); absent ids are no-ops.
-  __device__ __forceinline__ void by_id(const DevMsg& m, bool remove) {
+  __device__ __forceinline__ bool by_id(const DevMsg& m, bool remove) {
     const int s = m.side;
     const uint32_t lo = static_cast<uint32_t>(m.order_id), hi = static_cast<uint32_t>(m.order_id >> 32);
     int nm, lk;
@@ -710,7 +710,7 @@ struct WarpEnv {
     else
       scan_id_t<0>(lo, hi, nm, lk);
     const uint32_t b = __ballot_sync(FULLMASK, nm > 0);
-    if (b == 0) return;
+    if (b == 0) return false;
     int owner = __ffs(b) - 1;
     if (__reduce_add_sync(FULLMASK, static_cast<uint32_t>(nm)) != 1)
       owner = s ? dup_owner_t<1>(lo, hi, lk) : dup_owner_t<0>(lo, hi, lk);
@@ -727,24 +727,31 @@ struct WarpEnv {
       } else {
         if (--live0 > 0 && p == best0) best0 = side_best_t<0>();
       }
-    } else {
-      slot_setq(s, lk, me, nq);
+      return true;
     }
+    slot_setq(s, lk, me, nq);
+    return false;
   }
 
-  // book.hpp:65-86 + env.hpp:223-235
+  // env.hpp:230: the mid follows the tops; it is refreshed only on the paths
+  // that can move a top (any NewLimit, removals), not per message.
+  __device__ __forceinline__ void refresh_mid() {
+    const int64_t b0 = best0, b1 = best1;
+    mid_half = live0 > 0 ? (live1 > 0 ? b0 + b1 : 2 * b0) : (live1 > 0 ? 2 * b1 : mid_half);
+  }
+
+  // book.hpp:65-86 + env.hpp:223-235 (mid_count / last_time / messages are
+  // derived once after the loop: they only depend on the message count).
   __device__ __forceinline__ void run_message(const DevMsg& m) {
     if (m.kind == MLOB_NEW_LIMIT) {
-      if (m.qty > 0) new_limit(m);
+      if (m.qty > 0) {
+        new_limit(m);
+        refresh_mid();
+      }
     } else if (m.kind <= MLOB_EXECUTE_VISIBLE) {
-      by_id(m, m.kind == MLOB_DELETE);
+      if (by_id(m, m.kind == MLOB_DELETE)) refresh_mid();
     }
-    const bool hb = live0 > 0, ha = live1 > 0;
-    const int64_t b0 = best0, b1 = best1;
-    mid_half = hb ? (ha ? b0 + b1 : 2 * b0) : (ha ? 2 * b1 : mid_half);
     mid_sum += mid_half;
-    ++mid_count;
-    last_time = m.time;
   }
 
   // Agent messages, then the replay slice staged in smem chunks (env.hpp:236-237).
@@ -770,7 +777,10 @@ struct WarpEnv {
 #endif
       if (seg >= 0 && seg + 2 < nch) stage(slice + (seg + 2) * kChunk, min(kChunk, mps - (seg + 2) * kChunk));
     }
-    msgs += static_cast<uint64_t>(n_amsg + mps);
+    const int total = n_amsg + mps;
+    msgs += static_cast<uint64_t>(total);
+    mid_count = total;
+    if (total > 0) last_time = mps > 0 ? slice[mps - 1].time : lds_msg(sm.amsg + n_amsg - 1).time;
     __syncwarp();  // lane 0's agent updates become visible to the warp
   }
 
