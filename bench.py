@@ -30,7 +30,7 @@ UNIT = "msg-steps/s"
 # Algorithmic bytes per message-level step, SURVEY.md §8(d) / DESIGN.md
 # ("Roofline"): book slots r+w, replay message read, env/agent state r+w,
 # outputs; per config.
-B_MSG = {"B": 171.4, "C": 169.1, "E": 169.1}
+B_MSG = {"B": 171.4, "C": 169.1, "D": 1431.0, "E": 169.1}
 HBM_FALLBACK = 6650.0
 
 
@@ -40,6 +40,13 @@ def workload(name: str):
     from paper_2511_02136_b200 import abi
     ex = abi.agent_spec(abi.EXECUTOR)
     mm = abi.agent_spec(abi.MARKET_MAKER)
+    if name == "D":  # deep book: SURVEY §8d config D (trimmed store, 64 full episodes)
+        cfg = abi.env_config([mm, ex], steps_per_episode=64, messages_per_step=100,
+                             start_stride_steps=64, book_capacity=1000)
+        synth = abi.synth_config(n_messages=80 * 6400, state_sample_every=6400, initial_mid=100000,
+                                 band=2000, p_new_passive=0.46, p_new_cross=0.04, p_cancel=0.30,
+                                 p_delete=0.16, p_execute=0.02, state_depth=1000)
+        return 262144, cfg, synth, "D: 262144 envs, two-agent, deep book (capacity 1000, 2000 live orders)"
     n_envs, specs, label = {
         "B": (4096, [ex], "B: 4096 envs, single execution agent"),
         "C": (65536, [mm, ex], "C: 65536 envs, two-agent (market maker + execution)"),
@@ -109,8 +116,15 @@ def cpu_reference_run(n_envs_cap: int, steps: int, warmup: int, name: str):
     n_envs, cfg, synth, label = workload(name)
     n = min(n_envs, n_envs_cap)
     from paper_2511_02136_b200 import abi
-    small = abi.synth_config(n_messages=(n + 64) * 100, state_sample_every=100)
-    store = o.synth(small, 0)   # the same stream's prefix: identical episodes 0..n
+    if name == "D":
+        from oracle.oracle import OStore
+        full = o.synth(synth, 0)
+        msgs = full.messages()[16 * 6400:]
+        states = [(i - 16 * 6400, b, a) for i, b, a in full.states() if i >= 16 * 6400]
+        store = o.store_from(msgs, states)
+    else:
+        small = abi.synth_config(n_messages=(n + 64) * 100, state_sample_every=100)
+        store = o.synth(small, 0)   # the same stream's prefix: identical episodes 0..n
     workers = os.cpu_count() or 1
     row = bench_run(o, store, cfg, n, steps, warmup, workers, 0, 100, 1)
     return row, workers, n, label
@@ -167,6 +181,8 @@ def gpu_arm(args) -> None:
     n_local = per if rank < world - 1 else n_total - base
     t0 = time.time()
     hs = HostStore.synth(synth, 0)
+    if args.workload == "D":
+        hs.trim_front(16 * 6400)  # every remaining episode starts with a full 1000-level book
     gen_s = time.time() - t0
     store = DeviceStore(hs, dev)
     del hs
@@ -308,7 +324,7 @@ def main():
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--workload", default="E", choices=["B", "C", "E"])
+    p.add_argument("--workload", default="E", choices=["B", "C", "D", "E"])
     p.add_argument("--envs", type=int, default=0, help="override the env count")
     p.add_argument("--mps", type=int, default=0, help="override messages per step (diagnostics)")
     p.add_argument("--ref-envs", type=int, default=65536)

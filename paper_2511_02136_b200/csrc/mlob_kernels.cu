@@ -6,6 +6,14 @@
 
 namespace mlob {
 
+__host__ __device__ inline int spl_of(int capacity) {
+  const int need = (capacity + kWarp - 1) / kWarp;
+  return need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : need <= 8 ? 8 : need <= 16 ? 16 : need <= 32 ? 32 : -1;
+}
+__host__ __device__ inline size_t book_smem_bytes(int capacity) {
+  return static_cast<size_t>(2) * 5 * spl_of(capacity) * kWarp * sizeof(uint32_t);
+}
+
 __host__ __device__ inline size_t warp_smem_bytes(const DevCfg& c) {
   const int chunk = c.mps < kChunk ? c.mps : kChunk;
   const int nbuf = c.mps > kChunk ? 2 : 1;
@@ -20,6 +28,8 @@ __host__ __device__ inline size_t warp_smem_bytes(const DevCfg& c) {
   b += 16;  // scalars
   b += static_cast<size_t>(2 * c.obs_depth) * sizeof(L2Lvl);
   b += static_cast<size_t>(c.max_obs_dim + 1) * sizeof(double);
+  b = (b + 15) / 16 * 16;
+  if (c.capacity > 8 * kWarp) b += book_smem_bytes(c.capacity);  // deep book lives in smem
   return (b + 127) / 128 * 128;
 }
 
@@ -49,6 +59,13 @@ __device__ WarpSmem carve(char* base, const DevCfg& c) {
   p += static_cast<size_t>(2 * c.obs_depth) * sizeof(L2Lvl);
   s.obs = reinterpret_cast<double*>(p);
   return s;
+}
+
+// deep-book smem region of a warp (after the WarpSmem carve-out)
+__device__ inline uint32_t* book_region(char* base, const DevCfg& c) {
+  size_t b = warp_smem_bytes(c) - ((c.capacity > 8 * kWarp) ? book_smem_bytes(c.capacity) : 0);
+  b = b / 16 * 16;
+  return reinterpret_cast<uint32_t*>(base + b);
 }
 
 constexpr int kWarpsPerBlock = 4;
@@ -117,8 +134,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp, MLOB_MIN_BLOCKS)
     return stride + __shfl_sync(FULLMASK, t, 0);
   };
   const DevCfg& cfg = sp_.cfg;
-  WarpSmem sm = carve(smem + warp * warp_smem_bytes(cfg), cfg);
-  WarpEnv<SPL> w(kp, cfg, sm, first, lane);
+  char* wbase = smem + warp * warp_smem_bytes(cfg);
+  WarpSmem sm = carve(wbase, cfg);
+  WarpEnv<SPL> w(kp, cfg, sm, first, lane, book_region(wbase, cfg));
   const int mps = cfg.mps;
   const int nch = (mps + kChunk - 1) / kChunk;
   const int A = cfg.n_agents;
@@ -261,8 +279,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp)
   const uint64_t env = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + warp;
   if (env >= kp.n_envs) return;
   const DevCfg& cfg = sp_.cfg;
-  WarpSmem sm = carve(smem + warp * warp_smem_bytes(cfg), cfg);
-  WarpEnv<SPL> w(kp, cfg, sm, env, lane);
+  char* wbase = smem + warp * warp_smem_bytes(cfg);
+  WarpSmem sm = carve(wbase, cfg);
+  WarpEnv<SPL> w(kp, cfg, sm, env, lane, book_region(wbase, cfg));
   w.load_hdr();  // keeps last_time / messages_processed across resets
   w.load_agents();
   w.load_book();
@@ -359,14 +378,7 @@ static cudaError_t launch_reset_t(const KParams& kp, const DevCfg& cfg, cudaStre
   return cudaGetLastError();
 }
 
-int slots_per_lane(int capacity) {
-  const int need = (capacity + kWarp - 1) / kWarp;
-  if (need <= 1) return 1;
-  if (need <= 2) return 2;
-  if (need <= 4) return 4;
-  if (need <= 8) return 8;
-  return -1;
-}
+int slots_per_lane(int capacity) { return spl_of(capacity); }
 
 cudaError_t launch_step(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s) {
   switch (spl) {
@@ -374,6 +386,8 @@ cudaError_t launch_step(const KParams& kp, const DevCfg& cfg, int spl, cudaStrea
     case 2: return launch_step_t<2>(kp, cfg, s);
     case 4: return launch_step_t<4>(kp, cfg, s);
     case 8: return launch_step_t<8>(kp, cfg, s);
+    case 16: return launch_step_t<16>(kp, cfg, s);
+    case 32: return launch_step_t<32>(kp, cfg, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -384,6 +398,8 @@ cudaError_t launch_reset(const KParams& kp, const DevCfg& cfg, int spl, cudaStre
     case 2: return launch_reset_t<2>(kp, cfg, s);
     case 4: return launch_reset_t<4>(kp, cfg, s);
     case 8: return launch_reset_t<8>(kp, cfg, s);
+    case 16: return launch_reset_t<16>(kp, cfg, s);
+    case 32: return launch_reset_t<32>(kp, cfg, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -580,7 +580,7 @@ mlob_status mlob_venv_create(const mlob_venv_desc* desc, mlob_venv** out) {
     if (v->n_envs < 1) fail(MLOB_E_INVALID_ARGUMENT, "MarketVecEnv: n_envs >= 1");
     // device limits (stricter than the reference)
     v->spl = slots_per_lane(static_cast<int>(std::min<uint64_t>(c.book_capacity, 1u << 20)));
-    if (v->spl < 0) fail(MLOB_E_INVALID_ARGUMENT, "book_capacity above the device limit (256)");
+    if (v->spl < 0) fail(MLOB_E_INVALID_ARGUMENT, "book_capacity above the device limit (1024)");
     if (c.obs_depth > static_cast<uint64_t>(kMaxObsDepth))
       fail(MLOB_E_INVALID_ARGUMENT, "obs_depth above the device limit (64)");
     int A = 0;

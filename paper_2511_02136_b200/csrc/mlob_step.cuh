@@ -25,6 +25,7 @@
 
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "mlob_dev.h"
 
@@ -140,6 +141,61 @@ struct RegSide {
         q_[kk] = 0;
         st_[kk] = kEmptySt;
       }
+  }
+};
+
+// Book side in shared memory (deep books, capacity > 256): same interface and
+// slot layout as RegSide (row k, lane l at [k * 32 + l]); dynamic rows are
+// plain indexed accesses.
+template <int SPL>
+struct SmemSide {
+  int32_t* p_;
+  int32_t* q_;
+  uint32_t* lo_;
+  uint32_t* hi_;
+  uint32_t* st_;
+  __device__ __forceinline__ int32_t P(int k) const { return p_[k * 32]; }
+  __device__ __forceinline__ int32_t Q(int k) const { return q_[k * 32]; }
+  __device__ __forceinline__ uint32_t LO(int k) const { return lo_[k * 32]; }
+  __device__ __forceinline__ uint32_t HI(int k) const { return hi_[k * 32]; }
+  __device__ __forceinline__ uint32_t ST(int k) const { return st_[k * 32]; }
+  __device__ __forceinline__ void put(int k, int32_t p, int32_t q, uint32_t lo, uint32_t hi,
+                                      uint32_t st) {
+    p_[k * 32] = p;
+    q_[k * 32] = q;
+    lo_[k * 32] = lo;
+    hi_[k * 32] = hi;
+    st_[k * 32] = st;
+  }
+  __device__ __forceinline__ void get_pq(int k, int32_t& p, int32_t& q) const {
+    p = p_[k * 32];
+    q = q_[k * 32];
+  }
+  __device__ __forceinline__ void get_qid(int k, int32_t& q, uint32_t& lo, uint32_t& hi) const {
+    q = q_[k * 32];
+    lo = lo_[k * 32];
+    hi = hi_[k * 32];
+  }
+  __device__ __forceinline__ void set(int k, bool pred, int32_t p, int32_t q, uint32_t lo,
+                                      uint32_t hi, uint32_t st) {
+    if (pred) put(k, p, q, lo, hi, st);
+  }
+  __device__ __forceinline__ void setq(int k, bool pred, int32_t q) {
+    if (pred) q_[k * 32] = q;
+  }
+  __device__ __forceinline__ void clear(int k, bool pred, int32_t empty_p) {
+    if (pred) {
+      p_[k * 32] = empty_p;
+      q_[k * 32] = 0;
+      st_[k * 32] = kEmptySt;
+    }
+  }
+  __device__ __forceinline__ void bind(uint32_t* base, int lane) {  // 5 arrays of SPL*32 words
+    p_ = reinterpret_cast<int32_t*>(base) + lane;
+    q_ = reinterpret_cast<int32_t*>(base + SPL * 32) + lane;
+    lo_ = base + 2 * SPL * 32 + lane;
+    hi_ = base + 3 * SPL * 32 + lane;
+    st_ = base + 4 * SPL * 32 + lane;
   }
 };
 
@@ -288,9 +344,10 @@ __device__ __forceinline__ void attribute_fill(int n_agents, const DevCfg& cfg, 
 }
 
 // ---------------------------------------------------------------------------
-template <int SPL>
+template <int SPL, bool SMEM = (SPL > 8)>
 struct WarpEnv {
-  using SideT = RegSide<SPL>;
+  using SideT = typename std::conditional<SMEM, SmemSide<SPL>, RegSide<SPL>>::type;
+  static constexpr int kUnr = SMEM ? 4 : SPL;  // full unroll only for register books
   SideT bid, ask;
   const KParams& kp;
   const DevCfg& cfg;
@@ -317,8 +374,14 @@ struct WarpEnv {
   int64_t topq0, topq1;  // level-0 aggregated qty per side
   int64_t sumq0, sumq1;  // Σ qty over the top-D levels per side
 
-  __device__ WarpEnv(const KParams& p, const DevCfg& c, const WarpSmem& s, uint64_t e, int ln)
+  // book_smem: deep books only, [2 sides][5 arrays][SPL*32] words
+  __device__ WarpEnv(const KParams& p, const DevCfg& c, const WarpSmem& s, uint64_t e, int ln,
+                     uint32_t* book_smem)
       : kp(p), cfg(c), sm(s), lane(ln), env(e) {
+    if constexpr (SMEM) {
+      bid.bind(book_smem, ln);
+      ask.bind(book_smem + 5 * SPL * 32, ln);
+    }
     bind(e);
     err = 0;
     capacity = c.capacity;

@@ -56,8 +56,8 @@ def test_config_a_golden_digest(name):
 @pytest.mark.parametrize("scenario", list(scenario_configs().keys()))
 def test_scenario_parity(orc, scenario):
     cfg, synth_kw, n_steps = scenario_configs()[scenario]
-    if cfg.book_capacity > 256:
-        pytest.skip("deep-book kernel (capacity > 256) not in this build")
+    if cfg.book_capacity > 1024:
+        pytest.skip("capacity above the device limit")
     host_kw = {"n_messages": 20000, "state_sample_every": 100}
     host_kw.update(synth_kw)
     dev = dev_store(synth_kw)
