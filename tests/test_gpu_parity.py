@@ -236,3 +236,31 @@ def test_reset_determinism_and_executor_direction():  # test_env.cpp:70-111
     b2 = MarketEnvBatch(dev, cfg, n_envs=n, seed=0, env_seeds=np.arange(n), env_indices=np.zeros(n))
     b2.reset(np.zeros(n))
     assert b2.obs_type(0).tobytes() == b.obs_type(0).tobytes()
+
+
+def test_two_shards_equal_one_batch():
+    """Sharded handles (env_index_base / n_envs_global) reproduce the unsharded
+    batch env for env (what each GPU rank runs under torchrun)."""
+    import torch
+    from paper_2511_02136_b200.sharding import reduce_episode_stats, sharded_vec_env
+    cfg = abi.env_config([abi.agent_spec(abi.MARKET_MAKER), abi.agent_spec(abi.EXECUTOR)],
+                         steps_per_episode=8, messages_per_step=50, start_stride_steps=1)
+    dev = dev_store({"state_sample_every": 50, "n_messages": 60000})
+    n = 1000
+    full = MarketVecEnv(dev, cfg, seed=4, n_envs=n)
+    shards = [sharded_vec_env(dev, cfg, n, r, 3, seed=4) for r in range(3)]
+    for v in [full] + shards:
+        v.reset_all()
+    for t in range(20):
+        for v in [full] + shards:
+            v.step_random(11, t)
+    for ty in range(cfg.n_specs):
+        a = full.gather(ty)
+        b = [s.gather(ty) for s in shards]
+        assert a[0].tobytes() == np.concatenate([x[0] for x in b]).tobytes()
+        assert a[1].tobytes() == np.concatenate([x[1] for x in b]).tobytes()
+    assert full.rewards().tobytes() == np.concatenate([s.rewards() for s in shards]).tobytes()
+    tot = sum(reduce_episode_stats(s) for s in shards)
+    ref = reduce_episode_stats(full)
+    assert torch.equal(tot[:, [0, 1, 3, 4]], ref[:, [0, 1, 3, 4]])
+    assert float(tot[:, 4].sum()) > 0
