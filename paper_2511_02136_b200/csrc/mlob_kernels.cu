@@ -68,10 +68,37 @@ __device__ inline uint32_t* book_region(char* base, const DevCfg& c) {
   return reinterpret_cast<uint32_t*>(base + b);
 }
 
-constexpr int kWarpsPerBlock = 4;
-#ifndef MLOB_MIN_BLOCKS
-#define MLOB_MIN_BLOCKS 4
+// Register-book kernels run one block of kSyncWarps warps per SM with block
+// barriers between the step phases, so all warps of an SM execute the same
+// phase's code at the same time: the unsynchronised kernel was front-end
+// (instruction-cache) bound with warps spread over ~9.5k instructions
+// (profiles/r1_*).  Deep (smem) books keep 4-warp blocks.
+#ifndef MLOB_PHASE_SYNC
+#define MLOB_PHASE_SYNC 1
 #endif
+#ifndef MLOB_SYNC_WARPS
+#define MLOB_SYNC_WARPS 10
+#endif
+#ifndef MLOB_SYNC_REGS
+#define MLOB_SYNC_REGS 96
+#endif
+template <int SPL>
+__host__ __device__ constexpr bool phase_sync() {
+  return MLOB_PHASE_SYNC && SPL <= 8;
+}
+template <int SPL>
+__host__ __device__ constexpr int warps_per_block() {
+  return phase_sync<SPL>() ? MLOB_SYNC_WARPS : 4;
+}
+template <int SPL>
+__host__ __device__ constexpr int min_blocks() {
+  // blocks per SM for the register budget MLOB_SYNC_REGS (65536 regs / SM)
+  return phase_sync<SPL>() ? (65536 / (MLOB_SYNC_REGS * 32 * MLOB_SYNC_WARPS) > 0
+                                  ? 65536 / (MLOB_SYNC_REGS * 32 * MLOB_SYNC_WARPS)
+                                  : 1)
+                           : 4;
+}
+constexpr int kWarpsPerBlock = 4;  // reset kernel
 
 #ifdef MLOB_PHASE_TIMING
 #define PHASE(i)                                                               \
@@ -115,19 +142,22 @@ __device__ __forceinline__ void stage_params(StagedParams& sp, const KParams& kp
 static_assert(sizeof(KParams) % 16 == 0, "KParams must be int4-copyable");
 
 template <int SPL>
-__global__ void __launch_bounds__(kWarpsPerBlock * kWarp, MLOB_MIN_BLOCKS)
+__global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL>())
     step_kernel(const __grid_constant__ KParams kparam) {
+  constexpr int kWarpsPerBlock = warps_per_block<SPL>();
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(16) StagedParams sp_;
   stage_params(sp_, kparam);
   const KParams& kp = sp_.kp;
   const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarpsPerBlock;
-  // dynamic work distribution: the first env of each warp is static, later
-  // ones come from a global ticket counter (fetched one env ahead so the next
-  // env's data can be prefetched); kp.ticket is zeroed before each launch.
+  // dynamic work distribution (MLOB_PERSIST): the first env of each warp is
+  // static, later ones come from a global ticket counter fetched one env ahead
+  // so the next env's data can be prefetched; kp.ticket is zeroed per launch.
   const uint64_t first = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + warp;
-  if (first >= kp.n_envs) return;
+  // phase-sync builds keep idle warps alive for the block barriers
+  const bool idle = first >= kp.n_envs;
+  if (idle && !phase_sync<SPL>()) return;
   const auto ticket = [&]() -> uint64_t {
     unsigned long long t = 0;
     if (lane == 0) t = atomicAdd(kp.ticket, 1ull);
@@ -136,7 +166,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp, MLOB_MIN_BLOCKS)
   const DevCfg& cfg = sp_.cfg;
   char* wbase = smem + warp * warp_smem_bytes(cfg);
   WarpSmem sm = carve(wbase, cfg);
-  WarpEnv<SPL> w(kp, cfg, sm, first, lane, book_region(wbase, cfg));
+  WarpEnv<SPL> w(kp, cfg, sm, idle ? 0 : first, lane, book_region(wbase, cfg));
   const int mps = cfg.mps;
   const int nch = (mps + kChunk - 1) / kChunk;
   const int A = cfg.n_agents;
@@ -150,117 +180,128 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp, MLOB_MIN_BLOCKS)
     const EnvHdr& h = kp.hdr[e];
     return kp.msgs + kp.ep_start[h.episode] + static_cast<uint64_t>(h.step) * mps;
   };
-  if (mps > 0) w.stage(slice_of(first), min(kChunk, mps));
+  if (!idle && mps > 0) w.stage(slice_of(first), min(kChunk, mps));
 
-  uint64_t nenv = MLOB_PERSIST ? ticket() : kp.n_envs;
-  for (uint64_t env = first; env < kp.n_envs;) {
-    w.bind(env);
-    PHASE(0);
-    w.load_hdr();
-    const DevMsg* slice = kp.msgs + kp.ep_start[w.episode] + static_cast<uint64_t>(w.step) * mps;
-    if (nch >= 2) w.stage(slice + kChunk, min(kChunk, mps - kChunk));
+  uint64_t nenv = (MLOB_PERSIST && !phase_sync<SPL>()) ? ticket() : kp.n_envs;
+  for (uint64_t env = first; env < kp.n_envs || (idle && env == first);) {
+    const DevMsg* slice = nullptr;
     const bool has_next = nenv < kp.n_envs;
     const DevMsg* next_slice = nullptr;
-    if (has_next) {
-      next_slice = mps > 0 ? slice_of(nenv) : nullptr;
-#if MLOB_PREFETCH
-      const EnvHdr& nh = kp.hdr[nenv];
-      if (lane == 0) prefetch_l2(&nh);
-      if (lane < A) prefetch_l2(kp.agents + nenv * A + lane);
-#pragma unroll
-      for (int s = 0; s < 2; ++s)
-#pragma unroll
-        for (int k = 0; k < SPL; ++k)
-          if (k * kWarp < (s ? nh.hwm[1] : nh.hwm[0])) {
-            const size_t i = ((nenv * 2 + s) * SPL + k) * kWarp + lane;
-            prefetch_l2(kp.bk_p + i);
-            prefetch_l2(kp.bk_q + i);
-            prefetch_l2(kp.bk_id + i);
-            prefetch_l2(kp.bk_st + i);
-          }
-#endif
-    }
-    w.load_agents();
-    w.clear_step_acc();
-    const int64_t step_time = mps > 0 ? slice[0].time : w.last_time + 1;
-    PHASE(1);
-
-    // (1) actions -> agent messages, (2) Fisher-Yates (rng.hpp:63-71)
     int n_amsg = 0;
-    for (int a = 0; a < A; ++a) w.convert_action(a, step_time, n_amsg);
-    __syncwarp();
-    if (n_amsg >= 2 && lane == 0) {
-      uint64_t h = splitmix64(w.seed);
-      h = key_fold(h, w.genv);
-      h = key_fold(h, w.episode);
-      h = key_fold(h, static_cast<uint64_t>(w.step));
-      h = key_fold(h, kRngShuffle);
-      Rng r{h};
-      for (int i = n_amsg - 1; i > 0; --i) {
-        const int j = static_cast<int>(r.below(static_cast<uint64_t>(i + 1)));
-        if (i != j) {
-          const DevMsg t = sm.amsg[i];
-          sm.amsg[i] = sm.amsg[j];
-          sm.amsg[j] = t;
+    if (!idle) {  // ---- phase 1: header, agents, actions -> agent messages
+      w.bind(env);
+      PHASE(0);
+      w.load_hdr();
+      slice = kp.msgs + kp.ep_start[w.episode] + static_cast<uint64_t>(w.step) * mps;
+      if (nch >= 2) w.stage(slice + kChunk, min(kChunk, mps - kChunk));
+      if (has_next) {
+        next_slice = mps > 0 ? slice_of(nenv) : nullptr;
+#if MLOB_PREFETCH
+        const EnvHdr& nh = kp.hdr[nenv];
+        if (lane == 0) prefetch_l2(&nh);
+        if (lane < A) prefetch_l2(kp.agents + nenv * A + lane);
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+          for (int k = 0; k < SPL; ++k)
+            if (k * kWarp < (s ? nh.hwm[1] : nh.hwm[0])) {
+              const size_t i = ((nenv * 2 + s) * SPL + k) * kWarp + lane;
+              prefetch_l2(kp.bk_p + i);
+              prefetch_l2(kp.bk_q + i);
+              prefetch_l2(kp.bk_id + i);
+              prefetch_l2(kp.bk_st + i);
+            }
+#endif
+      }
+      w.load_agents();
+      w.clear_step_acc();
+      const int64_t step_time = mps > 0 ? slice[0].time : w.last_time + 1;
+      PHASE(1);
+      // (1) actions -> agent messages, (2) Fisher-Yates (rng.hpp:63-71)
+      for (int a = 0; a < A; ++a) w.convert_action(a, step_time, n_amsg);
+      __syncwarp();
+      if (n_amsg >= 2 && lane == 0) {
+        uint64_t h = splitmix64(w.seed);
+        h = key_fold(h, w.genv);
+        h = key_fold(h, w.episode);
+        h = key_fold(h, static_cast<uint64_t>(w.step));
+        h = key_fold(h, kRngShuffle);
+        Rng r{h};
+        for (int i = n_amsg - 1; i > 0; --i) {
+          const int j = static_cast<int>(r.below(static_cast<uint64_t>(i + 1)));
+          if (i != j) {
+            const DevMsg t = sm.amsg[i];
+            sm.amsg[i] = sm.amsg[j];
+            sm.amsg[j] = t;
+          }
         }
       }
+      __syncwarp();
+      PHASE(2);
     }
-    __syncwarp();
-    PHASE(2);
-    // book registers are loaded only now: nothing above needs them (tops are
-    // in the header) and they must not be live across subroutine calls
-    w.load_book();
-
-    // (3) + (4): agent messages, then the replay slice
-    w.prev_mid_half = w.mid_half;
-    w.mid_sum = 0;
-    w.mid_count = 0;
-    w.n_trades = 0;
-    PHASE(3);
-    w.process_messages(n_amsg, slice);
-    PHASE(4);
-    if (has_next && mps > 0) w.stage(next_slice, min(kChunk, mps));  // overlaps the outcomes
-    if (w.live0 > 0) w.last_bid = w.best0;
-    if (w.live1 > 0) w.last_ask = w.best1;
-
-    // (5) outcomes
-    w.mbar = w.mid_count > 0 ? static_cast<double>(w.mid_sum) / (2.0 * static_cast<double>(w.mid_count))
-                             : static_cast<double>(w.prev_mid_half) / 2.0;
-    if (sm.scal[1] && lane == 0) atomicAdd(kp.fill_overflow, 1ull);
-    w.rebuild_active();
-    PHASE(5);
-    ++w.step;
-    w.terminal = w.step >= cfg.steps_per_episode;
-    uint8_t just_reset = 0;
-    for (int pass = 0;; ++pass) {  // pass 1: the auto-reset env's fresh outputs
+    if constexpr (phase_sync<SPL>()) __syncthreads();
+    if (!idle) {  // ---- phase 2: book in registers, message loop, book out
+      // book registers are loaded only now: nothing above needs them (tops are
+      // in the header) and they must not be live across subroutine calls
+      w.load_book();
+      // (3) + (4): agent messages, then the replay slice
+      w.prev_mid_half = w.mid_half;
+      w.mid_sum = 0;
+      w.mid_count = 0;
+      w.n_trades = 0;
+      PHASE(3);
+      w.process_messages(n_amsg, slice);
+      PHASE(4);
+      if (has_next && mps > 0) w.stage(next_slice, min(kChunk, mps));  // overlaps the outcomes
+      if (w.live0 > 0) w.last_bid = w.best0;
+      if (w.live1 > 0) w.last_ask = w.best1;
+      // (5) outcomes
+      w.mbar = w.mid_count > 0 ? static_cast<double>(w.mid_sum) / (2.0 * static_cast<double>(w.mid_count))
+                               : static_cast<double>(w.prev_mid_half) / 2.0;
+      if (sm.scal[1] && lane == 0) atomicAdd(kp.fill_overflow, 1ull);
+      w.rebuild_active();
+      PHASE(5);
+      ++w.step;
+      w.terminal = w.step >= cfg.steps_per_episode;
       w.snapshot();
-      if (pass == 0) PHASE(6);
+      PHASE(6);
       w.store_book();  // book registers dead from here on
-      if (pass == 0) PHASE(7);
-      w.outcomes(pass == 0);
-      if (pass == 0) PHASE(8);
-      if (pass > 0 || !(w.terminal && (kp.flags & MLOB_VENV_AUTO_RESET))) break;
-      if (lane == 0)
-        for (int a = 0; a < A; ++a) {  // rollout.hpp:300-313
-          const mlob_agent_info& info = kp.infos[env * A + a];
-          const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
-          const size_t slot = env * A + a;
-          kp.t_pv[slot] += info.portfolio_value;
-          kp.t_slip[slot] += info.slippage_total;
-          kp.t_comp[slot] += sp.type == MLOB_EXECUTOR
-                                 ? 1.0 - static_cast<double>(info.task_remaining) /
-                                             static_cast<double>(sp.task_size)
-                                 : 0.0;
-          kp.t_inv[slot] += static_cast<double>(info.inventory) * static_cast<double>(info.inventory);
-        }
-      ++w.ep_finished;
-      const uint64_t ep = w.episode_for(w.cursor);
-      ++w.cursor;
-      if (!w.reset(ep, false)) break;
-      just_reset = 1;
+      PHASE(7);
     }
-    w.store_state(just_reset);
-    PHASE(9);
+    if constexpr (phase_sync<SPL>()) __syncthreads();
+    if (!idle) {  // ---- phase 3: rewards / infos / observations, auto-reset
+      uint8_t just_reset = 0;
+      for (int pass = 0;; ++pass) {  // pass 1: the auto-reset env's fresh outputs
+        if (pass > 0) {
+          w.snapshot();
+          w.store_book();
+        }
+        w.outcomes(pass == 0);
+        if (pass == 0) PHASE(8);
+        if (pass > 0 || !(w.terminal && (kp.flags & MLOB_VENV_AUTO_RESET))) break;
+        if (lane == 0)
+          for (int a = 0; a < A; ++a) {  // rollout.hpp:300-313
+            const mlob_agent_info& info = kp.infos[env * A + a];
+            const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
+            const size_t slot = env * A + a;
+            kp.t_pv[slot] += info.portfolio_value;
+            kp.t_slip[slot] += info.slippage_total;
+            kp.t_comp[slot] += sp.type == MLOB_EXECUTOR
+                                   ? 1.0 - static_cast<double>(info.task_remaining) /
+                                               static_cast<double>(sp.task_size)
+                                   : 0.0;
+            kp.t_inv[slot] += static_cast<double>(info.inventory) * static_cast<double>(info.inventory);
+          }
+        ++w.ep_finished;
+        const uint64_t ep = w.episode_for(w.cursor);
+        ++w.cursor;
+        if (!w.reset(ep, false)) break;
+        just_reset = 1;
+      }
+      w.store_state(just_reset);
+      PHASE(9);
+    }
+    if (idle) break;
     env = nenv;
     if (has_next) nenv = ticket();
   }
@@ -340,7 +381,10 @@ __global__ void clear_finished_kernel(EnvHdr* hdr, uint64_t n) {
 // ---------------------------------------------------------------------------
 // host-side launchers
 
-size_t step_smem_bytes(const DevCfg& c) { return warp_smem_bytes(c) * kWarpsPerBlock; }  // dynamic part
+size_t step_smem_bytes(const DevCfg& c) {  // dynamic smem of the step kernel's block
+  const int wpb = spl_of(c.capacity) <= 8 && MLOB_PHASE_SYNC ? MLOB_SYNC_WARPS : 4;
+  return warp_smem_bytes(c) * wpb;
+}
 
 static unsigned grid_for(uint64_t n) {
   const uint64_t b = (n + 255) / 256;
@@ -349,7 +393,8 @@ static unsigned grid_for(uint64_t n) {
 
 template <int SPL>
 static cudaError_t launch_step_t(const KParams& kp, const DevCfg& cfg, cudaStream_t s) {
-  const size_t sm = step_smem_bytes(cfg);
+  constexpr int kWarpsPerBlock = warps_per_block<SPL>();
+  const size_t sm = warp_smem_bytes(cfg) * kWarpsPerBlock;
   cudaError_t e = cudaFuncSetAttribute(step_kernel<SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sm));
   if (e != cudaSuccess) return e;
@@ -362,14 +407,15 @@ static cudaError_t launch_step_t(const KParams& kp, const DevCfg& cfg, cudaStrea
     return e;
   const uint64_t need = (kp.n_envs + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const uint64_t cap = static_cast<uint64_t>(n_sm) * (per_sm > 0 ? per_sm : 1);
-  const unsigned blocks = static_cast<unsigned>(MLOB_PERSIST ? (need < cap ? need : cap) : need);
+  const unsigned blocks =
+      static_cast<unsigned>((MLOB_PERSIST && !phase_sync<SPL>()) ? (need < cap ? need : cap) : need);
   step_kernel<SPL><<<blocks, kWarpsPerBlock * kWarp, sm, s>>>(kp);
   return cudaGetLastError();
 }
 
 template <int SPL>
 static cudaError_t launch_reset_t(const KParams& kp, const DevCfg& cfg, cudaStream_t s) {
-  const size_t sm = step_smem_bytes(cfg);
+  const size_t sm = warp_smem_bytes(cfg) * kWarpsPerBlock;
   cudaError_t e = cudaFuncSetAttribute(reset_kernel<SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sm));
   if (e != cudaSuccess) return e;
