@@ -133,6 +133,16 @@ struct RegSide {
     for (int kk = 0; kk < SPL; ++kk)
       if (pred && k == kk) q_[kk] = q;
   }
+  // insert at a warp-uniform row: uniform branch + predicated writes
+  __device__ __forceinline__ void set_u(int k, bool pred, int32_t p, int32_t q, uint32_t lo,
+                                        uint32_t hi, uint32_t st) {
+#pragma unroll
+    for (int kk = 0; kk < SPL; ++kk) {
+      if (k == kk) {
+        if (pred) put(kk, p, q, lo, hi, st);
+      }
+    }
+  }
   __device__ __forceinline__ void clear(int k, bool pred, int32_t empty_p) {
 #pragma unroll
     for (int kk = 0; kk < SPL; ++kk)
@@ -179,6 +189,10 @@ struct SmemSide {
   __device__ __forceinline__ void set(int k, bool pred, int32_t p, int32_t q, uint32_t lo,
                                       uint32_t hi, uint32_t st) {
     if (pred) put(k, p, q, lo, hi, st);
+  }
+  __device__ __forceinline__ void set_u(int k, bool pred, int32_t p, int32_t q, uint32_t lo,
+                                        uint32_t hi, uint32_t st) {
+    set(k, pred, p, q, lo, hi, st);
   }
   __device__ __forceinline__ void setq(int k, bool pred, int32_t q) {
     if (pred) q_[k * 32] = q;
@@ -585,20 +599,19 @@ struct WarpEnv {
       nm += c ? 1 : 0;
     }
   }
-  // lowest free position: (row, lane)
+  // lowest free position (row-major: row * 32 + lane) -> (row, lane), one
+  // redux.min over each lane's lowest free row
   template <int S>
   __device__ __forceinline__ void free_slot_t(int& pk, int& pl) {
     SideT& d = sd<S>();
-    pk = -1;
-    pl = 0;
+    uint32_t fm = 0;
 #pragma unroll
-    for (int k = 0; k < SPL; ++k) {
-      const uint32_t b = __ballot_sync(FULLMASK, d.Q(k) == 0);
-      if (pk < 0 && b) {
-        pk = k;
-        pl = __ffs(b) - 1;
-      }
-    }
+    for (int k = 0; k < SPL; ++k) fm |= (d.Q(k) == 0 ? 1u : 0u) << k;
+    const uint32_t key = fm ? (static_cast<uint32_t>(__ffs(fm) - 1) << 5) | static_cast<uint32_t>(lane)
+                            : 0xffffffffu;
+    const uint32_t g = __reduce_min_sync(FULLMASK, key);
+    pk = static_cast<int>(g >> 5);
+    pl = static_cast<int>(g & 31u);
   }
   __device__ __forceinline__ void slot_get_pq(int s, int k, int32_t& p, int32_t& q) const {
     if (s)
@@ -695,6 +708,8 @@ struct WarpEnv {
       attribute_fill(n_agents, cfg, sm, price, qty, static_cast<int>(pt), m.trader, aside);
   }
 
+  bool moved;  // a top (best price or side emptiness) changed: refresh the mid
+
   // book.hpp:150-187 (process_new_limit + rest_order)
   __device__ __forceinline__ void new_limit(const DevMsg& m) {
     const int s = m.side, o = s ^ 1;
@@ -725,6 +740,7 @@ struct WarpEnv {
       rem -= fill;
       if (fill == q) {
         slot_clear(o, lk, me);
+        moved = true;
         if (o) {
           if (--live1 > 0) best1 = side_best_t<1>();
         } else {
@@ -740,6 +756,7 @@ struct WarpEnv {
     if ((s ? live1 : live0) == capacity) {
       const bool ev = s ? evict_t<1>(m.price) : evict_t<0>(m.price);
       if (!ev) return;  // newcomer dropped: no sequence number consumed
+      moved = true;
       if (s)
         --live1;
       else
@@ -755,11 +772,17 @@ struct WarpEnv {
     const uint32_t st = (seq << 8) | static_cast<uint32_t>(m.trader & 0xff);
     const uint32_t ilo = static_cast<uint32_t>(m.order_id), ihi = static_cast<uint32_t>(m.order_id >> 32);
     if (s) {
-      ask.set(pk, lane == pl, m.price, rem, ilo, ihi, st);
-      best1 = ++live1 == 1 ? m.price : min(best1, m.price);
+      ask.set_u(pk, lane == pl, m.price, rem, ilo, ihi, st);
+      if (++live1 == 1 || m.price < best1) {
+        best1 = m.price;
+        moved = true;
+      }
     } else {
-      bid.set(pk, lane == pl, m.price, rem, ilo, ihi, st);
-      best0 = ++live0 == 1 ? m.price : max(best0, m.price);
+      bid.set_u(pk, lane == pl, m.price, rem, ilo, ihi, st);
+      if (++live0 == 1 || m.price > best0) {
+        best0 = m.price;
+        moved = true;
+      }
     }
   }
 
@@ -808,8 +831,9 @@ struct WarpEnv {
   __device__ __forceinline__ void run_message(const DevMsg& m) {
     if (m.kind == MLOB_NEW_LIMIT) {
       if (m.qty > 0) {
+        moved = false;
         new_limit(m);
-        refresh_mid();
+        if (moved) refresh_mid();
       }
     } else if (m.kind <= MLOB_EXECUTE_VISIBLE) {
       if (by_id(m, m.kind == MLOB_DELETE)) refresh_mid();
