@@ -162,11 +162,25 @@ def gpu_arm(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = local if world > 1 else 0
+    # diagnostics only: MLOB_BENCH_BACKEND=gloo + MLOB_BENCH_DEVICE=0 run several
+    # ranks on one GPU to exercise the multi-rank path (sharding, max-over-ranks
+    # timing, stats all-reduce); real runs use one GPU per rank and NCCL.
+    backend = os.environ.get("MLOB_BENCH_BACKEND", "nccl")
+    dev = int(os.environ.get("MLOB_BENCH_DEVICE", local))
     torch.cuda.set_device(dev)
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+    coll_dev = "cuda" if backend == "nccl" else "cpu"
+
+    def allreduce(t, op=None):
+        if world > 1:
+            x = t.to(coll_dev)
+            dist.all_reduce(x, op=op or dist.ReduceOp.SUM)
+            t.copy_(x)
+        return t
 
     n_total, cfg, synth, label = workload(args.workload)
     if args.mps:
@@ -220,9 +234,8 @@ def gpu_arm(args) -> None:
     # whole-job: max time over ranks, sum of messages
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     m = torch.tensor([msgs], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(m, op=dist.ReduceOp.SUM)
+    allreduce(t, dist.ReduceOp.MAX)
+    allreduce(m)
     ms_max, msgs_all = float(t.item()), float(m.item())
     value = msgs_all / (ms_max / 1e3)
     env_steps = n_total * args.steps / (ms_max / 1e3)
@@ -231,8 +244,7 @@ def gpu_arm(args) -> None:
     stats = torch.zeros(5 * cfg.n_specs, dtype=torch.float64, device="cuda")
     venv.episode_stats_device(stats.data_ptr())
     venv.synchronize()
-    if world > 1:
-        dist.all_reduce(stats)
+    allreduce(stats)
 
     # e2e through the public API with host buffers: pinned actions H2D, step,
     # rewards + dones + observations D2H, every step
@@ -260,8 +272,7 @@ def gpu_arm(args) -> None:
             E._check(L.mlob_venv_gather(venv.h, ty, obs_bufs[ty].data_ptr(), rs.data_ptr()))
     torch.cuda.synchronize()
     e_wall = torch.tensor([time.perf_counter() - w0], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(e_wall, op=dist.ReduceOp.MAX)
+    allreduce(e_wall, dist.ReduceOp.MAX)
     e_msgs = msgs_all / args.steps * e_steps  # same per-step message volume
     h2d = acts.numel() * 4
     d2h = rew.numel() * 8 + dn.numel() + sum(b.numel() * 8 for b in obs_bufs) + \

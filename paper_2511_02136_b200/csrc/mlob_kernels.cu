@@ -29,7 +29,7 @@ __host__ __device__ inline size_t warp_smem_bytes(const DevCfg& c) {
   b += static_cast<size_t>(2 * c.obs_depth) * sizeof(L2Lvl);
   b += static_cast<size_t>(c.max_obs_dim + 1) * sizeof(double);
   b = (b + 15) / 16 * 16;
-  if (c.capacity > 8 * kWarp) b += book_smem_bytes(c.capacity);  // deep book lives in smem
+  if (c.capacity > 8 * kWarp || MLOB_SMEM_BOOK) b += book_smem_bytes(c.capacity);  // smem book
   return (b + 127) / 128 * 128;
 }
 
@@ -63,7 +63,7 @@ __device__ WarpSmem carve(char* base, const DevCfg& c) {
 
 // deep-book smem region of a warp (after the WarpSmem carve-out)
 __device__ inline uint32_t* book_region(char* base, const DevCfg& c) {
-  size_t b = warp_smem_bytes(c) - ((c.capacity > 8 * kWarp) ? book_smem_bytes(c.capacity) : 0);
+  size_t b = warp_smem_bytes(c) - ((c.capacity > 8 * kWarp || MLOB_SMEM_BOOK) ? book_smem_bytes(c.capacity) : 0);
   b = b / 16 * 16;
   return reinterpret_cast<uint32_t*>(base + b);
 }

@@ -728,13 +728,19 @@ mlob_status mlob_venv_set_actions(mlob_venv* v, const int32_t* ids, int on_devic
     const uint64_t n = v->n_envs * v->A;
     v->set_device();
     if (!on_device) {
-      for (uint64_t i = 0; i < n; ++i) {
-        const int a = static_cast<int>(i % v->A);
-        const int ar = v->dcfg.specs[v->dcfg.flat_spec[a]].arity;
-        if (ids[i] < 0 || ids[i] >= ar)
-          fail(MLOB_E_OUT_OF_RANGE, "action id " + std::to_string(ids[i]) + " out of range for agent " +
-                                        std::to_string(a) + " (arity " + std::to_string(ar) + ")");
-      }
+      // actions.hpp:69-70 range check, env-major without per-element division
+      uint32_t ar[MLOB_MAX_AGENTS];
+      for (int a = 0; a < v->A; ++a) ar[a] = static_cast<uint32_t>(v->dcfg.specs[v->dcfg.flat_spec[a]].arity);
+      bool bad = false;
+      for (uint64_t e = 0, i = 0; e < v->n_envs; ++e)
+        for (int a = 0; a < v->A; ++a, ++i) bad |= static_cast<uint32_t>(ids[i]) >= ar[a];
+      if (bad)
+        for (uint64_t i = 0; i < n; ++i) {
+          const int a = static_cast<int>(i % v->A);
+          if (static_cast<uint32_t>(ids[i]) >= ar[a])
+            fail(MLOB_E_OUT_OF_RANGE, "action id " + std::to_string(ids[i]) + " out of range for agent " +
+                                          std::to_string(a) + " (arity " + std::to_string(ar[a]) + ")");
+        }
       cuda_check(cudaMemcpyAsync(v->d_actions, ids, n * 4, cudaMemcpyHostToDevice, v->stream), "H2D");
     } else {
       cuda_check(cudaMemcpyAsync(v->d_actions, ids, n * 4, cudaMemcpyDeviceToDevice, v->stream), "D2D");

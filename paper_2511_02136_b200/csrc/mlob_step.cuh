@@ -358,7 +358,10 @@ __device__ __forceinline__ void attribute_fill(int n_agents, const DevCfg& cfg, 
 }
 
 // ---------------------------------------------------------------------------
-template <int SPL, bool SMEM = (SPL > 8)>
+#ifndef MLOB_SMEM_BOOK  // 1: shared-memory book for every capacity (experiment)
+#define MLOB_SMEM_BOOK 0
+#endif
+template <int SPL, bool SMEM = (SPL > 8) || MLOB_SMEM_BOOK>
 struct WarpEnv {
   using SideT = typename std::conditional<SMEM, SmemSide<SPL>, RegSide<SPL>>::type;
   static constexpr int kUnr = SMEM ? 4 : SPL;  // full unroll only for register books
