@@ -79,21 +79,30 @@ __device__ inline uint32_t* book_region(char* base, const DevCfg& c) {
 #ifndef MLOB_SYNC_WARPS
 #define MLOB_SYNC_WARPS 10
 #endif
+#ifndef MLOB_SYNC_A  // barrier before the message loop (measured: no gain)
+#define MLOB_SYNC_A 0
+#endif
+#ifndef MLOB_SYNC_B  // barrier after the message loop
+#define MLOB_SYNC_B 1
+#endif
+#ifndef MLOB_DEEP_SYNC  // phase barriers for the deep (smem) book too
+#define MLOB_DEEP_SYNC 0
+#endif
 #ifndef MLOB_SYNC_REGS
 #define MLOB_SYNC_REGS 96
 #endif
 template <int SPL>
 __host__ __device__ constexpr bool phase_sync() {
-  return MLOB_PHASE_SYNC && SPL <= 8;
+  return MLOB_PHASE_SYNC && (SPL <= 8 || MLOB_DEEP_SYNC);
 }
 template <int SPL>
 __host__ __device__ constexpr int warps_per_block() {
-  return phase_sync<SPL>() ? MLOB_SYNC_WARPS : 4;
+  return (phase_sync<SPL>() && SPL <= 8) ? MLOB_SYNC_WARPS : 4;  // deep books: smem-bound 4-warp blocks
 }
 template <int SPL>
 __host__ __device__ constexpr int min_blocks() {
   // blocks per SM for the register budget MLOB_SYNC_REGS (65536 regs / SM)
-  return phase_sync<SPL>() ? (65536 / (MLOB_SYNC_REGS * 32 * MLOB_SYNC_WARPS) > 0
+  return (phase_sync<SPL>() && SPL <= 8) ? (65536 / (MLOB_SYNC_REGS * 32 * MLOB_SYNC_WARPS) > 0
                                   ? 65536 / (MLOB_SYNC_REGS * 32 * MLOB_SYNC_WARPS)
                                   : 1)
                            : 4;
@@ -239,7 +248,7 @@ __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL
       __syncwarp();
       PHASE(2);
     }
-    if constexpr (phase_sync<SPL>()) __syncthreads();
+    if constexpr (phase_sync<SPL>() && MLOB_SYNC_A) __syncthreads();
     if (!idle) {  // ---- phase 2: book in registers, message loop, book out
       // book registers are loaded only now: nothing above needs them (tops are
       // in the header) and they must not be live across subroutine calls
@@ -268,7 +277,7 @@ __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL
       w.store_book();  // book registers dead from here on
       PHASE(7);
     }
-    if constexpr (phase_sync<SPL>()) __syncthreads();
+    if constexpr (phase_sync<SPL>() && MLOB_SYNC_B) __syncthreads();
     if (!idle) {  // ---- phase 3: rewards / infos / observations, auto-reset
       uint8_t just_reset = 0;
       for (int pass = 0;; ++pass) {  // pass 1: the auto-reset env's fresh outputs
