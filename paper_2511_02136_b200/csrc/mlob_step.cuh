@@ -361,10 +361,18 @@ __device__ __forceinline__ void attribute_fill(int n_agents, const DevCfg& cfg, 
 #ifndef MLOB_SMEM_BOOK  // 1: shared-memory book for every capacity (experiment)
 #define MLOB_SMEM_BOOK 0
 #endif
+// row loop over a side's SPL rows, unrolled kUnr at a time
+#define MLOB_ROWS(k)                                        \
+  _Pragma("unroll 1") for (int k##_g = 0; k##_g < SPL; k##_g += kUnr) \
+  _Pragma("unroll") for (int k = k##_g; k < k##_g + kUnr; ++k)
 template <int SPL, bool SMEM = (SPL > 8) || MLOB_SMEM_BOOK>
 struct WarpEnv {
   using SideT = typename std::conditional<SMEM, SmemSide<SPL>, RegSide<SPL>>::type;
-  static constexpr int kUnr = SMEM ? 4 : SPL;  // full unroll only for register books
+  // rows per unrolled group: all rows for register books (a full unroll keeps
+  // them in registers), groups of 4 for shared-memory books (code size).  An
+  // explicit `#pragma unroll N` on the row loops changes the register-book
+  // code (measured -11% on config C), hence the two-level loop below.
+  static constexpr int kUnr = (SMEM && SPL >= 4) ? 4 : SPL;
   SideT bid, ask;
   const KParams& kp;
   const DevCfg& cfg;
@@ -427,8 +435,7 @@ struct WarpEnv {
   template <int S>
   __device__ __forceinline__ void load_side(int hwm) {
     SideT& d = sd<S>();
-#pragma unroll (SMEM ? 4 : SPL)
-    for (int k = 0; k < SPL; ++k) {
+    MLOB_ROWS(k) {
       if (k * kWarp < hwm) {
         const size_t i = row_index(S, k);
         const uint2 id = kp.bk_id[i];
@@ -442,13 +449,11 @@ struct WarpEnv {
   __device__ __forceinline__ int store_side() {
     SideT& d = sd<S>();
     int hwm = 0;
-#pragma unroll (SMEM ? 4 : SPL)
-    for (int k = 0; k < SPL; ++k) {
+    MLOB_ROWS(k) {
       const uint32_t b = __ballot_sync(FULLMASK, d.Q(k) > 0);
       if (b) hwm = k * kWarp + 32 - __clz(b);
     }
-#pragma unroll (SMEM ? 4 : SPL)
-    for (int k = 0; k < SPL; ++k) {
+    MLOB_ROWS(k) {
       if (k * kWarp < hwm) {
         const size_t i = row_index(S, k);
         kp.bk_p[i] = d.P(k);
@@ -571,9 +576,8 @@ struct WarpEnv {
   template <int S>
   __device__ __forceinline__ int32_t side_best_t() {
     SideT& d = sd<S>();
-    int32_t b = d.P(0);
-#pragma unroll (SMEM ? 4 : SPL)
-    for (int k = 1; k < SPL; ++k) b = better_of<S>(b, d.P(k));
+    int32_t b = empty_price<S>();
+    MLOB_ROWS(k) b = better_of<S>(b, d.P(k));
     return redux_best<S>(b);
   }
   // lane-local oldest slot (min st) at `price`
@@ -582,8 +586,7 @@ struct WarpEnv {
     SideT& d = sd<S>();
     m = kEmptySt;
     lk = 0;
-#pragma unroll (SMEM ? 4 : SPL)
-    for (int k = 0; k < SPL; ++k) {
+    MLOB_ROWS(k) {
       const bool c = d.P(k) == price && d.ST(k) < m;
       m = c ? d.ST(k) : m;
       lk = c ? k : lk;
@@ -595,8 +598,7 @@ struct WarpEnv {
     SideT& d = sd<S>();
     nm = 0;
     lk = 0;
-#pragma unroll (SMEM ? 4 : SPL)
-    for (int k = 0; k < SPL; ++k) {
+    MLOB_ROWS(k) {
       const bool c = d.Q(k) > 0 && d.LO(k) == lo && d.HI(k) == hi;
       lk = (c && nm == 0) ? k : lk;
       nm += c ? 1 : 0;
@@ -608,8 +610,7 @@ struct WarpEnv {
   __device__ __forceinline__ void free_slot_t(int& pk, int& pl) {
     SideT& d = sd<S>();
     uint32_t fm = 0;
-#pragma unroll (SMEM ? 4 : SPL)
-    for (int k = 0; k < SPL; ++k) fm |= (d.Q(k) == 0 ? 1u : 0u) << k;
+    MLOB_ROWS(k) fm |= (d.Q(k) == 0 ? 1u : 0u) << k;
     const uint32_t key = fm ? (static_cast<uint32_t>(__ffs(fm) - 1) << 5) | static_cast<uint32_t>(lane)
                             : 0xffffffffu;
     const uint32_t g = __reduce_min_sync(FULLMASK, key);
@@ -647,8 +648,7 @@ struct WarpEnv {
   __device__ __forceinline__ bool evict_t(int32_t price) {
     SideT& d = sd<S>();
     int32_t lw = S == 0 ? INT_MAX : INT_MIN;
-#pragma unroll (SMEM ? 4 : SPL)
-    for (int k = 0; k < SPL; ++k)
+    MLOB_ROWS(k)
       if (d.Q(k) > 0) lw = S == 0 ? min(lw, d.P(k)) : max(lw, d.P(k));
     const int32_t worst = S == 0 ? __reduce_min_sync(FULLMASK, lw) : __reduce_max_sync(FULLMASK, lw);
     const bool better = S == 0 ? price > worst : price < worst;
@@ -667,16 +667,14 @@ struct WarpEnv {
   __device__ __forceinline__ int dup_owner_t(uint32_t lo, uint32_t hi, int& lk) {
     SideT& d = sd<S>();
     int32_t kp_ = S == 0 ? INT_MAX : INT_MIN;
-#pragma unroll (SMEM ? 4 : SPL)
-    for (int k = 0; k < SPL; ++k) {
+    MLOB_ROWS(k) {
       const bool c = d.Q(k) > 0 && d.LO(k) == lo && d.HI(k) == hi;
       if (c) kp_ = S == 0 ? min(kp_, d.P(k)) : max(kp_, d.P(k));
     }
     const int32_t gp = S == 0 ? __reduce_min_sync(FULLMASK, kp_) : __reduce_max_sync(FULLMASK, kp_);
     uint32_t ms = 0;
     bool any = false;
-#pragma unroll (SMEM ? 4 : SPL)
-    for (int k = 0; k < SPL; ++k) {
+    MLOB_ROWS(k) {
       const bool c = d.Q(k) > 0 && d.LO(k) == lo && d.HI(k) == hi && d.P(k) == gp;
       if (c && (!any || d.ST(k) > ms)) {
         ms = d.ST(k);
@@ -1067,8 +1065,7 @@ struct WarpEnv {
     int32_t prev = 0;
     for (; n < D; ++n) {
       int32_t lb = empty_price<S>();
-#pragma unroll (SMEM ? 4 : SPL)
-      for (int k = 0; k < SPL; ++k) {
+      MLOB_ROWS(k) {
         const bool ok = d.Q(k) > 0 && (n == 0 || (S == 0 ? d.P(k) < prev : d.P(k) > prev));
         if (ok) lb = better_of<S>(lb, d.P(k));
       }
@@ -1077,8 +1074,7 @@ struct WarpEnv {
       // per-lane sum < SPL * 2^31: reduce as 16-bit-split halves so the 32-bit
       // redux.sync add cannot overflow
       uint64_t s64 = 0;
-#pragma unroll (SMEM ? 4 : SPL)
-      for (int k = 0; k < SPL; ++k)
+      MLOB_ROWS(k)
         if (d.P(k) == lvl) s64 += static_cast<uint32_t>(d.Q(k));
       const uint32_t lo = __reduce_add_sync(FULLMASK, static_cast<uint32_t>(s64 & 0xffffu));
       const uint32_t hi = __reduce_add_sync(FULLMASK, static_cast<uint32_t>(s64 >> 16));
@@ -1147,8 +1143,7 @@ struct WarpEnv {
   template <int S>
   __device__ __forceinline__ int compact_side(ActTmp* tmp, int base, int cap) {
     SideT& d = sd<S>();
-#pragma unroll (SMEM ? 4 : SPL)
-    for (int k = 0; k < SPL; ++k) {
+    MLOB_ROWS(k) {
       const bool is_ag = d.Q(k) > 0 && (d.ST(k) & 0xffu) != 0;
       const uint32_t b = __ballot_sync(FULLMASK, is_ag);
       if (b == 0) continue;
@@ -1359,8 +1354,7 @@ struct WarpEnv {
     }
     uint32_t m = 0;
     bool far = false;
-#pragma unroll (SMEM ? 4 : SPL)
-    for (int k = 0; k < SPL; ++k) {
+    MLOB_ROWS(k) {
       if (d.Q(k) > 0) {
         const uint32_t off = static_cast<uint32_t>(S == 0 ? best - d.P(k) : d.P(k) - best);
         if (off < 32)
@@ -1378,8 +1372,7 @@ struct WarpEnv {
     for (int i = 1; i < n; ++i) mm &= mm - 1;
     const uint32_t cut = static_cast<uint32_t>(__ffs(mm) - 1);  // offset of the n-th level
     uint64_t sa = 0, st = 0;
-#pragma unroll (SMEM ? 4 : SPL)
-    for (int k = 0; k < SPL; ++k) {
+    MLOB_ROWS(k) {
       const uint32_t off = static_cast<uint32_t>(S == 0 ? best - d.P(k) : d.P(k) - best);
       const uint32_t q = d.Q(k) > 0 ? static_cast<uint32_t>(d.Q(k)) : 0u;
       sa += off <= cut ? q : 0u;
@@ -1491,8 +1484,7 @@ struct WarpEnv {
   template <int S>
   __device__ __forceinline__ void init_side(const DevLevel* lv, uint32_t n, uint64_t id_base, uint32_t seq_base) {
     SideT& d = sd<S>();
-#pragma unroll (SMEM ? 4 : SPL)
-    for (int k = 0; k < SPL; ++k) {
+    MLOB_ROWS(k) {
       const uint32_t i = static_cast<uint32_t>(k * kWarp + lane);
       if (i < n) {
         const uint64_t id = id_base + i;
