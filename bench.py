@@ -246,8 +246,9 @@ def gpu_arm(args) -> None:
     venv.synchronize()
     allreduce(stats)
 
-    # e2e through the public API with host buffers: pinned actions H2D, step,
-    # rewards + dones + observations D2H, every step
+    # e2e through the public API with host buffers, every step: pinned actions
+    # H2D, step, rewards + dones + per-type observations and reset flags D2H
+    # (mlob_venv_step_io: one call; the copies overlap the chunked step)
     A = venv.n_agents
     rng = np.random.default_rng(1234)
     ar = np.array([abi.action_arity(cfg.specs[s]) for s in abi.flat_specs(cfg)])
@@ -257,26 +258,27 @@ def gpu_arm(args) -> None:
                 for t in range(cfg.n_specs)]
     rew = torch.empty((n_local, A), dtype=torch.float64).pin_memory()
     dn = torch.empty((n_local, A), dtype=torch.uint8).pin_memory()
-    rs = torch.empty(max(venv.n_streams(t) for t in range(cfg.n_specs)), dtype=torch.uint8).pin_memory()
-    from paper_2511_02136_b200 import env as E
-    L = E.lib()
+    rsb = [torch.empty(venv.n_streams(t), dtype=torch.uint8).pin_memory() for t in range(cfg.n_specs)]
     e_steps = max(3, min(args.steps, args.e2e_steps))
+
+    def e2e_step():
+        venv.step_io(actions=acts, rewards=rew, dones=dn, obs=obs_bufs, resets=rsb)
+
+    e2e_step()  # warm-up (creates the copy streams)
+    em0 = venv.messages_processed()
     barrier()
     w0 = time.perf_counter()
     for _ in range(e_steps):
-        E._check(L.mlob_venv_set_actions(venv.h, acts.data_ptr(), 0))
-        venv.step()
-        E._check(L.mlob_venv_rewards(venv.h, rew.data_ptr()))
-        E._check(L.mlob_venv_dones(venv.h, dn.data_ptr()))
-        for ty in range(cfg.n_specs):
-            E._check(L.mlob_venv_gather(venv.h, ty, obs_bufs[ty].data_ptr(), rs.data_ptr()))
+        e2e_step()
     torch.cuda.synchronize()
     e_wall = torch.tensor([time.perf_counter() - w0], dtype=torch.float64, device="cuda")
     allreduce(e_wall, dist.ReduceOp.MAX)
-    e_msgs = msgs_all / args.steps * e_steps  # same per-step message volume
+    e_m = torch.tensor([venv.messages_processed() - em0], dtype=torch.float64, device="cuda")
+    allreduce(e_m)
+    e_msgs = float(e_m.item())
     h2d = acts.numel() * 4
     d2h = rew.numel() * 8 + dn.numel() + sum(b.numel() * 8 for b in obs_bufs) + \
-        sum(venv.n_streams(t) for t in range(cfg.n_specs))
+        sum(b.numel() for b in rsb)
     e2e_val = e_msgs / float(e_wall.item())
 
     if rank != 0:

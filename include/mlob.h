@@ -393,6 +393,26 @@ const double* mlob_venv_rewards_device(const mlob_venv* v);
 const uint8_t* mlob_venv_dones_device(const mlob_venv* v);
 /* MarketEnv::output().infos, [n_envs_local * n_agents] (env.hpp:445-464). */
 mlob_status mlob_venv_infos(mlob_venv* v, mlob_agent_info* out);
+
+/* One collect_rollout iteration's env I/O in a single call (set_action,
+ * step_all, reward/done, then the next gather: rollout.hpp:72-98): host action ids in,
+ * host rewards / dones / infos / per-type obs + reset flags out, same layouts
+ * as the separate calls.  Any pointer may be NULL (actions NULL = step with
+ * the current actions).  Actions are range-checked on the device before any
+ * env steps (actions.hpp:69-70; a bad id fails with MLOB_E_OUT_OF_RANGE and
+ * leaves every env unchanged).  The step runs in env chunks on two streams
+ * while a copy stream returns each finished chunk's outputs, so the
+ * transfers overlap the step.  Host buffers should be page-locked for the
+ * overlap.  Returns when every output is in host memory. */
+typedef struct mlob_step_io {
+  const int32_t* actions;                  /* [n_envs_local * n_agents] */
+  double* rewards;                         /* [n_envs_local * n_agents] */
+  uint8_t* dones;                          /* [n_envs_local * n_agents] */
+  mlob_agent_info* infos;                  /* [n_envs_local * n_agents] */
+  double* obs[MLOB_MAX_SPECS];             /* per type [n_streams(t) * obs_dim(t)] */
+  uint8_t* resets[MLOB_MAX_SPECS];         /* per type [n_streams(t)] */
+} mlob_step_io;
+mlob_status mlob_venv_step_io(mlob_venv* v, const mlob_step_io* io);
 /* MarketEnv::output().obs for one env, all agents concatenated. */
 mlob_status mlob_venv_env_obs(mlob_venv* v, uint64_t env, double* out, uint64_t cap);
 

@@ -134,6 +134,13 @@ class SynthConfig(C.Structure):
                 ("state_depth", u64)]
 
 
+class StepIO(C.Structure):
+    """mlob_step_io: host buffers of one fused step (NULL = skip)."""
+    _fields_ = [("actions", C.c_void_p), ("rewards", C.c_void_p), ("dones", C.c_void_p),
+                ("infos", C.c_void_p), ("obs", C.c_void_p * MAX_SPECS),
+                ("resets", C.c_void_p * MAX_SPECS)]
+
+
 class VenvDesc(C.Structure):
     _fields_ = [("store", C.c_void_p), ("cfg", EnvConfig), ("episode_pool", C.POINTER(u64)),
                 ("pool_len", u64), ("seed", u64), ("n_envs_global", u64),

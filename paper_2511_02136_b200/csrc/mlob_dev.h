@@ -164,6 +164,8 @@ struct __align__(16) KParams {
   const uint64_t* reset_episodes;  // reset kernel: per-env episode
   uint32_t* error;
   const DevCfg* cfg;  // device copy; staged into shared memory by each block
+  const uint32_t* gate;  // optional: non-zero word = skip the launch (rejected actions)
+  uint64_t _pad_gate;
 };
 
 }  // namespace mlob

@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL
   __shared__ __align__(16) StagedParams sp_;
   stage_params(sp_, kparam);
   const KParams& kp = sp_.kp;
+  if (kp.gate && *kp.gate) return;  // the batch's actions were rejected: no env steps
   const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarpsPerBlock;
   // dynamic work distribution (MLOB_PERSIST): the first env of each warp is
@@ -382,6 +383,30 @@ __global__ void sum_msgs_kernel(const EnvHdr* hdr, uint64_t n, unsigned long lon
   if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
 }
 
+// actions.hpp:69-70 range check of a whole batch of action ids on the device;
+// any failure sets kErrBadAction and closes the gate of the following step.
+__global__ void validate_actions_kernel(const int32_t* ids, uint64_t n, const DevCfg* cfg, uint32_t* error,
+                                        uint32_t* gate) {
+  __shared__ uint32_t ar[MLOB_MAX_AGENTS];
+  const int A = cfg->n_agents;
+  if (threadIdx.x < A) ar[threadIdx.x] = static_cast<uint32_t>(cfg->specs[cfg->flat_spec[threadIdx.x]].arity);
+  __syncthreads();
+  bool bad = false;
+  for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    bad |= static_cast<uint32_t>(ids[i]) >= ar[i % A];
+  if (__any_sync(FULLMASK, bad) && (threadIdx.x & 31) == 0) {
+    atomicOr(error, static_cast<uint32_t>(kErrBadAction));
+    *gate = 1;
+  }
+}
+
+// per-stream reset flags of one type: resets[e * count + k] = just_reset[e]
+__global__ void expand_resets_kernel(const uint8_t* just_reset, uint64_t n_envs, int count, uint8_t* out) {
+  for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_envs * count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = just_reset[i / count];
+}
+
 __global__ void clear_finished_kernel(EnvHdr* hdr, uint64_t n) {
   for (uint64_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     hdr[e].episodes_finished = 0;
@@ -463,6 +488,20 @@ cudaError_t launch_stats(const KParams& kp, const DevCfg& cfg, double* out, cuda
   cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double) * 5 * cfg.n_specs, s);
   if (e != cudaSuccess) return e;
   stats_kernel<<<dim3(grid_for(kp.n_envs), cfg.n_specs), 256, 0, s>>>(kp, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_validate_actions(const int32_t* ids, uint64_t n, const DevCfg* cfg, uint32_t* error,
+                                    uint32_t* gate, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(gate, 0, sizeof(uint32_t), s);
+  if (e != cudaSuccess) return e;
+  validate_actions_kernel<<<grid_for(n), 256, 0, s>>>(ids, n, cfg, error, gate);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expand_resets(const uint8_t* just_reset, uint64_t n_envs, int count, uint8_t* out,
+                                 cudaStream_t s) {
+  expand_resets_kernel<<<grid_for(n_envs * count), 256, 0, s>>>(just_reset, n_envs, count, out);
   return cudaGetLastError();
 }
 

@@ -22,6 +22,10 @@ cudaError_t launch_step(const KParams& kp, const DevCfg& cfg, int spl, cudaStrea
 cudaError_t launch_reset(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s);
 cudaError_t launch_stats(const KParams& kp, const DevCfg& cfg, double* out, cudaStream_t s);
 cudaError_t launch_sum_msgs(const EnvHdr* hdr, uint64_t n, unsigned long long* out, cudaStream_t s);
+cudaError_t launch_validate_actions(const int32_t* ids, uint64_t n, const DevCfg* cfg, uint32_t* error,
+                                    uint32_t* gate, cudaStream_t s);
+cudaError_t launch_expand_resets(const uint8_t* just_reset, uint64_t n_envs, int count, uint8_t* out,
+                                 cudaStream_t s);
 cudaError_t launch_clear_finished(EnvHdr* hdr, uint64_t n, cudaStream_t s);
 }  // namespace mlob
 
@@ -104,11 +108,18 @@ struct mlob_venv {
   uint32_t flags = 0, trade_cap = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // step_io pipeline: second compute stream, copy stream, per-chunk events
+  cudaStream_t stream2 = nullptr, copy_stream = nullptr;
+  std::vector<cudaEvent_t> io_events;
+  uint32_t* d_gate = nullptr;
+  uint8_t* d_resets[MLOB_MAX_SPECS] = {};
   std::vector<uint64_t> starts;
   std::vector<EpState> ep_state;
   std::vector<uint64_t> pool;  // empty = identity
   std::vector<uint64_t> genv;  // global env index per local env
-  std::vector<int32_t> steps;  // host mirror of per-env step (-1 = never reset)
+  // host mirror of the per-env step: resets reset every env and steps step every
+  // env, so all envs share it (-1 = never reset)
+  int32_t step_ctr = -1;
   int action_mode = kActIds;
   uint64_t launches = 0;
   std::vector<void*> allocs;
@@ -151,6 +162,12 @@ struct mlob_venv {
   ~mlob_venv() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
+    for (cudaStream_t s : {stream2, copy_stream})
+      if (s) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
+    for (cudaEvent_t e : io_events) cudaEventDestroy(e);
     for (void* p : allocs) cudaFree(p);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
@@ -626,7 +643,7 @@ mlob_status mlob_venv_create(const mlob_venv_desc* desc, mlob_venv** out) {
     v->genv.resize(v->n_envs);
     for (uint64_t e = 0; e < v->n_envs; ++e)
       v->genv[e] = desc->env_indices ? desc->env_indices[e] : desc->env_index_base + e;
-    v->steps.assign(v->n_envs, -1);
+    v->step_ctr = -1;
     build_devcfg(*v);
 
     v->set_device();
@@ -708,7 +725,7 @@ static void do_reset(mlob_venv* v, const std::vector<uint64_t>& eps) {
   const KParams kp = v->params();
   cuda_check(launch_reset(kp, v->dcfg, v->spl, v->stream), "reset kernel");
   ++v->launches;
-  std::fill(v->steps.begin(), v->steps.end(), 0);
+  v->step_ctr = 0;
 }
 
 mlob_status mlob_venv_reset_all(mlob_venv* v) {
@@ -723,6 +740,19 @@ mlob_status mlob_venv_reset_envs(mlob_venv* v, const uint64_t* episodes) {
   return guarded([&] { do_reset(v, std::vector<uint64_t>(episodes, episodes + v->n_envs)); });
 }
 
+// actions.hpp:69-70: the first out-of-range id, reported like set_action does
+static void fail_bad_action(const mlob_venv* v, const int32_t* ids) {
+  const uint64_t n = v->n_envs * v->A;
+  for (uint64_t i = 0; i < n; ++i) {
+    const int a = static_cast<int>(i % v->A);
+    const int ar = v->dcfg.specs[v->dcfg.flat_spec[a]].arity;
+    if (ids[i] < 0 || ids[i] >= ar)
+      fail(MLOB_E_OUT_OF_RANGE, "action id " + std::to_string(ids[i]) + " out of range for agent " +
+                                    std::to_string(a) + " (arity " + std::to_string(ar) + ")");
+  }
+  fail(MLOB_E_OUT_OF_RANGE, "action id out of range for its action space");
+}
+
 mlob_status mlob_venv_set_actions(mlob_venv* v, const int32_t* ids, int on_device) {
   return guarded([&] {
     const uint64_t n = v->n_envs * v->A;
@@ -734,14 +764,10 @@ mlob_status mlob_venv_set_actions(mlob_venv* v, const int32_t* ids, int on_devic
       bool bad = false;
       for (uint64_t e = 0, i = 0; e < v->n_envs; ++e)
         for (int a = 0; a < v->A; ++a, ++i) bad |= static_cast<uint32_t>(ids[i]) >= ar[a];
-      if (bad)
-        for (uint64_t i = 0; i < n; ++i) {
-          const int a = static_cast<int>(i % v->A);
-          if (static_cast<uint32_t>(ids[i]) >= ar[a])
-            fail(MLOB_E_OUT_OF_RANGE, "action id " + std::to_string(ids[i]) + " out of range for agent " +
-                                          std::to_string(a) + " (arity " + std::to_string(ar[a]) + ")");
-        }
+      if (bad) fail_bad_action(v, ids);
       cuda_check(cudaMemcpyAsync(v->d_actions, ids, n * 4, cudaMemcpyHostToDevice, v->stream), "H2D");
+      // a page-locked `ids` is read asynchronously: the caller may reuse it on return
+      cuda_check(cudaStreamSynchronize(v->stream), "sync");
     } else {
       cuda_check(cudaMemcpyAsync(v->d_actions, ids, n * 4, cudaMemcpyDeviceToDevice, v->stream), "D2D");
     }
@@ -777,11 +803,14 @@ mlob_status mlob_venv_set_direct_actions(mlob_venv* v, const mlob_agent_action* 
   });
 }
 
+static void advance_step(mlob_venv* v) {
+  if (++v->step_ctr >= v->cfg.steps_per_episode && (v->flags & MLOB_VENV_AUTO_RESET)) v->step_ctr = 0;
+}
+
 static void do_step(mlob_venv* v, int mode, uint64_t bench_seed, uint64_t global_step) {
   const bool auto_reset = (v->flags & MLOB_VENV_AUTO_RESET) != 0;
-  for (uint64_t e = 0; e < v->n_envs; ++e)
-    if (v->steps[e] < 0 || (!auto_reset && v->steps[e] >= v->cfg.steps_per_episode))
-      fail(MLOB_E_LOGIC, "MarketEnv::step: episode is terminal; reset first");
+  if (v->step_ctr < 0 || (!auto_reset && v->step_ctr >= v->cfg.steps_per_episode))
+    fail(MLOB_E_LOGIC, "MarketEnv::step: episode is terminal; reset first");
   v->set_device();
   KParams kp = v->params();
   kp.action_mode = mode;
@@ -790,10 +819,7 @@ static void do_step(mlob_venv* v, int mode, uint64_t bench_seed, uint64_t global
   cuda_check(cudaMemsetAsync(v->d_ticket, 0, sizeof(unsigned long long), v->stream), "ticket reset");
   cuda_check(launch_step(kp, v->dcfg, v->spl, v->stream), "step kernel");
   ++v->launches;
-  for (auto& s : v->steps) {
-    ++s;
-    if (auto_reset && s >= v->cfg.steps_per_episode) s = 0;
-  }
+  advance_step(v);
 }
 
 mlob_status mlob_venv_step(mlob_venv* v) {
@@ -820,16 +846,17 @@ mlob_status mlob_venv_gather(mlob_venv* v, int type, double* obs, uint8_t* reset
     if (obs)
       cuda_check(cudaMemcpyAsync(obs, v->d_obs[type], v->n_envs * cnt * dim * 8, cudaMemcpyDeviceToHost,
                                  v->stream), "D2H");
-    std::vector<uint8_t> jr;
-    if (resets) {
-      jr.resize(v->n_envs);
-      cuda_check(cudaMemcpyAsync(jr.data(), v->d_just_reset, v->n_envs, cudaMemcpyDeviceToHost, v->stream),
-                 "D2H");
+    if (resets) {  // per-stream flags (rollout.hpp:206-211), expanded on the device
+      const uint8_t* src = v->d_just_reset;
+      if (cnt > 1) {
+        if (!v->d_resets[type]) v->d_resets[type] = v->alloc<uint8_t>(v->n_envs * cnt, "resets");
+        cuda_check(launch_expand_resets(v->d_just_reset, v->n_envs, static_cast<int>(cnt), v->d_resets[type],
+                                        v->stream), "resets");
+        src = v->d_resets[type];
+      }
+      cuda_check(cudaMemcpyAsync(resets, src, v->n_envs * cnt, cudaMemcpyDeviceToHost, v->stream), "D2H");
     }
     v->check_device_errors();
-    if (resets)
-      for (uint64_t e = 0; e < v->n_envs; ++e)
-        for (uint64_t k = 0; k < cnt; ++k) resets[e * cnt + k] = jr[e];
   });
 }
 
@@ -854,6 +881,134 @@ mlob_status mlob_venv_dones(mlob_venv* v, uint8_t* out) {
 }
 mlob_status mlob_venv_infos(mlob_venv* v, mlob_agent_info* out) {
   return guarded([&] { d2h(v, out, v->d_infos, v->n_envs * v->A); });
+}
+
+// ---- fused env I/O: chunked step with overlapped transfers -----------------
+
+// KParams of the env range [c0, c0 + n): every per-env array offset by c0,
+// the global env identity (RNG keys, episode pool) kept
+static KParams chunk_params(const mlob_venv* v, const KParams& k0, uint64_t c0, uint64_t n) {
+  KParams k = k0;
+  const uint64_t A = static_cast<uint64_t>(v->A);
+  const size_t bs = static_cast<size_t>(2 * v->spl * kWarp) * c0;
+  k.bk_p += bs;
+  k.bk_q += bs;
+  k.bk_id += bs;
+  k.bk_st += bs;
+  k.hdr += c0;
+  k.agents += c0 * A;
+  k.active += c0 * A * kMaxActive;
+  if (k.action_ids) k.action_ids += c0 * A;
+  if (k.action_direct) k.action_direct += c0 * A;
+  for (int t = 0; t < v->cfg.n_specs; ++t)
+    k.obs[t] += c0 * static_cast<uint64_t>(v->cfg.specs[t].count) * static_cast<uint64_t>(v->dcfg.specs[t].obs_dim);
+  k.rewards += c0 * A;
+  k.dones += c0 * A;
+  k.infos += c0 * A;
+  k.just_reset += c0;
+  k.t_pv += c0 * A;
+  k.t_slip += c0 * A;
+  k.t_comp += c0 * A;
+  k.t_inv += c0 * A;
+  if (k.trades) k.trades += c0 * v->trade_cap;
+  if (k.timing) k.timing += c0 * 16;
+  if (k.env_seed) k.env_seed += c0;
+  if (k.env_index) k.env_index += c0;
+  k.env_index_base += c0;
+  k.n_envs = n;
+  return k;
+}
+
+static uint64_t io_chunk_envs(uint64_t n) {
+  if (const char* e = std::getenv("MLOB_IO_CHUNKS")) {  // diagnostics: fixed chunk count
+    const uint64_t c = std::strtoull(e, nullptr, 10);
+    if (c > 0) return (n + c - 1) / c;
+  }
+  // ≤ 8 chunks of ≥ 64k envs: each chunk is many waves, so the per-chunk tail is
+  // small; the last chunk's copies are the only exposed transfer
+  uint64_t c = (n + 7) / 8;
+  if (c < 65536) c = 65536;
+  return (c + 1279) / 1280 * 1280;
+}
+
+mlob_status mlob_venv_step_io(mlob_venv* v, const mlob_step_io* io) {
+  return guarded([&] {
+    if (!io) fail(MLOB_E_INVALID_ARGUMENT, "step_io: null descriptor");
+    const bool auto_reset = (v->flags & MLOB_VENV_AUTO_RESET) != 0;
+    if (v->step_ctr < 0 || (!auto_reset && v->step_ctr >= v->cfg.steps_per_episode))
+      fail(MLOB_E_LOGIC, "MarketEnv::step: episode is terminal; reset first");
+    v->set_device();
+    const uint64_t n = v->n_envs, A = static_cast<uint64_t>(v->A);
+    const uint64_t chunk = io_chunk_envs(n);
+    const uint64_t nc = (n + chunk - 1) / chunk;
+    if (!v->copy_stream) {
+      cuda_check(cudaStreamCreateWithFlags(&v->stream2, cudaStreamNonBlocking), "stream");
+      cuda_check(cudaStreamCreateWithFlags(&v->copy_stream, cudaStreamNonBlocking), "stream");
+      v->d_gate = v->alloc<uint32_t>(1, "gate");
+    }
+    while (v->io_events.size() < nc + 3) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      v->io_events.push_back(e);
+    }
+    for (int t = 0; t < v->cfg.n_specs; ++t)
+      if (io->resets[t] && v->cfg.specs[t].count > 1 && !v->d_resets[t])
+        v->d_resets[t] = v->alloc<uint8_t>(n * static_cast<uint64_t>(v->cfg.specs[t].count), "resets");
+    KParams k0 = v->params();
+    if (io->actions) {  // stage + validate the whole batch before any env steps
+      cuda_check(cudaMemcpyAsync(v->d_actions, io->actions, n * A * 4, cudaMemcpyHostToDevice, v->stream), "H2D");
+      cuda_check(launch_validate_actions(v->d_actions, n * A, v->d_cfg, v->d_error, v->d_gate, v->stream),
+                 "validate kernel");
+      v->action_mode = kActIds;
+      k0.gate = v->d_gate;
+    }
+    k0.action_mode = v->action_mode;
+    cudaEvent_t* ev = v->io_events.data();
+    cuda_check(cudaEventRecord(ev[0], v->stream), "event");
+    cuda_check(cudaStreamWaitEvent(v->stream2, ev[0], 0), "wait");
+    const auto d2h = [&](void* dst, const void* src, uint64_t bytes) {
+      if (dst && bytes) cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, v->copy_stream), "D2H");
+    };
+    for (uint64_t i = 0; i < nc; ++i) {
+      const uint64_t c0 = i * chunk, m = std::min(chunk, n - c0);
+      cudaStream_t s = (i & 1) ? v->stream2 : v->stream;
+      cuda_check(launch_step(chunk_params(v, k0, c0, m), v->dcfg, v->spl, s), "step kernel");
+      ++v->launches;
+      for (int t = 0; t < v->cfg.n_specs; ++t)
+        if (io->resets[t] && v->cfg.specs[t].count > 1) {
+          const int cnt = v->cfg.specs[t].count;
+          cuda_check(launch_expand_resets(v->d_just_reset + c0, m, cnt, v->d_resets[t] + c0 * cnt, s), "resets");
+          ++v->launches;
+        }
+      cuda_check(cudaEventRecord(ev[1 + i], s), "event");
+      cuda_check(cudaStreamWaitEvent(v->copy_stream, ev[1 + i], 0), "wait");
+      d2h(io->rewards ? io->rewards + c0 * A : nullptr, v->d_rewards + c0 * A, m * A * 8);
+      d2h(io->dones ? io->dones + c0 * A : nullptr, v->d_dones + c0 * A, m * A);
+      d2h(io->infos ? io->infos + c0 * A : nullptr, v->d_infos + c0 * A, m * A * sizeof(mlob_agent_info));
+      for (int t = 0; t < v->cfg.n_specs; ++t) {
+        const uint64_t cnt = static_cast<uint64_t>(v->cfg.specs[t].count);
+        const uint64_t w = cnt * static_cast<uint64_t>(v->dcfg.specs[t].obs_dim);
+        d2h(io->obs[t] ? io->obs[t] + c0 * w : nullptr, v->d_obs[t] + c0 * w, m * w * 8);
+        if (io->resets[t])
+          d2h(io->resets[t] + c0 * cnt, cnt > 1 ? v->d_resets[t] + c0 * cnt : v->d_just_reset + c0, m * cnt);
+      }
+    }
+    // join: later work on the handle's stream is ordered after both streams and the copies
+    cuda_check(cudaEventRecord(ev[nc + 1], v->stream2), "event");
+    cuda_check(cudaEventRecord(ev[nc + 2], v->copy_stream), "event");
+    cuda_check(cudaStreamWaitEvent(v->stream, ev[nc + 1], 0), "wait");
+    cuda_check(cudaStreamWaitEvent(v->stream, ev[nc + 2], 0), "wait");
+    uint32_t e = 0;
+    cuda_check(cudaMemcpyAsync(&e, v->d_error, sizeof e, cudaMemcpyDeviceToHost, v->stream), "error word");
+    cuda_check(cudaStreamSynchronize(v->stream), "stream sync");
+    if ((e & kErrBadAction) && io->actions) {  // gate closed: no env stepped
+      cuda_check(cudaMemsetAsync(v->d_error, 0, sizeof e, v->stream), "error reset");
+      cuda_check(cudaStreamSynchronize(v->stream), "stream sync");
+      fail_bad_action(v, io->actions);
+    }
+    advance_step(v);
+    if (e) v->check_device_errors();
+  });
 }
 
 mlob_status mlob_venv_env_obs(mlob_venv* v, uint64_t env, double* out, uint64_t cap) {
@@ -928,7 +1083,7 @@ mlob_status mlob_venv_read_scalars(mlob_venv* v, uint64_t env, mlob_env_scalars*
     d2h(v, &h, v->d_hdr + env, 1);
     std::memset(o, 0, sizeof *o);
     o->step = h.step;
-    o->terminal = v->steps[env] < 0 ? 1 : h.terminal;
+    o->terminal = v->step_ctr < 0 ? 1 : h.terminal;
     o->episode = h.episode;
     o->mid_half = h.mid_half;
     o->prev_mid_half = h.prev_mid_half;

@@ -89,6 +89,7 @@ _SIGS = {
     "mlob_venv_rewards_device": (_vp, [_vp]),
     "mlob_venv_dones_device": (_vp, [_vp]),
     "mlob_venv_infos": (C.c_int, [_vp, _vp]),
+    "mlob_venv_step_io": (C.c_int, [_vp, _P(abi.StepIO)]),
     "mlob_venv_env_obs": (C.c_int, [_vp, C.c_uint64, _P(C.c_double), C.c_uint64]),
     "mlob_venv_episode_stats": (C.c_int, [_vp, C.c_int, _P(EpisodeStats)]),
     "mlob_venv_episode_stats_device": (C.c_int, [_vp, _vp]),
@@ -147,6 +148,20 @@ INFO_DTYPE = np.dtype([("inventory", "<i8"), ("cash", "<i8"), ("portfolio_value"
 
 
 # ---- stores --------------------------------------------------------------------
+
+def _host_ptr(x, dtype, n):
+    """Address of a contiguous host buffer of n elements of `dtype` (numpy
+    array or CPU torch tensor); None -> NULL."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):  # torch tensor
+        if x.is_cuda or not x.is_contiguous() or x.numel() != n or x.element_size() != np.dtype(dtype).itemsize:
+            raise ValueError(f"expected a contiguous host tensor of {n} x {np.dtype(dtype)}")
+        return x.data_ptr()
+    if not isinstance(x, np.ndarray) or not x.flags.c_contiguous or x.size != n or x.dtype != np.dtype(dtype):
+        raise ValueError(f"expected a C-contiguous {np.dtype(dtype)} array of {n} elements")
+    return x.ctypes.data
+
 
 class HostStore:
     """data::MessageStore in host memory (contiguous messages + sampled states)."""
@@ -352,6 +367,23 @@ class _Venv:
     def synchronize(self) -> None:
         _check(lib().mlob_venv_synchronize(self.h))
 
+    def step_io(self, actions=None, rewards=None, dones=None, infos=None, obs=None, resets=None) -> None:
+        """Fused set_actions + step + rewards/dones/infos + per-type gather
+        (mlob_venv_step_io).  Buffers are C-contiguous host numpy arrays or
+        (page-locked, for overlapped copies) CPU torch tensors of the layouts
+        the separate calls use; obs / resets are per-type lists, None skips."""
+        io = abi.StepIO()
+        io.actions = _host_ptr(actions, np.int32, self.n_envs * self.n_agents)
+        io.rewards = _host_ptr(rewards, np.float64, self.n_envs * self.n_agents)
+        io.dones = _host_ptr(dones, np.uint8, self.n_envs * self.n_agents)
+        io.infos = _host_ptr(infos, INFO_DTYPE, self.n_envs * self.n_agents)
+        for t in range(self.n_types()):
+            if obs is not None and obs[t] is not None:
+                io.obs[t] = _host_ptr(obs[t], np.float64, self.n_streams(t) * self.obs_dim(t))
+            if resets is not None and resets[t] is not None:
+                io.resets[t] = _host_ptr(resets[t], np.uint8, self.n_streams(t))
+        _check(lib().mlob_venv_step_io(self.h, C.byref(io)))
+
     def rewards(self) -> np.ndarray:
         out = np.zeros((self.n_envs, self.n_agents), dtype=np.float64)
         _check(lib().mlob_venv_rewards(self.h, _vp(out.ctypes.data)))
@@ -411,6 +443,8 @@ class MarketVecEnv(_Venv):
         kw.setdefault("auto_reset", True)
         super().__init__(store, cfg, n_envs, seed, pool=episode_pool, **kw)
         self._actions = np.zeros((n_envs, self.n_agents), dtype=np.int32)
+        self._rewards = np.zeros((n_envs, self.n_agents), dtype=np.float64)
+        self._dones = np.zeros((n_envs, self.n_agents), dtype=np.uint8)
 
     def reset_all(self) -> None:  # rollout.hpp:194-200
         _check(lib().mlob_venv_reset_all(self.h))
@@ -430,21 +464,20 @@ class MarketVecEnv(_Venv):
         count = self.cfg.specs[t].count
         self._actions[stream // count, self.type_offset[t] + stream % count] = action
 
-    def step_all(self) -> None:  # rollout.hpp:224-234
-        self.set_actions(self._actions)
-        self.step()
+    def step_all(self) -> None:  # rollout.hpp:224-234 (+ the reward/done caches)
+        self.step_io(actions=self._actions, rewards=self._rewards, dones=self._dones)
 
     def _locate(self, t, s):
         count = self.cfg.specs[t].count
         return s // count, self.type_offset[t] + s % count
 
-    def reward(self, t: int, stream: int) -> float:
+    def reward(self, t: int, stream: int) -> float:  # rollout.hpp:236-239
         e, a = self._locate(t, stream)
-        return float(self.rewards()[e, a])
+        return float(self._rewards[e, a])
 
-    def done(self, t: int, stream: int) -> bool:
+    def done(self, t: int, stream: int) -> bool:  # rollout.hpp:240-243
         e, a = self._locate(t, stream)
-        return bool(self.dones()[e, a])
+        return bool(self._dones[e, a])
 
 
 class MarketEnvBatch(_Venv):

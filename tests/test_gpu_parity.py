@@ -264,3 +264,54 @@ def test_two_shards_equal_one_batch():
     ref = reduce_episode_stats(full)
     assert torch.equal(tot[:, [0, 1, 3, 4]], ref[:, [0, 1, 3, 4]])
     assert float(tot[:, 4].sum()) > 0
+
+
+@pytest.mark.parametrize("chunks", ["1", "3"])
+def test_step_io_matches_separate_calls(monkeypatch, chunks):
+    """mlob_venv_step_io (chunked step on two streams + overlapped copies) gives
+    the same outputs and state as set_actions + step + rewards/dones/infos/gather,
+    across auto-resets; a bad action id is rejected before any env steps."""
+    import torch
+    monkeypatch.setenv("MLOB_IO_CHUNKS", chunks)
+    cfg = abi.env_config([abi.agent_spec(abi.MARKET_MAKER, count=2), abi.agent_spec(abi.EXECUTOR),
+                          abi.agent_spec(abi.DIRECTIONAL)],
+                         steps_per_episode=6, messages_per_step=30, start_stride_steps=2)
+    dev = dev_store({"state_sample_every": 30})
+    n = 7
+    a, b = (MarketVecEnv(dev, cfg, seed=9, n_envs=n) for _ in range(2))
+    a.reset_all()
+    b.reset_all()
+    A, T = a.n_agents, a.n_types()
+    ar = np.array([abi.action_arity(cfg.specs[s]) for s in abi.flat_specs(cfg)])
+    rng = np.random.default_rng(5)
+    pin = lambda shape, dt: torch.empty(shape, dtype=dt).pin_memory()  # noqa: E731
+    obs = [pin((b.n_streams(t), b.obs_dim(t)), torch.float64) for t in range(T)]
+    rst = [pin(b.n_streams(t), torch.uint8) for t in range(T)]
+    rew, dn = pin((n, A), torch.float64), pin((n, A), torch.uint8)
+    infos = np.zeros((n, A), dtype=a.infos().dtype)
+    acts = pin((n, A), torch.int32)
+    for step in range(15):
+        if step == 4:  # rejected batch: nothing changes
+            before = [(a.view(e).book(0).tobytes(), a.view(e).book(1).tobytes()) for e in range(n)]
+            bad = acts.clone()
+            bad[n - 1, A - 1] = int(ar[A - 1])
+            with pytest.raises(IndexError):
+                b.step_io(actions=bad)
+            assert [(b.view(e).book(0).tobytes(), b.view(e).book(1).tobytes()) for e in range(n)] == before
+        acts.copy_(torch.from_numpy((rng.integers(0, 1 << 20, size=(n, A)) % ar).astype(np.int32)))
+        a.set_actions(acts.numpy())
+        a.step()
+        b.step_io(actions=acts, rewards=rew, dones=dn, infos=infos, obs=obs, resets=rst)
+        assert rew.numpy().tobytes() == a.rewards().tobytes()
+        assert dn.numpy().tobytes() == a.dones().tobytes()
+        assert infos.tobytes() == a.infos().tobytes()
+        for t in range(T):
+            go, gr = a.gather(t)
+            assert obs[t].numpy().tobytes() == go.tobytes()
+            assert rst[t].numpy().tobytes() == gr.tobytes()
+        for e in range(n):
+            assert b.view(e).scalars().step == a.view(e).scalars().step
+            assert b.view(e).book(0).tobytes() == a.view(e).book(0).tobytes()
+            assert b.view(e).book(1).tobytes() == a.view(e).book(1).tobytes()
+    for t in range(T):
+        assert bytes(a.episode_stats(t)) == bytes(b.episode_stats(t))
