@@ -341,7 +341,7 @@ def main():
     p.add_argument("--envs", type=int, default=0, help="override the env count")
     p.add_argument("--mps", type=int, default=0, help="override messages per step (diagnostics)")
     p.add_argument("--ref-envs", type=int, default=65536)
-    p.add_argument("--cpu-steps", type=int, default=200)
+    p.add_argument("--cpu-steps", type=int, default=300)
     p.add_argument("--e2e-steps", type=int, default=10)
     p.add_argument("--no-cpu", action="store_true")
     args = p.parse_args()

@@ -413,6 +413,67 @@ typedef struct mlob_step_io {
   uint8_t* resets[MLOB_MAX_SPECS];         /* per type [n_streams(t)] */
 } mlob_step_io;
 mlob_status mlob_venv_step_io(mlob_venv* v, const mlob_step_io* io);
+
+/* ---- Scripted policies and cross-play evaluation (ippo/evaluate.hpp) ------ */
+
+/* ippo::PolicyKind (evaluate.hpp:17); Learned is not available on the device. */
+enum { MLOB_POLICY_LEARNED = 0, MLOB_POLICY_TWAP = 1, MLOB_POLICY_AVST = 2, MLOB_POLICY_RANDOM = 3,
+       MLOB_POLICY_NOOP = 4 };
+/* baselines::TwapPriceMode (twap.hpp:11) */
+enum { MLOB_TWAP_AGGRESSIVE = 0, MLOB_TWAP_PASSIVE = 1 };
+
+/* ippo::PolicyChoice (evaluate.hpp:19-25) without the network pointer:
+ * AvSt = baselines::AvStBaseline (avst.hpp:14-17), TWAP = the price mode of
+ * baselines::make_twap_plan (twap.hpp:21-33).  mlob_default_policy() fills
+ * the reference defaults (AvStParams actions.hpp:142-147, gamma_index 1). */
+typedef struct mlob_policy {
+  int32_t kind;
+  int32_t twap_mode;
+  int32_t avst_gamma_index;
+  int32_t n_gamma;
+  double gamma_grid[MLOB_MAX_GAMMA];
+  double kappa;
+  double sigma;
+  double horizon;
+} mlob_policy;
+void mlob_default_policy(int kind, mlob_policy* out);
+
+/* Scripted actions for the next steps (evaluate.hpp:56-99 choose_action,
+ * twap.hpp:37-58, avst.hpp:19-32): env e's agents of type t act by
+ * policies[env_policy[e * n_types + t]] from the env's own state on the
+ * device; Random draws CounterRng(make_key(env seed, EpisodeDraw, env_cell[e],
+ * episode, step, agent)).below(arity) (env_cell NULL = 0).  Stays in force
+ * until set_actions / set_direct_actions. */
+mlob_status mlob_venv_set_policies(mlob_venv* v, const mlob_policy* policies, int n_policies,
+                                   const uint8_t* env_policy, const uint64_t* env_cell);
+
+/* ippo::TypeCellStats / CellStats (evaluate.hpp:27-42), labels omitted. */
+typedef struct mlob_type_cell_stats {
+  double pv_mean;
+  double pv_stderr;
+  double slippage_mean;
+  double slippage_stderr;
+  double completion_mean;
+  int64_t filled_total;
+  int32_t no_fills;
+  int32_t _pad;
+} mlob_type_cell_stats;
+typedef struct mlob_cell_stats {
+  mlob_type_cell_stats per_type[2];
+  int64_t episodes;
+} mlob_cell_stats;
+
+/* ippo::evaluate_matrix (evaluate.hpp:104-217) for scripted policies: every
+ * (row, col, episode) of the cross-play grid is one environment of a single
+ * device batch (env seed = `seed`, env index 0, as the reference's one
+ * MarketEnv), stepped to the episode end; the per-cell statistics are then
+ * formed on the host in the reference's order.  out[n_rows * n_cols],
+ * row-major.  Errors: invalid_argument as the reference (two types, episodes
+ * non-empty); a Learned option -> MLOB_E_INVALID_ARGUMENT. */
+mlob_status mlob_evaluate_matrix(const mlob_store* store, const mlob_env_config* cfg,
+                                 const uint64_t* episodes, uint64_t n_episodes,
+                                 const mlob_policy* type0, int n_type0, const mlob_policy* type1,
+                                 int n_type1, uint64_t seed, int device, mlob_cell_stats* out);
 /* MarketEnv::output().obs for one env, all agents concatenated. */
 mlob_status mlob_venv_env_obs(mlob_venv* v, uint64_t env, double* out, uint64_t cap);
 

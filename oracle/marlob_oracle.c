@@ -1642,3 +1642,156 @@ void orc_random_stream(const orc_stream_config* cfg, uint64_t seed, mlob_message
     out[i] = m;
   }
 }
+
+/* ------------------------------------------------------------------------ */
+/* baselines/twap.hpp, baselines/avst.hpp, ippo/evaluate.hpp (scripted)      */
+
+static void quotes_to_action(const quote_list* q, mlob_agent_action* act) {
+  memset(act, 0, sizeof *act);
+  act->direct = 1;
+  act->n_quotes = q->n;
+  for (int i = 0; i < q->n; ++i) act->quotes[i] = q->q[i];
+}
+
+/* twap_policy (twap.hpp:37-58) over make_twap_plan(task_size, steps) (twap.hpp:21-33) */
+static void twap_action(const env* e, int a, int mode, int step, mlob_agent_action* act) {
+  const agent_state* st = &e->ag[a];
+  const int64_t T = spec_of(e, a)->params.task_size, S = e->cfg.steps_per_episode;
+  const int64_t sched = ((int64_t)(step + 1) * T) / S - ((int64_t)step * T) / S;
+  const int last = step + 1 == S;
+  const int64_t qty = last ? st->task_remaining : (sched < st->task_remaining ? sched : st->task_remaining);
+  quote_list q = {.n = 0};
+  if (qty > 0) {
+    int64_t bid, ask;
+    effective_tops(e, a, &bid, &ask);
+    const int buy = st->task_dir == MLOB_TASK_BUY;
+    const int64_t price = mode == MLOB_TWAP_AGGRESSIVE ? (buy ? ask : bid) : (buy ? bid : ask);
+    ql_push(&q, buy ? MLOB_BID : MLOB_ASK, price, qty);
+  }
+  quotes_to_action(&q, act);
+}
+
+/* avst_policy (avst.hpp:19-32): decode_avst with the baseline's parameters */
+static int avst_action(const env* e, int a, const mlob_policy* p, mlob_agent_action* act) {
+  if (p->avst_gamma_index < 0 || p->avst_gamma_index >= p->n_gamma)
+    return fail(MLOB_E_OUT_OF_RANGE, "avst_policy: gamma_index out of range");
+  mlob_agent_params prm;
+  memset(&prm, 0, sizeof prm);
+  prm.n_gamma = p->n_gamma;
+  memcpy(prm.gamma_grid, p->gamma_grid, sizeof prm.gamma_grid);
+  prm.kappa = p->kappa;
+  prm.sigma = p->sigma;
+  prm.horizon = p->horizon;
+  quote_list q = {.n = 0};
+  const int rc = decode_avst(p->avst_gamma_index, e->mid_half, e->ag[a].inventory, e->step, &prm,
+                             spec_of(e, a)->params.order_size, &q);
+  if (rc != MLOB_OK) return rc;
+  quotes_to_action(&q, act);
+  return MLOB_OK;
+}
+
+/* detail::choose_action (evaluate.hpp:56-99) for the scripted kinds */
+static int choose_action(const env* e, int a, const mlob_policy* p, int step, uint64_t seed,
+                         uint64_t cell_id, uint64_t episode, mlob_agent_action* act) {
+  memset(act, 0, sizeof *act);
+  switch (p->kind) {
+    case MLOB_POLICY_NOOP: act->direct = 1; return MLOB_OK;
+    case MLOB_POLICY_TWAP: twap_action(e, a, p->twap_mode, step, act); return MLOB_OK;
+    case MLOB_POLICY_AVST: return avst_action(e, a, p, act);
+    case MLOB_POLICY_RANDOM: {
+      const uint64_t w[5] = {8 /* EpisodeDraw */, cell_id, episode, (uint64_t)step, (uint64_t)a};
+      crng r = {make_key(seed, 5, w)};
+      act->id = (int)crng_below(&r, (uint64_t)action_arity(spec_of(e, a)));
+      return MLOB_OK;
+    }
+  }
+  return fail(MLOB_E_INVALID_ARGUMENT, "evaluate_matrix: learned policy without a network");
+}
+
+int orc_choose_action(void* e, int a, const mlob_policy* p, int step, uint64_t seed, uint64_t cell_id,
+                      uint64_t episode, mlob_agent_action* out) {
+  return choose_action((const env*)e, a, p, step, seed, cell_id, episode, out);
+}
+
+static void mean_stderr(const double* xs, uint64_t n, double* mean, double* se) { /* evaluate.hpp:188-197 */
+  const double k = (double)n;
+  double m = 0.0;
+  for (uint64_t i = 0; i < n; ++i) m += xs[i];
+  m /= k;
+  double var = 0.0;
+  for (uint64_t i = 0; i < n; ++i) var += (xs[i] - m) * (xs[i] - m);
+  *mean = m;
+  *se = n > 1 ? sqrt(var / (k - 1.0) / k) : 0.0;
+}
+
+int orc_evaluate_matrix(void* store_, const mlob_env_config* cfg, const uint64_t* episodes, uint64_t n_eps,
+                        const mlob_policy* t0, int n0, const mlob_policy* t1, int n1, uint64_t seed,
+                        mlob_cell_stats* out) { /* evaluate.hpp:104-217 */
+  if (cfg->n_specs != 2)
+    return fail(MLOB_E_INVALID_ARGUMENT, "evaluate_matrix: exactly two agent types required");
+  if (n_eps == 0) return fail(MLOB_E_INVALID_ARGUMENT, "evaluate_matrix: empty episode set");
+  for (int i = 0; i < n0 + n1; ++i)
+    if ((i < n0 ? t0[i] : t1[i - n0]).kind == MLOB_POLICY_LEARNED)
+      return fail(MLOB_E_INVALID_ARGUMENT, "evaluate_matrix: learned policy without a network");
+  int status = MLOB_OK;
+  env* e = orc_env_create(store_, cfg, seed, 0, &status);
+  if (!e) return status;
+  const int A = e->n_agents;
+  double* pv[2] = {malloc(n_eps * sizeof(double)), malloc(n_eps * sizeof(double))};
+  double* slip[2] = {malloc(n_eps * sizeof(double)), malloc(n_eps * sizeof(double))};
+  mlob_agent_action acts[MLOB_MAX_AGENTS];
+  for (int row = 0; row < n0 && status == MLOB_OK; ++row)
+    for (int col = 0; col < n1 && status == MLOB_OK; ++col) {
+      const mlob_policy* choice[2] = {&t0[row], &t1[col]};
+      const uint64_t cell_id = (uint64_t)row * 1000 + (uint64_t)col;
+      double completion_sum[2] = {0.0, 0.0};
+      int64_t filled[2] = {0, 0};
+      for (uint64_t k = 0; k < n_eps && status == MLOB_OK; ++k) {
+        const uint64_t ep = episodes[k];
+        if ((status = orc_env_reset(e, ep)) != MLOB_OK) break;
+        for (int step = 0; !e->terminal && status == MLOB_OK; ++step) {
+          for (int a = 0; a < A && status == MLOB_OK; ++a)
+            status = choose_action(e, a, choice[e->flat_spec[a]], step, seed, cell_id, ep, &acts[a]);
+          if (status == MLOB_OK) status = orc_env_step(e, acts, (uint64_t)A);
+        }
+        if (status != MLOB_OK) break;
+        double ep_pv[2] = {0.0, 0.0}, ep_slip[2] = {0.0, 0.0};
+        int type_agents[2] = {0, 0};
+        for (int a = 0; a < A; ++a) {
+          const int tau = e->flat_spec[a];
+          const mlob_agent_info* info = &e->ag[a].info;
+          ep_pv[tau] += info->portfolio_value;
+          ep_slip[tau] += info->slippage_total;
+          ++type_agents[tau];
+          filled[tau] += e->ag[a].filled_total;
+          const mlob_agent_spec* sp = spec_of(e, a);
+          if (sp->type == MLOB_EXECUTOR)
+            completion_sum[tau] += 1.0 - (double)info->task_remaining / (double)sp->params.task_size;
+          else
+            completion_sum[tau] += 0.0;
+        }
+        for (int tau = 0; tau < 2; ++tau) {
+          pv[tau][k] = ep_pv[tau] / type_agents[tau];
+          slip[tau][k] = ep_slip[tau] / type_agents[tau];
+        }
+      }
+      if (status != MLOB_OK) break;
+      mlob_cell_stats* cs = &out[row * n1 + col];
+      memset(cs, 0, sizeof *cs);
+      cs->episodes = (int64_t)n_eps;
+      for (int tau = 0; tau < 2; ++tau) {
+        mlob_type_cell_stats* t = &cs->per_type[tau];
+        mean_stderr(pv[tau], n_eps, &t->pv_mean, &t->pv_stderr);
+        t->filled_total = filled[tau];
+        t->no_fills = filled[tau] == 0;
+        if (!t->no_fills) mean_stderr(slip[tau], n_eps, &t->slippage_mean, &t->slippage_stderr);
+        t->completion_mean = completion_sum[tau] / ((double)n_eps * (double)cfg->specs[tau].count);
+      }
+    }
+  for (int tau = 0; tau < 2; ++tau) {
+    free(pv[tau]);
+    free(slip[tau]);
+  }
+  orc_env_free(e);
+  return status;
+}

@@ -112,6 +112,9 @@ _SIG = {
     "bench_run": (C.c_int, [C.c_void_p, _P(EnvConfig), C.c_int, C.c_int, C.c_int, C.c_int,
                             C.c_uint64, C.c_int, C.c_int, _P(BenchRow)]),
     "random_stream": (None, [_P(StreamConfig), C.c_uint64, _P(Message)]),
+    "evaluate_matrix": (C.c_int, [C.c_void_p, _P(EnvConfig), _P(C.c_uint64), C.c_uint64,
+                                  _P(abi.Policy), C.c_int, _P(abi.Policy), C.c_int, C.c_uint64,
+                                  _P(abi.CellStats)]),
 }
 _REF_ONLY = {
     "naive_create": (C.c_void_p, []),
@@ -124,6 +127,8 @@ _ORC_ONLY = {
     "splitmix64": (C.c_uint64, [C.c_uint64]),
     "make_key": (C.c_uint64, [C.c_uint64, C.c_int, _P(C.c_uint64)]),
     "crng_draws": (None, [C.c_uint64, C.c_uint64, _P(C.c_uint64)]),
+    "choose_action": (C.c_int, [C.c_void_p, C.c_int, _P(abi.Policy), C.c_int, C.c_uint64,
+                                C.c_uint64, C.c_uint64, _P(AgentAction)]),
 }
 
 _cache: dict[str, "Oracle"] = {}
@@ -157,6 +162,16 @@ class Oracle:
     def check(self, rc: int) -> None:
         if rc != abi.MLOB_OK:
             raise _EXC.get(rc, OracleError)(self.last_error().decode())
+
+    def evaluate(self, store: "OStore", cfg: EnvConfig, episodes, type0, type1, seed: int):
+        """evaluate_matrix (evaluate.hpp:104-217) -> list of CellStats, row-major."""
+        eps = np.ascontiguousarray(episodes, dtype=np.uint64)
+        t0 = (abi.Policy * max(1, len(type0)))(*type0)
+        t1 = (abi.Policy * max(1, len(type1)))(*type1)
+        out = (abi.CellStats * max(1, len(type0) * len(type1)))()
+        self.check(self.evaluate_matrix(store.h, C.byref(cfg), eps.ctypes.data_as(_P(C.c_uint64)),
+                                        len(eps), t0, len(type0), t1, len(type1), seed, out))
+        return list(out)[:len(type0) * len(type1)]
 
     # ---- stores ----
     def synth(self, cfg: SynthConfig, seed: int) -> "OStore":
@@ -321,6 +336,13 @@ class OEnv:
     def step_ids(self, ids):
         arr = (C.c_int32 * max(1, len(ids)))(*ids)
         self.o.check(self.o.env_step_ids(self.h, arr, len(ids)))
+
+    def policy_action(self, a: int, pol, step: int, seed: int, cell: int, episode: int):
+        """choose_action (evaluate.hpp:56-99) for a scripted policy (orc only)."""
+        out = AgentAction()
+        self.o.check(self.o.choose_action(self.h, a, C.byref(pol), step, seed, cell, episode,
+                                          C.byref(out)))
+        return out
 
     def step(self, actions):
         arr = (AgentAction * max(1, len(actions)))(*actions)

@@ -89,7 +89,11 @@ typedef struct orc_bench_row {
   /* throughput harness (bench/bench.hpp run_throughput, one grid cell) */                     \
   int P##bench_run(void* store, const mlob_env_config* base, int n_envs, int n_steps,          \
                    int warmup, int workers, uint64_t seed, int messages_per_step,              \
-                   int agents_per_type, orc_bench_row* out);
+                   int agents_per_type, orc_bench_row* out);                                   \
+  /* cross-play grid (ippo/evaluate.hpp evaluate_matrix, scripted policies) */                \
+  int P##evaluate_matrix(void* store, const mlob_env_config* cfg, const uint64_t* episodes,   \
+                         uint64_t n_episodes, const mlob_policy* type0, int n0,               \
+                         const mlob_policy* type1, int n1, uint64_t seed, mlob_cell_stats* out);
 
 ORACLE_DECLARE(orc_)
 ORACLE_DECLARE(ref_)
@@ -109,6 +113,9 @@ uint64_t orc_splitmix64(uint64_t z);
 uint64_t orc_make_key(uint64_t seed, int n, const uint64_t* words);
 void orc_crng_draws(uint64_t key, uint64_t n, uint64_t* out);
 void orc_random_stream(const orc_stream_config* cfg, uint64_t seed, mlob_message* out);
+/* evaluate.hpp:56-99 choose_action (scripted kinds) on an orc env */
+int orc_choose_action(void* env, int agent, const mlob_policy* p, int step, uint64_t seed,
+                      uint64_t cell_id, uint64_t episode, mlob_agent_action* out);
 void ref_random_stream(const orc_stream_config* cfg, uint64_t seed, mlob_message* out);
 /* tests/reference/naive_book.hpp:16-134 (reference-side only) */
 void* ref_naive_create(void);

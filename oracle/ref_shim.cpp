@@ -18,6 +18,7 @@
 #include "marlob/data/store.hpp"
 #include "marlob/data/synth.hpp"
 #include "marlob/env/env.hpp"
+#include "marlob/ippo/evaluate.hpp"
 #include "marlob/ippo/rollout.hpp"
 #include "marlob/lob/book.hpp"
 #include "marlob/util/thread_pool.hpp"
@@ -458,6 +459,50 @@ int ref_bench_run(void* store, const mlob_env_config* base, int n_envs, int n_st
     out->steps_per_sec = r.steps_per_sec;
     out->messages_per_sec = r.messages_per_sec;
     out->worker_utilization = r.worker_utilization;
+  });
+}
+
+// ---- cross-play (ippo::evaluate_matrix, the reference's own driver) ----
+int ref_evaluate_matrix(void* store, const mlob_env_config* cfg, const uint64_t* episodes, uint64_t n_eps,
+                        const mlob_policy* t0, int n0, const mlob_policy* t1, int n1, uint64_t seed,
+                        mlob_cell_stats* out) {
+  return guarded([&] {
+    const auto to_choice = [](const mlob_policy& p) {
+      ippo::PolicyChoice c;
+      c.kind = static_cast<ippo::PolicyKind>(p.kind);
+      c.avst.params.gamma_grid.assign(p.gamma_grid, p.gamma_grid + p.n_gamma);
+      c.avst.params.kappa = p.kappa;
+      c.avst.params.sigma = p.sigma;
+      c.avst.params.horizon = p.horizon;
+      c.avst.gamma_index = p.avst_gamma_index;
+      c.twap_mode = static_cast<baselines::TwapPriceMode>(p.twap_mode);
+      return c;
+    };
+    std::vector<ippo::PolicyChoice> o0, o1;
+    for (int i = 0; i < n0; ++i) o0.push_back(to_choice(t0[i]));
+    for (int i = 0; i < n1; ++i) o1.push_back(to_choice(t1[i]));
+    const env::EnvConfig c = to_cfg(*cfg);
+    const data::MessageStore& st = static_cast<StoreH*>(store)->store;
+    const data::EpisodeIndex index =
+        data::build_episode_index(st, c.steps_per_episode, c.messages_per_step, c.start_stride_steps);
+    const std::vector<std::size_t> eps(episodes, episodes + n_eps);
+    const ippo::CrossPlayResult r = ippo::evaluate_matrix(st, index, c, eps, o0, o1, seed);
+    for (std::size_t i = 0; i < r.cells.size(); ++i) {
+      const ippo::CellStats& cs = r.cells[i];
+      std::memset(&out[i], 0, sizeof out[i]);
+      out[i].episodes = cs.episodes;
+      for (int t = 0; t < 2; ++t) {
+        const ippo::TypeCellStats& s = cs.per_type[t];
+        mlob_type_cell_stats& d = out[i].per_type[t];
+        d.pv_mean = s.pv_mean;
+        d.pv_stderr = s.pv_stderr;
+        d.slippage_mean = s.slippage_mean;
+        d.slippage_stderr = s.slippage_stderr;
+        d.completion_mean = s.completion_mean;
+        d.filled_total = s.filled_total;
+        d.no_fills = s.no_fills ? 1 : 0;
+      }
+    }
   });
 }
 

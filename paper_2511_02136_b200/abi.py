@@ -33,6 +33,9 @@ MAX_AGENTS = 32
 
 VENV_AUTO_RESET = 1 << 0
 VENV_RECORD_TRADES = 1 << 1
+# ippo::PolicyKind (evaluate.hpp:17), baselines::TwapPriceMode (twap.hpp:11)
+POLICY_LEARNED, POLICY_TWAP, POLICY_AVST, POLICY_RANDOM, POLICY_NOOP = range(5)
+TWAP_AGGRESSIVE, TWAP_PASSIVE = 0, 1
 
 
 class Message(C.Structure):
@@ -132,6 +135,38 @@ class SynthConfig(C.Structure):
                 ("p_delete", f64), ("p_execute", f64), ("band", i32), ("seed_levels", i32),
                 ("max_qty", i64), ("seed_qty", i64), ("state_sample_every", u64),
                 ("state_depth", u64)]
+
+
+class Policy(C.Structure):
+    """mlob_policy = ippo::PolicyChoice without the network (evaluate.hpp:19-25)."""
+    _fields_ = [("kind", i32), ("twap_mode", i32), ("avst_gamma_index", i32), ("n_gamma", i32),
+                ("gamma_grid", f64 * MAX_GAMMA), ("kappa", f64), ("sigma", f64), ("horizon", f64)]
+
+
+class TypeCellStats(C.Structure):  # evaluate.hpp:27-35
+    _fields_ = [("pv_mean", f64), ("pv_stderr", f64), ("slippage_mean", f64),
+                ("slippage_stderr", f64), ("completion_mean", f64), ("filled_total", i64),
+                ("no_fills", i32), ("_pad", i32)]
+
+
+class CellStats(C.Structure):  # evaluate.hpp:37-42 (labels omitted)
+    _fields_ = [("per_type", TypeCellStats * 2), ("episodes", i64)]
+
+
+def policy(kind: int, twap_mode: int = TWAP_AGGRESSIVE, gamma_index: int = 1,
+           gamma_grid=(0.05, 0.1, 0.5, 1.0), kappa: float = 1.5, sigma: float = 2.0,
+           horizon: float = 64.0) -> Policy:
+    """A policy option with the reference defaults (AvStBaseline avst.hpp:14-17 over
+    AvStParams actions.hpp:142-147; TwapPriceMode::Aggressive evaluate.hpp:24)."""
+    p = Policy()
+    p.kind, p.twap_mode, p.avst_gamma_index = kind, twap_mode, gamma_index
+    if len(gamma_grid) > MAX_GAMMA:
+        raise ValueError(f"at most {MAX_GAMMA} gamma values")
+    p.n_gamma = len(gamma_grid)
+    for i, g in enumerate(gamma_grid):
+        p.gamma_grid[i] = g
+    p.kappa, p.sigma, p.horizon = kappa, sigma, horizon
+    return p
 
 
 class StepIO(C.Structure):

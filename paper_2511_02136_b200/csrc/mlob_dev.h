@@ -106,7 +106,15 @@ struct ActiveRec {
   uint32_t qty_side;
 };
 
-enum ActionMode : int32_t { kActIds = 0, kActDirect = 1, kActBench = 2 };
+enum ActionMode : int32_t { kActIds = 0, kActDirect = 1, kActBench = 2, kActScripted = 3 };
+
+// A scripted policy (mlob_policy) resolved for the device: AvSt's gamma and
+// log1p term are taken on the host (glibc), as for the AvSt action space.
+struct DevPolicy {
+  int32_t kind, twap_mode;
+  double gamma, sigma, horizon, avst_term;
+};
+constexpr int kMaxPolicies = 64;
 
 enum DevError : uint32_t {
   kErrMissingState = 1u << 0,   // runtime_error, env.hpp:149-153
@@ -165,7 +173,10 @@ struct __align__(16) KParams {
   uint32_t* error;
   const DevCfg* cfg;  // device copy; staged into shared memory by each block
   const uint32_t* gate;  // optional: non-zero word = skip the launch (rejected actions)
-  uint64_t _pad_gate;
+  // kActScripted: policies[env_policy[env * n_specs + type]], Random keyed by env_cell[env]
+  const DevPolicy* policies;
+  const uint8_t* env_policy;
+  const uint64_t* env_cell;
 };
 
 }  // namespace mlob

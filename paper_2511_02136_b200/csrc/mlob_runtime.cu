@@ -113,6 +113,11 @@ struct mlob_venv {
   std::vector<cudaEvent_t> io_events;
   uint32_t* d_gate = nullptr;
   uint8_t* d_resets[MLOB_MAX_SPECS] = {};
+  // scripted policies (kActScripted)
+  DevPolicy* d_policies = nullptr;
+  uint8_t* d_env_policy = nullptr;
+  uint64_t* d_env_cell = nullptr;
+  bool has_cells = false;
   std::vector<uint64_t> starts;
   std::vector<EpState> ep_state;
   std::vector<uint64_t> pool;  // empty = identity
@@ -216,6 +221,9 @@ struct mlob_venv {
     k.reset_episodes = d_reset_eps;
     k.error = d_error;
     k.cfg = d_cfg;
+    k.policies = d_policies;
+    k.env_policy = d_env_policy;
+    k.env_cell = has_cells ? d_env_cell : nullptr;
     return k;
   }
 
@@ -881,6 +889,174 @@ mlob_status mlob_venv_dones(mlob_venv* v, uint8_t* out) {
 }
 mlob_status mlob_venv_infos(mlob_venv* v, mlob_agent_info* out) {
   return guarded([&] { d2h(v, out, v->d_infos, v->n_envs * v->A); });
+}
+
+// ---- scripted policies and cross-play evaluation ----------------------------
+
+void mlob_default_policy(int kind, mlob_policy* out) {
+  std::memset(out, 0, sizeof *out);
+  out->kind = kind;
+  out->twap_mode = MLOB_TWAP_AGGRESSIVE;
+  out->avst_gamma_index = 1;  // AvStBaseline, avst.hpp:14-17
+  const double grid[4] = {0.05, 0.1, 0.5, 1.0};  // AvStParams, actions.hpp:142-147
+  out->n_gamma = 4;
+  for (int i = 0; i < 4; ++i) out->gamma_grid[i] = grid[i];
+  out->kappa = 1.5;
+  out->sigma = 2.0;
+  out->horizon = 64.0;
+}
+
+static DevPolicy resolve_policy(const mlob_policy& p) {
+  if (p.kind < MLOB_POLICY_LEARNED || p.kind > MLOB_POLICY_NOOP)
+    fail(MLOB_E_INVALID_ARGUMENT, "policy: unknown kind " + std::to_string(p.kind));
+  if (p.kind == MLOB_POLICY_LEARNED)
+    fail(MLOB_E_INVALID_ARGUMENT, "policy: learned policies are not evaluated on the device");
+  if (p.kind == MLOB_POLICY_TWAP && p.twap_mode != MLOB_TWAP_AGGRESSIVE && p.twap_mode != MLOB_TWAP_PASSIVE)
+    fail(MLOB_E_INVALID_ARGUMENT, "policy: twap_mode");
+  DevPolicy d{};
+  d.kind = p.kind;
+  d.twap_mode = p.twap_mode;
+  if (p.kind == MLOB_POLICY_AVST) {
+    if (p.n_gamma < 0 || p.n_gamma > MLOB_MAX_GAMMA) fail(MLOB_E_INVALID_ARGUMENT, "policy: n_gamma");
+    if (p.avst_gamma_index < 0 || p.avst_gamma_index >= p.n_gamma)  // avst.hpp:21-23
+      fail(MLOB_E_OUT_OF_RANGE, "avst_policy: gamma_index out of range");
+    const double g = p.gamma_grid[p.avst_gamma_index];
+    d.gamma = g;
+    d.sigma = p.sigma;
+    d.horizon = p.horizon;
+    d.avst_term = (2.0 / g) * std::log1p(g / p.kappa);  // actions.hpp:158, host libm
+  }
+  return d;
+}
+
+static void set_policies(mlob_venv* v, const mlob_policy* policies, int n_policies, const uint8_t* env_policy,
+                         const uint64_t* env_cell) {
+  if (n_policies < 1 || n_policies > kMaxPolicies)
+    fail(MLOB_E_INVALID_ARGUMENT, "set_policies: 1.." + std::to_string(kMaxPolicies) + " policies");
+  std::vector<DevPolicy> dp(n_policies);
+  for (int i = 0; i < n_policies; ++i) dp[i] = resolve_policy(policies[i]);
+  const uint64_t n = v->n_envs * static_cast<uint64_t>(v->cfg.n_specs);
+  for (uint64_t i = 0; i < n; ++i)
+    if (env_policy[i] >= n_policies) fail(MLOB_E_OUT_OF_RANGE, "set_policies: policy index out of range");
+  v->set_device();
+  if (!v->d_policies) {
+    v->d_policies = v->alloc<DevPolicy>(kMaxPolicies, "policies");
+    v->d_env_policy = v->alloc<uint8_t>(n > 0 ? n : 1, "env_policy");
+    v->d_env_cell = v->alloc<uint64_t>(v->n_envs, "env_cell");
+  }
+  cuda_check(cudaMemcpyAsync(v->d_policies, dp.data(), dp.size() * sizeof(DevPolicy), cudaMemcpyHostToDevice,
+                             v->stream), "H2D");
+  cuda_check(cudaMemcpyAsync(v->d_env_policy, env_policy, n, cudaMemcpyHostToDevice, v->stream), "H2D");
+  v->has_cells = env_cell != nullptr;
+  if (env_cell)
+    cuda_check(cudaMemcpyAsync(v->d_env_cell, env_cell, v->n_envs * 8, cudaMemcpyHostToDevice, v->stream), "H2D");
+  cuda_check(cudaStreamSynchronize(v->stream), "sync");  // host arrays may be temporaries
+  v->action_mode = kActScripted;
+}
+
+mlob_status mlob_venv_set_policies(mlob_venv* v, const mlob_policy* policies, int n_policies,
+                                   const uint8_t* env_policy, const uint64_t* env_cell) {
+  return guarded([&] { set_policies(v, policies, n_policies, env_policy, env_cell); });
+}
+
+mlob_status mlob_evaluate_matrix(const mlob_store* store, const mlob_env_config* cfg, const uint64_t* episodes,
+                                 uint64_t n_episodes, const mlob_policy* type0, int n_type0,
+                                 const mlob_policy* type1, int n_type1, uint64_t seed, int device,
+                                 mlob_cell_stats* out) {
+  return guarded([&] {
+    if (cfg->n_specs != 2) fail(MLOB_E_INVALID_ARGUMENT, "evaluate_matrix: exactly two agent types required");
+    if (n_episodes == 0) fail(MLOB_E_INVALID_ARGUMENT, "evaluate_matrix: empty episode set");
+    for (int i = 0; i < n_type0 + n_type1; ++i)
+      if ((i < n_type0 ? type0[i] : type1[i - n_type0]).kind == MLOB_POLICY_LEARNED)
+        fail(MLOB_E_INVALID_ARGUMENT, "evaluate_matrix: learned policy without a network");
+    if (n_type0 <= 0 || n_type1 <= 0) return;
+    if (n_type0 + n_type1 > kMaxPolicies)
+      fail(MLOB_E_INVALID_ARGUMENT, "evaluate_matrix: at most " + std::to_string(kMaxPolicies) + " options");
+    std::vector<mlob_policy> table(type0, type0 + n_type0);
+    table.insert(table.end(), type1, type1 + n_type1);
+    for (const auto& p : table) resolve_policy(p);  // argument errors before any work
+    // one env per (row, col, episode), cell-major; every env is the reference's
+    // MarketEnv(seed, env index 0) (evaluate.hpp:128)
+    const uint64_t cells = static_cast<uint64_t>(n_type0) * n_type1, n = cells * n_episodes;
+    std::vector<uint64_t> zeros(n, 0), eps(n), cell(n);
+    std::vector<uint8_t> pol(n * 2);
+    for (uint64_t e = 0; e < n; ++e) {
+      const uint64_t c = e / n_episodes, row = c / n_type1, col = c % n_type1;
+      eps[e] = episodes[e % n_episodes];
+      cell[e] = row * 1000 + col;  // evaluate.hpp:139
+      pol[e * 2] = static_cast<uint8_t>(row);
+      pol[e * 2 + 1] = static_cast<uint8_t>(n_type0 + col);
+    }
+    mlob_venv_desc d{};
+    d.store = store;
+    d.cfg = *cfg;
+    d.seed = seed;
+    d.n_envs_global = d.n_envs_local = n;
+    d.env_indices = zeros.data();
+    d.device = device;
+    mlob_venv* raw = nullptr;
+    const mlob_status st = mlob_venv_create(&d, &raw);
+    if (st != MLOB_OK) fail(st, mlob_last_error());
+    std::unique_ptr<mlob_venv> v(raw);
+    do_reset(v.get(), eps);
+    set_policies(v.get(), table.data(), static_cast<int>(table.size()), pol.data(), cell.data());
+    for (int t = 0; t < cfg->steps_per_episode; ++t) do_step(v.get(), kActScripted, 0, 0);
+    const int A = v->A;
+    std::vector<mlob_agent_info> info(n * A);
+    std::vector<AgentRec> ag(n * A);
+    d2h(v.get(), info.data(), v->d_infos, n * A);
+    d2h(v.get(), ag.data(), v->d_agents, n * A);
+    // per-cell statistics in the reference's order (evaluate.hpp:171-213)
+    const auto mean_stderr = [](const std::vector<double>& xs, double& mean, double& se) {
+      const double k = static_cast<double>(xs.size());
+      mean = 0.0;
+      for (const double x : xs) mean += x;
+      mean /= k;
+      double var = 0.0;
+      for (const double x : xs) var += (x - mean) * (x - mean);
+      se = xs.size() > 1 ? std::sqrt(var / (k - 1.0) / k) : 0.0;
+    };
+    for (uint64_t c = 0; c < cells; ++c) {
+      std::vector<double> pv[2], slip[2];
+      double completion_sum[2] = {0.0, 0.0};
+      int64_t filled[2] = {0, 0};
+      for (uint64_t k = 0; k < n_episodes; ++k) {
+        const uint64_t e = c * n_episodes + k;
+        double ep_pv[2] = {0.0, 0.0}, ep_slip[2] = {0.0, 0.0};
+        int type_agents[2] = {0, 0};
+        for (int a = 0; a < A; ++a) {
+          const int tau = v->dcfg.flat_spec[a];
+          const mlob_agent_info& inf = info[e * A + a];
+          ep_pv[tau] += inf.portfolio_value;
+          ep_slip[tau] += inf.slippage_total;
+          ++type_agents[tau];
+          filled[tau] += ag[e * A + a].filled_total;
+          const mlob_agent_spec& sp = cfg->specs[tau];
+          if (sp.type == MLOB_EXECUTOR)
+            completion_sum[tau] +=
+                1.0 - static_cast<double>(inf.task_remaining) / static_cast<double>(sp.params.task_size);
+          else
+            completion_sum[tau] += 0.0;
+        }
+        for (int tau = 0; tau < 2; ++tau) {
+          pv[tau].push_back(ep_pv[tau] / type_agents[tau]);
+          slip[tau].push_back(ep_slip[tau] / type_agents[tau]);
+        }
+      }
+      mlob_cell_stats& cs = out[c];
+      std::memset(&cs, 0, sizeof cs);
+      cs.episodes = static_cast<int64_t>(n_episodes);
+      for (int tau = 0; tau < 2; ++tau) {
+        mlob_type_cell_stats& t = cs.per_type[tau];
+        mean_stderr(pv[tau], t.pv_mean, t.pv_stderr);
+        t.filled_total = filled[tau];
+        t.no_fills = filled[tau] == 0;
+        if (!t.no_fills) mean_stderr(slip[tau], t.slippage_mean, t.slippage_stderr);
+        t.completion_mean = completion_sum[tau] / (static_cast<double>(n_episodes) *
+                                                   static_cast<double>(cfg->specs[tau].count));
+      }
+    }
+  });
 }
 
 // ---- fused env I/O: chunked step with overlapped transfers -----------------

@@ -76,7 +76,7 @@ struct Rng {
   }
   __device__ __forceinline__ bool coin() { return (next() & 1ull) != 0; }
 };
-enum : uint64_t { kRngShuffle = 1, kRngTaskDir = 2, kRngBenchAction = 7 };
+enum : uint64_t { kRngShuffle = 1, kRngTaskDir = 2, kRngBenchAction = 7, kRngEpisodeDraw = 8 };
 
 // ---------------------------------------------------------------------------
 // Book side held in registers: SPL rows of 32 slots (lane-major).
@@ -959,16 +959,42 @@ struct WarpEnv {
       q.push(MLOB_ASK, (ah + 1) / 2, sp.order_size);
       q.finish_two_sided();
     } else {  // AvSt, actions.hpp:151-178
-      const double gamma = sp.gamma[id];
-      const double rem = sp.horizon - static_cast<double>(step);
-      const double ttg = 0.0 < rem ? rem : 0.0;
-      const double mid_ticks = static_cast<double>(mid_half) / 2.0;
-      const double reservation =
-          mid_ticks - static_cast<double>(st.inventory) * gamma * sp.sigma * sp.sigma * ttg;
-      const double half_spread = 0.5 * (gamma * sp.sigma * sp.sigma * ttg + sp.avst_term[id]);
-      q.push(MLOB_BID, static_cast<int64_t>(floor(reservation - half_spread)), sp.order_size);
-      q.push(MLOB_ASK, static_cast<int64_t>(ceil(reservation + half_spread)), sp.order_size);
-      q.finish_two_sided();
+      avst(sp.gamma[id], sp.sigma, sp.horizon, sp.avst_term[id], st.inventory, sp.order_size, q);
+    }
+  }
+
+  // decode_avst (actions.hpp:164-178) over avst_quotes (actions.hpp:151-162);
+  // avst_term = (2/gamma) log1p(gamma/kappa), evaluated on the host
+  __device__ __forceinline__ void avst(double gamma, double sigma, double horizon, double avst_term,
+                                       int64_t inventory, int64_t order_size, Quotes& q) const {
+    const double rem = horizon - static_cast<double>(step);
+    const double ttg = 0.0 < rem ? rem : 0.0;
+    const double mid_ticks = static_cast<double>(mid_half) / 2.0;
+    const double reservation = mid_ticks - static_cast<double>(inventory) * gamma * sigma * sigma * ttg;
+    const double half_spread = 0.5 * (gamma * sigma * sigma * ttg + avst_term);
+    q.push(MLOB_BID, static_cast<int64_t>(floor(reservation - half_spread)), order_size);
+    q.push(MLOB_ASK, static_cast<int64_t>(ceil(reservation + half_spread)), order_size);
+    q.finish_two_sided();
+  }
+
+  // Scripted direct actions (evaluate.hpp:63-73): NoOp, twap_policy
+  // (twap.hpp:37-58, plan = make_twap_plan over steps_per_episode, twap.hpp:21-33),
+  // avst_policy (avst.hpp:19-32).
+  __device__ __forceinline__ void scripted(int a, const DevPolicy& pol, Quotes& q) {
+    const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
+    const AgentRec& st = sm.ag[a];
+    if (pol.kind == MLOB_POLICY_TWAP) {
+      const int64_t S = cfg.steps_per_episode, T = sp.task_size, s = step;
+      const int64_t sched = ((s + 1) * T) / S - (s * T) / S;
+      const int64_t qty = s + 1 == S ? st.task_remaining : min(sched, st.task_remaining);
+      if (qty <= 0) return;
+      int64_t bb, ba;
+      effective_tops(sp, bb, ba);
+      const bool buy = st.task_dir == MLOB_TASK_BUY;
+      const int64_t price = pol.twap_mode == MLOB_TWAP_AGGRESSIVE ? (buy ? ba : bb) : (buy ? bb : ba);
+      q.push(buy ? MLOB_BID : MLOB_ASK, price, qty);
+    } else if (pol.kind == MLOB_POLICY_AVST) {
+      avst(pol.gamma, pol.sigma, pol.horizon, pol.avst_term, st.inventory, sp.order_size, q);
     }
   }
 
@@ -998,15 +1024,23 @@ struct WarpEnv {
     q.n = 0;
     q.s0 = q.s1 = 0;
     q.p0 = q.p1 = q.q0 = q.q1 = 0;
-    if (kp.action_mode == kActDirect && kp.action_direct[env * cfg.n_agents + a].direct) {
-      const mlob_agent_action& da = kp.action_direct[env * cfg.n_agents + a];
-      q.n = da.n_quotes;
-      q.s0 = da.quotes[0].side;
-      q.p0 = da.quotes[0].price;
-      q.q0 = da.quotes[0].quantity;
-      q.s1 = da.quotes[1].side;
-      q.p1 = da.quotes[1].price;
-      q.q1 = da.quotes[1].quantity;
+    const DevPolicy* pol =
+        kp.action_mode == kActScripted ? &kp.policies[kp.env_policy[env * cfg.n_specs + cfg.flat_spec[a]]] : nullptr;
+    const bool direct = pol ? pol->kind != MLOB_POLICY_RANDOM
+                            : kp.action_mode == kActDirect && kp.action_direct[env * cfg.n_agents + a].direct;
+    if (direct) {  // env.hpp:290-298
+      if (pol) {
+        scripted(a, *pol, q);
+      } else {
+        const mlob_agent_action& da = kp.action_direct[env * cfg.n_agents + a];
+        q.n = da.n_quotes;
+        q.s0 = da.quotes[0].side;
+        q.p0 = da.quotes[0].price;
+        q.q0 = da.quotes[0].quantity;
+        q.s1 = da.quotes[1].side;
+        q.p1 = da.quotes[1].price;
+        q.q1 = da.quotes[1].quantity;
+      }
       if (sp.type == MLOB_EXECUTOR) {
         if (q.n >= 1 && q.q0 > st.task_remaining) q.q0 = st.task_remaining;
         if (q.n >= 2 && q.q1 > st.task_remaining) q.q1 = st.task_remaining;
@@ -1018,6 +1052,11 @@ struct WarpEnv {
         Rng r{key_fold(key_fold(key_fold(splitmix64(kp.bench_seed), kRngBenchAction), genv),
                        kp.global_step)};
         for (int b = 0; b < a; ++b) r.next();
+        id = static_cast<int>(r.below(static_cast<uint64_t>(sp.arity)));
+      } else if (pol) {  // PolicyKind::Random, evaluate.hpp:74-79
+        uint64_t h = key_fold(key_fold(splitmix64(seed), kRngEpisodeDraw), kp.env_cell ? kp.env_cell[env] : 0);
+        h = key_fold(key_fold(key_fold(h, episode), static_cast<uint64_t>(step)), static_cast<uint64_t>(a));
+        Rng r{h};
         id = static_cast<int>(r.below(static_cast<uint64_t>(sp.arity)));
       } else if (kp.action_mode == kActDirect) {
         id = kp.action_direct[env * cfg.n_agents + a].id;

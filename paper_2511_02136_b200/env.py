@@ -90,6 +90,11 @@ _SIGS = {
     "mlob_venv_dones_device": (_vp, [_vp]),
     "mlob_venv_infos": (C.c_int, [_vp, _vp]),
     "mlob_venv_step_io": (C.c_int, [_vp, _P(abi.StepIO)]),
+    "mlob_default_policy": (None, [C.c_int, _P(abi.Policy)]),
+    "mlob_venv_set_policies": (C.c_int, [_vp, _P(abi.Policy), C.c_int, _vp, _vp]),
+    "mlob_evaluate_matrix": (C.c_int, [_vp, _P(EnvConfig), _P(C.c_uint64), C.c_uint64,
+                                       _P(abi.Policy), C.c_int, _P(abi.Policy), C.c_int,
+                                       C.c_uint64, C.c_int, _P(abi.CellStats)]),
     "mlob_venv_env_obs": (C.c_int, [_vp, C.c_uint64, _P(C.c_double), C.c_uint64]),
     "mlob_venv_episode_stats": (C.c_int, [_vp, C.c_int, _P(EpisodeStats)]),
     "mlob_venv_episode_stats_device": (C.c_int, [_vp, _vp]),
@@ -367,6 +372,17 @@ class _Venv:
     def synchronize(self) -> None:
         _check(lib().mlob_venv_synchronize(self.h))
 
+    def set_policies(self, policies, env_policy, env_cell=None) -> None:
+        """Scripted actions (mlob_venv_set_policies): env e's type-t agents act by
+        policies[env_policy[e, t]]; Random draws are keyed by env_cell[e]."""
+        pol = (abi.Policy * max(1, len(policies)))(*policies)
+        ep = np.ascontiguousarray(env_policy, dtype=np.uint8).reshape(-1)
+        if ep.size != self.n_envs * self.n_types():
+            raise ValueError(f"env_policy: expected {self.n_envs} x {self.n_types()} entries")
+        cell = None if env_cell is None else np.ascontiguousarray(env_cell, dtype=np.uint64)
+        _check(lib().mlob_venv_set_policies(self.h, pol, len(policies), _vp(ep.ctypes.data),
+                                            None if cell is None else _vp(cell.ctypes.data)))
+
     def step_io(self, actions=None, rewards=None, dones=None, infos=None, obs=None, resets=None) -> None:
         """Fused set_actions + step + rewards/dones/infos + per-type gather
         (mlob_venv_step_io).  Buffers are C-contiguous host numpy arrays or
@@ -432,6 +448,20 @@ class _Venv:
 
     def view(self, e: int) -> "EnvView":
         return EnvView(self, e)
+
+
+def evaluate_matrix(store: "DeviceStore", cfg: EnvConfig, episodes, type0, type1, seed: int,
+                    device: int = 0):
+    """ippo::evaluate_matrix (evaluate.hpp:104-217) on the GPU: the whole
+    cross-play grid as one batch (mlob_evaluate_matrix).  type0 / type1 are
+    lists of abi.Policy; returns the CellStats list, row-major."""
+    eps = np.ascontiguousarray(episodes, dtype=np.uint64)
+    t0 = (abi.Policy * max(1, len(type0)))(*type0)
+    t1 = (abi.Policy * max(1, len(type1)))(*type1)
+    out = (abi.CellStats * max(1, len(type0) * len(type1)))()
+    _check(lib().mlob_evaluate_matrix(store.h, C.byref(cfg), eps.ctypes.data_as(_P(C.c_uint64)),
+                                      len(eps), t0, len(type0), t1, len(type1), seed, device, out))
+    return list(out)[:len(type0) * len(type1)]
 
 
 class MarketVecEnv(_Venv):

@@ -107,3 +107,19 @@ def state_dict(s: abi.AgentState):
     d = struct_dict(s)
     d["active"] = [struct_dict(s.active[i]) for i in range(min(s.n_active, abi.MAX_ACTIVE))]
     return d
+
+
+def crossplay_case():
+    """A two-type cross-play grid over every scripted policy kind
+    (evaluate.hpp:17): MM (AvSt space) vs Executor, 3 episodes."""
+    A = abi
+    cfg = A.env_config([A.agent_spec(A.MARKET_MAKER, count=2, mm_space=A.AVST),
+                        A.agent_spec(A.EXECUTOR, task_size=120, order_size=4)],
+                       steps_per_episode=12, messages_per_step=25, start_stride_steps=12)
+    synth_kw = {"state_sample_every": 25 * 12, "n_messages": 20000}
+    type0 = [A.policy(A.POLICY_NOOP), A.policy(A.POLICY_AVST),
+             A.policy(A.POLICY_AVST, gamma_index=3, kappa=2.5, sigma=1.0, horizon=12.0),
+             A.policy(A.POLICY_RANDOM), A.policy(A.POLICY_TWAP)]
+    type1 = [A.policy(A.POLICY_TWAP), A.policy(A.POLICY_TWAP, twap_mode=A.TWAP_PASSIVE),
+             A.policy(A.POLICY_RANDOM), A.policy(A.POLICY_NOOP), A.policy(A.POLICY_AVST)]
+    return cfg, synth_kw, [2, 0, 5], type0, type1

@@ -315,3 +315,45 @@ def test_step_io_matches_separate_calls(monkeypatch, chunks):
             assert b.view(e).book(1).tobytes() == a.view(e).book(1).tobytes()
     for t in range(T):
         assert bytes(a.episode_stats(t)) == bytes(b.episode_stats(t))
+
+
+def test_evaluate_matrix_matches_oracle(orc):
+    """Cross-play grid on the GPU (one env per cell x episode, policies
+    evaluated in the step kernel) against the oracle's evaluate_matrix."""
+    from paper_2511_02136_b200.env import evaluate_matrix
+    from tests.common import crossplay_case
+    cfg, synth_kw, eps, t0, t1 = crossplay_case()
+    got = evaluate_matrix(dev_store(synth_kw), cfg, eps, t0, t1, 7)
+    want = orc.evaluate(small_store(orc, synth_kw), cfg, eps, t0, t1, 7)
+    assert [bytes(x) for x in got] == [bytes(x) for x in want]
+    with pytest.raises(ValueError):
+        evaluate_matrix(dev_store(synth_kw), cfg, eps, [abi.policy(abi.POLICY_LEARNED)], t1, 7)
+    with pytest.raises(IndexError):
+        evaluate_matrix(dev_store(synth_kw), cfg, eps, [abi.policy(abi.POLICY_AVST, gamma_index=9)],
+                        t1, 7)
+
+
+def test_scripted_policies_per_step(orc):
+    """set_policies: every env-step of scripted agents equals the oracle env
+    driven by the same policies (twap.hpp:37-58, avst.hpp:19-32, evaluate.hpp:74-79)."""
+    from oracle.oracle import OEnv
+    from tests.common import crossplay_case
+    cfg, synth_kw, eps, t0, t1 = crossplay_case()
+    dev, ost = dev_store(synth_kw), small_store(orc, synth_kw)
+    pols = t0 + t1
+    n = len(t0) * len(t1)
+    env_policy = np.array([[i // len(t1), len(t0) + i % len(t1)] for i in range(n)], dtype=np.uint8)
+    cells = np.array([(i // len(t1)) * 1000 + i % len(t1) for i in range(n)], dtype=np.uint64)
+    b = MarketEnvBatch(dev, cfg, n_envs=n, seed=7, env_indices=np.zeros(n))
+    b.reset([eps[i % len(eps)] for i in range(n)])
+    b.set_policies(pols, env_policy, cells)
+    refs = [OEnv(orc, ost, cfg, 7, 0) for _ in range(n)]
+    for i, r in enumerate(refs):
+        r.reset(eps[i % len(eps)])
+    for t in range(cfg.steps_per_episode):
+        b.step()
+        for i, r in enumerate(refs):
+            acts = [r.policy_action(a, pols[env_policy[i, r.flat[a]]], t, 7, int(cells[i]),
+                                    eps[i % len(eps)]) for a in range(len(r.flat))]
+            r.step(acts)
+            compare_env_state(b.view(i), r)

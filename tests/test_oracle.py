@@ -280,3 +280,33 @@ def test_bench_harness_counts(orc, ref):
     b = bench_run(ref, sr, cfg, 8, 32, 2, 2, 0, 20, 1)
     assert a.env_steps == b.env_steps == 8 * 32
     assert a.messages == b.messages > 8 * 32 * 20
+
+
+def test_evaluate_matrix_matches_reference(orc, ref):
+    """Scripted cross-play (evaluate.hpp:104-217, twap.hpp, avst.hpp): the C
+    restatement against the reference's own evaluate_matrix, bit for bit."""
+    from tests.common import crossplay_case
+    cfg, synth_kw, eps, t0, t1 = crossplay_case()
+    a = orc.evaluate(small_store(orc, synth_kw), cfg, eps, t0, t1, 7)
+    b = ref.evaluate(small_store(ref, synth_kw), cfg, eps, t0, t1, 7)
+    assert len(a) == len(t0) * len(t1)
+    assert [bytes(x) for x in a] == [bytes(x) for x in b]
+    assert any(c.per_type[1].completion_mean > 0 for c in a)      # TWAP executes
+    assert any(c.per_type[0].filled_total > 0 for c in a)         # AvSt quotes fill
+
+
+def test_evaluate_matrix_errors(orc, ref):
+    from tests.common import crossplay_case
+    cfg, synth_kw, eps, t0, t1 = crossplay_case()
+    for o in (orc, ref):
+        st = small_store(o, synth_kw)
+        with pytest.raises(ValueError):   # evaluate.hpp:112 (empty episodes)
+            o.evaluate(st, cfg, [], t0, t1, 0)
+        with pytest.raises(ValueError):   # evaluate.hpp:114-117 (learned without a net)
+            o.evaluate(st, cfg, eps, [abi.policy(abi.POLICY_LEARNED)], t1, 0)
+        with pytest.raises(IndexError):   # avst.hpp:21-23
+            o.evaluate(st, cfg, eps, [abi.policy(abi.POLICY_AVST, gamma_index=4)], t1, 0)
+        one = abi.env_config([abi.agent_spec(abi.EXECUTOR)], steps_per_episode=12,
+                             messages_per_step=25, start_stride_steps=12)
+        with pytest.raises(ValueError):   # evaluate.hpp:110-111 (two types)
+            o.evaluate(st, one, eps, t0, t1, 0)
