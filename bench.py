@@ -252,24 +252,26 @@ def gpu_arm(args) -> None:
     A = venv.n_agents
     rng = np.random.default_rng(1234)
     ar = np.array([abi.action_arity(cfg.specs[s]) for s in abi.flat_specs(cfg)])
-    acts = torch.from_numpy((rng.integers(0, 1 << 30, size=(n_local, A)) % ar).astype(np.int32))
-    acts = acts.pin_memory()
+    e_steps = max(3, min(args.steps, args.e2e_steps))
+    # a fresh random action batch per step (pre-drawn, page-locked; not timed)
+    acts_all = [torch.from_numpy((rng.integers(0, 1 << 30, size=(n_local, A)) % ar).astype(np.int32))
+                .pin_memory() for _ in range(e_steps + 1)]
+    acts = acts_all[0]
     obs_bufs = [torch.empty((venv.n_streams(t), venv.obs_dim(t)), dtype=torch.float64).pin_memory()
                 for t in range(cfg.n_specs)]
     rew = torch.empty((n_local, A), dtype=torch.float64).pin_memory()
     dn = torch.empty((n_local, A), dtype=torch.uint8).pin_memory()
     rsb = [torch.empty(venv.n_streams(t), dtype=torch.uint8).pin_memory() for t in range(cfg.n_specs)]
-    e_steps = max(3, min(args.steps, args.e2e_steps))
 
-    def e2e_step():
-        venv.step_io(actions=acts, rewards=rew, dones=dn, obs=obs_bufs, resets=rsb)
+    def e2e_step(a):
+        venv.step_io(actions=a, rewards=rew, dones=dn, obs=obs_bufs, resets=rsb)
 
-    e2e_step()  # warm-up (creates the copy streams)
+    e2e_step(acts_all[e_steps])  # warm-up (creates the copy streams)
     em0 = venv.messages_processed()
     barrier()
     w0 = time.perf_counter()
-    for _ in range(e_steps):
-        e2e_step()
+    for i in range(e_steps):
+        e2e_step(acts_all[i])
     torch.cuda.synchronize()
     e_wall = torch.tensor([time.perf_counter() - w0], dtype=torch.float64, device="cuda")
     allreduce(e_wall, dist.ReduceOp.MAX)
