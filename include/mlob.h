@@ -414,6 +414,60 @@ typedef struct mlob_step_io {
 } mlob_step_io;
 mlob_status mlob_venv_step_io(mlob_venv* v, const mlob_step_io* io);
 
+/* ---- On-device policy inference and rollouts (ippo/net.hpp, rollout.hpp) -- */
+
+/* ippo::PolicyNet (net.hpp:18-30): host arrays in the reference's layout,
+ * gate order [reset, update, candidate]. */
+typedef struct mlob_policy_net {
+  int32_t obs_dim;
+  int32_t hidden;
+  int32_t n_actions;
+  int32_t _pad;
+  const double* w_ih;     /* (3H, obs_dim) */
+  const double* w_hh;     /* (3H, H) */
+  const double* b_ih;     /* 3H */
+  const double* b_hh;     /* 3H */
+  const double* w_actor;  /* (n_actions, H) */
+  const double* b_actor;  /* n_actions */
+  const double* w_critic; /* H */
+  double b_critic;
+} mlob_policy_net;
+
+/* One network per agent type (obs_dim / n_actions must match the type's;
+ * hidden <= 512, net.hpp:86-87).  Uploads the weights and zeroes the
+ * per-stream hidden states, as train_loop does before its first rollout
+ * (rollout.hpp:132-135).  Re-uploading weights keeps the hidden states when
+ * the shapes are unchanged (the learner's update between rollouts). */
+mlob_status mlob_venv_set_nets(mlob_venv* v, const mlob_policy_net* nets);
+
+/* TrainLoopConfig fields used by collect_rollout (rollout.hpp:30-37). */
+typedef struct mlob_rollout_config {
+  int32_t rollout_len;
+  int32_t _pad;
+  double discount;
+  double gae_lambda;
+  uint64_t seed;
+} mlob_rollout_config;
+
+/* collect_rollout (rollout.hpp:41-124) on the device: per step, for each type
+ * the GRU forward of every stream (net.hpp:120-188) and the categorical draw
+ * keyed (seed, ActionSample, type, update_index, t, stream) (ppo.hpp:80-98),
+ * then the env step with auto-reset; after T steps the bootstrap values and
+ * GAE (gae.hpp:14-32).  The rollout batch (ppo.hpp:33-48) stays in HBM; read
+ * it with mlob_venv_rollout_read / _device.  Hidden states persist across
+ * calls.  Needs MLOB_VENV_AUTO_RESET, set_nets and a reset. */
+mlob_status mlob_venv_collect_rollout(mlob_venv* v, const mlob_rollout_config* cfg, uint64_t update_index);
+
+/* RolloutBatch fields (ppo.hpp:33-48), time-major; HIDDEN = the persistent
+ * hidden state after the rollout, (B, H). */
+enum { MLOB_RB_OBS = 0, MLOB_RB_ACTIONS = 1, MLOB_RB_LOG_PROBS = 2, MLOB_RB_VALUES = 3,
+       MLOB_RB_REWARDS = 4, MLOB_RB_DONES = 5, MLOB_RB_RESETS = 6, MLOB_RB_H0 = 7,
+       MLOB_RB_ADVANTAGES = 8, MLOB_RB_RETURNS = 9, MLOB_RB_HIDDEN = 10 };
+/* Copies one field of type `type`'s batch to host memory (cap_bytes checked). */
+mlob_status mlob_venv_rollout_read(mlob_venv* v, int type, int field, void* out, uint64_t cap_bytes);
+/* Device pointer of the same field (NULL before the first rollout). */
+const void* mlob_venv_rollout_device(const mlob_venv* v, int type, int field);
+
 /* ---- Scripted policies and cross-play evaluation (ippo/evaluate.hpp) ------ */
 
 /* ippo::PolicyKind (evaluate.hpp:17); Learned is not available on the device. */

@@ -1322,7 +1322,9 @@ typedef struct venv {
   uint8_t* dones;
   int64_t* episodes_finished;
   double *t_pv, *t_slip, *t_comp, *t_inv;
+  struct rollout_state* roll; /* collect_rollout state (below) */
 } venv;
+static void rollout_free(struct rollout_state* r);
 
 void* orc_venv_create(void* st, const mlob_env_config* cfg, const uint64_t* pool,
                       uint64_t pool_len, uint64_t seed, int n_envs, int workers, int* status) {
@@ -1486,6 +1488,7 @@ void* orc_venv_instance(void* v, uint64_t e) { return ((venv*)v)->envs[e]; }
 void orc_venv_free(void* v_) {
   venv* v = v_;
   if (!v) return;
+  rollout_free(v->roll);
   for (int e = 0; e < v->n_envs; ++e) orc_env_free(v->envs[e]);
   free(v->envs);
   free(v->pool);
@@ -1794,4 +1797,255 @@ int orc_evaluate_matrix(void* store_, const mlob_env_config* cfg, const uint64_t
   }
   orc_env_free(e);
   return status;
+}
+
+/* ------------------------------------------------------------------------ */
+/* ippo/net.hpp PolicyNet, ppo.hpp sample_categorical, gae.hpp, rollout.hpp   */
+/* collect_rollout                                                           */
+
+int orc_make_policy_net(int D, int H, int A, uint64_t seed, double* out) { /* net.hpp:80-104 */
+  if (D < 1 || H < 1 || A < 1) return fail(MLOB_E_INVALID_ARGUMENT, "make_policy_net: dimensions must be >= 1");
+  if (H > 512) return fail(MLOB_E_INVALID_ARGUMENT, "make_policy_net: hidden size capped at 512");
+  const uint64_t w[4] = {5 /* ParamInit */, (uint64_t)D, (uint64_t)H, (uint64_t)A};
+  crng r = {make_key(seed, 4, w)};
+  double* p = out;
+#define INIT(n, fan_in, fan_out)                                        \
+  do {                                                                  \
+    const double bound = sqrt(6.0 / (double)((fan_in) + (fan_out)));    \
+    for (size_t i_ = 0; i_ < (size_t)(n); ++i_)                         \
+      p[i_] = -bound + (bound - -bound) * crng_uniform(&r);             \
+  } while (0)
+  INIT(3 * H * D, D, H); /* w_ih */
+  p += 3 * H * D;
+  INIT(3 * H * H, H, H); /* w_hh */
+  p += 3 * H * H;
+  for (int i = 0; i < 6 * H; ++i) *p++ = 0.0; /* b_ih, b_hh */
+  INIT(A * H, H, A); /* w_actor, then scaled (net.hpp:97-98) */
+  for (int i = 0; i < A * H; ++i) p[i] *= 0.01;
+  p += A * H;
+  for (int i = 0; i < A; ++i) *p++ = 0.0; /* b_actor */
+  INIT(H, H, 1); /* w_critic */
+  p += H;
+  *p = 0.0; /* b_critic */
+#undef INIT
+  return MLOB_OK;
+}
+
+static double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); } /* net.hpp:107 */
+
+/* policy_forward (net.hpp:120-188) without the backward cache */
+static void policy_forward(const mlob_policy_net* net, const double* obs, const double* hidden,
+                           const uint8_t* reset_mask, uint64_t batch, double* logits, double* values,
+                           double* hidden_out) {
+  const uint64_t H = (uint64_t)net->hidden, D = (uint64_t)net->obs_dim, A = (uint64_t)net->n_actions;
+  for (uint64_t b = 0; b < batch; ++b) {
+    const double* x = obs + b * D;
+    const double* h_prev = hidden + b * H;
+    const int reset = reset_mask[b] != 0;
+    for (uint64_t i = 0; i < H; ++i) {
+      double acc_r = net->b_ih[i] + net->b_hh[i];
+      double acc_z = net->b_ih[H + i] + net->b_hh[H + i];
+      double acc_n = net->b_ih[2 * H + i];
+      double acc_hn = net->b_hh[2 * H + i];
+      for (uint64_t d = 0; d < D; ++d) {
+        acc_r += net->w_ih[i * D + d] * x[d];
+        acc_z += net->w_ih[(H + i) * D + d] * x[d];
+        acc_n += net->w_ih[(2 * H + i) * D + d] * x[d];
+      }
+      if (!reset) {
+        for (uint64_t j = 0; j < H; ++j) {
+          const double hj = h_prev[j];
+          acc_r += net->w_hh[i * H + j] * hj;
+          acc_z += net->w_hh[(H + i) * H + j] * hj;
+          acc_hn += net->w_hh[(2 * H + i) * H + j] * hj;
+        }
+      }
+      const double r = sigmoid(acc_r);
+      const double z = sigmoid(acc_z);
+      const double n = tanh(acc_n + r * acc_hn);
+      const double h_old = reset ? 0.0 : h_prev[i];
+      hidden_out[b * H + i] = (1.0 - z) * n + z * h_old;
+    }
+    const double* h = hidden_out + b * H;
+    for (uint64_t a = 0; a < A; ++a) {
+      double acc = net->b_actor[a];
+      for (uint64_t j = 0; j < H; ++j) acc += net->w_actor[a * H + j] * h[j];
+      logits[b * A + a] = acc;
+    }
+    double v = net->b_critic;
+    for (uint64_t j = 0; j < H; ++j) v += net->w_critic[j] * h[j];
+    values[b] = v;
+  }
+}
+
+static int sample_categorical(const double* logits, int n, double u, double* logp) { /* ppo.hpp:80-98 */
+  double max_l = logits[0];
+  for (int a = 0; a < n; ++a) max_l = max_l < logits[a] ? logits[a] : max_l;
+  double z = 0.0;
+  for (int a = 0; a < n; ++a) z += exp(logits[a] - max_l);
+  const double target = u * z;
+  double cum = 0.0;
+  int action = n - 1;
+  for (int a = 0; a < n; ++a) {
+    cum += exp(logits[a] - max_l);
+    if (cum > target) {
+      action = a;
+      break;
+    }
+  }
+  *logp = logits[action] - max_l - log(z);
+  return action;
+}
+
+static void compute_gae(const double* rewards, const double* values, const uint8_t* dones, uint64_t T,
+                        uint64_t B, double discount, double gae_lambda, double* adv, double* ret) { /* gae.hpp:14-32 */
+  for (uint64_t b = 0; b < B; ++b) {
+    double carry = 0.0;
+    for (uint64_t t = T; t-- > 0;) {
+      const double not_done = dones[t * B + b] ? 0.0 : 1.0;
+      const double delta = rewards[t * B + b] + discount * values[(t + 1) * B + b] * not_done - values[t * B + b];
+      carry = delta + discount * gae_lambda * not_done * carry;
+      adv[t * B + b] = carry;
+      ret[t * B + b] = carry + values[t * B + b];
+    }
+  }
+}
+
+typedef struct rbatch { /* RolloutBatch, ppo.hpp:33-66 */
+  uint64_t T, B, D, H;
+  double *obs, *log_probs, *values, *rewards, *h0, *adv, *ret;
+  int32_t* actions;
+  uint8_t *dones, *resets;
+} rbatch;
+
+struct rollout_state {
+  int n_types;
+  double* hidden[MLOB_MAX_SPECS];
+  rbatch b[MLOB_MAX_SPECS];
+};
+
+static void rbatch_free(rbatch* b) {
+  free(b->obs); free(b->log_probs); free(b->values); free(b->rewards); free(b->h0);
+  free(b->adv); free(b->ret); free(b->actions); free(b->dones); free(b->resets);
+  memset(b, 0, sizeof *b);
+}
+
+static void rollout_free(struct rollout_state* r) {
+  if (!r) return;
+  for (int t = 0; t < r->n_types; ++t) {
+    free(r->hidden[t]);
+    rbatch_free(&r->b[t]);
+  }
+  free(r);
+}
+
+static void rbatch_resize(rbatch* b, uint64_t T, uint64_t B, uint64_t D, uint64_t H) { /* ppo.hpp:50-63 */
+  rbatch_free(b);
+  b->T = T; b->B = B; b->D = D; b->H = H;
+  b->obs = calloc(T * B * D + 1, 8);
+  b->actions = calloc(T * B + 1, 4);
+  b->log_probs = calloc(T * B + 1, 8);
+  b->values = calloc((T + 1) * B + 1, 8);
+  b->rewards = calloc(T * B + 1, 8);
+  b->dones = calloc(T * B + 1, 1);
+  b->resets = calloc(T * B + 1, 1);
+  b->h0 = calloc(B * H + 1, 8);
+  b->adv = calloc(T * B + 1, 8);
+  b->ret = calloc(T * B + 1, 8);
+}
+
+int orc_venv_collect_rollout(void* v_, const mlob_policy_net* nets, const mlob_rollout_config* cfg,
+                             uint64_t update_index) { /* rollout.hpp:41-124 */
+  venv* v = v_;
+  const int NT = v->cfg.n_specs;
+  if (!v->roll) { /* train_loop: zero hidden per type (rollout.hpp:132-135) */
+    v->roll = calloc(1, sizeof(struct rollout_state));
+    v->roll->n_types = NT;
+    for (int t = 0; t < NT; ++t)
+      v->roll->hidden[t] = calloc((uint64_t)v->n_envs * v->cfg.specs[t].count * nets[t].hidden + 1, 8);
+  }
+  struct rollout_state* rs = v->roll;
+  const uint64_t T = (uint64_t)cfg->rollout_len;
+  double* logits[MLOB_MAX_SPECS];
+  double* hidden_next[MLOB_MAX_SPECS];
+  for (int t = 0; t < NT; ++t) {
+    const uint64_t B = (uint64_t)v->n_envs * v->cfg.specs[t].count, H = (uint64_t)nets[t].hidden;
+    rbatch* b = &rs->b[t];
+    if (b->T != T || b->B != B)
+      rbatch_resize(b, T, B, observation_size(v->cfg.specs[t].obs_space, v->cfg.obs_depth), H);
+    logits[t] = calloc(B * nets[t].n_actions + 1, 8);
+    hidden_next[t] = calloc(B * H + 1, 8);
+    memcpy(b->h0, rs->hidden[t], B * H * 8);
+  }
+  int status = MLOB_OK;
+  for (uint64_t step = 0; step < T && status == MLOB_OK; ++step) {
+    for (int t = 0; t < NT; ++t) {
+      rbatch* b = &rs->b[t];
+      const uint64_t B = b->B, D = b->D, A = (uint64_t)nets[t].n_actions;
+      orc_venv_gather(v, t, b->obs + step * B * D, b->resets + step * B);
+      policy_forward(&nets[t], b->obs + step * B * D, rs->hidden[t], b->resets + step * B, B, logits[t],
+                     b->values + step * B, hidden_next[t]);
+      double* tmp = rs->hidden[t];
+      rs->hidden[t] = hidden_next[t];
+      hidden_next[t] = tmp;
+      for (uint64_t s = 0; s < B; ++s) {
+        const uint64_t w[5] = {3 /* ActionSample */, (uint64_t)t, update_index, step, s};
+        crng r = {make_key(cfg->seed, 5, w)};
+        double logp = 0.0;
+        const int action = sample_categorical(logits[t] + s * A, (int)A, crng_uniform(&r), &logp);
+        b->actions[step * B + s] = action;
+        b->log_probs[step * B + s] = logp;
+        orc_venv_set_action(v, t, s, action);
+      }
+    }
+    status = orc_venv_step_all(v);
+    for (int t = 0; t < NT && status == MLOB_OK; ++t) {
+      rbatch* b = &rs->b[t];
+      for (uint64_t s = 0; s < b->B; ++s) {
+        b->rewards[step * b->B + s] = orc_venv_reward(v, t, s);
+        b->dones[step * b->B + s] = orc_venv_done(v, t, s) ? 1 : 0;
+      }
+    }
+  }
+  for (int t = 0; t < NT && status == MLOB_OK; ++t) { /* bootstrap + GAE (rollout.hpp:105-123) */
+    rbatch* b = &rs->b[t];
+    double* boot_obs = calloc(b->B * b->D + 1, 8);
+    uint8_t* boot_reset = calloc(b->B + 1, 1);
+    double* scratch = calloc(b->B * b->H + 1, 8);
+    orc_venv_gather(v, t, boot_obs, boot_reset);
+    policy_forward(&nets[t], boot_obs, rs->hidden[t], boot_reset, b->B, logits[t], b->values + T * b->B, scratch);
+    compute_gae(b->rewards, b->values, b->dones, T, b->B, cfg->discount, cfg->gae_lambda, b->adv, b->ret);
+    free(boot_obs);
+    free(boot_reset);
+    free(scratch);
+  }
+  for (int t = 0; t < NT; ++t) {
+    free(logits[t]);
+    free(hidden_next[t]);
+  }
+  return status;
+}
+
+uint64_t orc_venv_rollout_field(void* v_, int type, int field, void* out, uint64_t cap) {
+  venv* v = v_;
+  if (!v->roll) return 0;
+  const rbatch* b = &v->roll->b[type];
+  const uint64_t TB = b->T * b->B;
+  const void* src = NULL;
+  uint64_t bytes = 0;
+  switch (field) {
+    case MLOB_RB_OBS: src = b->obs; bytes = TB * b->D * 8; break;
+    case MLOB_RB_ACTIONS: src = b->actions; bytes = TB * 4; break;
+    case MLOB_RB_LOG_PROBS: src = b->log_probs; bytes = TB * 8; break;
+    case MLOB_RB_VALUES: src = b->values; bytes = (TB + b->B) * 8; break;
+    case MLOB_RB_REWARDS: src = b->rewards; bytes = TB * 8; break;
+    case MLOB_RB_DONES: src = b->dones; bytes = TB; break;
+    case MLOB_RB_RESETS: src = b->resets; bytes = TB; break;
+    case MLOB_RB_H0: src = b->h0; bytes = b->B * b->H * 8; break;
+    case MLOB_RB_ADVANTAGES: src = b->adv; bytes = TB * 8; break;
+    case MLOB_RB_RETURNS: src = b->ret; bytes = TB * 8; break;
+    case MLOB_RB_HIDDEN: src = v->roll->hidden[type]; bytes = b->B * b->H * 8; break;
+  }
+  if (src && bytes <= cap) memcpy(out, src, bytes);
+  return bytes;
 }

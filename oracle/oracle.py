@@ -112,6 +112,10 @@ _SIG = {
     "bench_run": (C.c_int, [C.c_void_p, _P(EnvConfig), C.c_int, C.c_int, C.c_int, C.c_int,
                             C.c_uint64, C.c_int, C.c_int, _P(BenchRow)]),
     "random_stream": (None, [_P(StreamConfig), C.c_uint64, _P(Message)]),
+    "make_policy_net": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, _P(C.c_double)]),
+    "venv_collect_rollout": (C.c_int, [C.c_void_p, _P(abi.PolicyNetC), _P(abi.RolloutConfig),
+                                       C.c_uint64]),
+    "venv_rollout_field": (C.c_uint64, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_uint64]),
     "evaluate_matrix": (C.c_int, [C.c_void_p, _P(EnvConfig), _P(C.c_uint64), C.c_uint64,
                                   _P(abi.Policy), C.c_int, _P(abi.Policy), C.c_int, C.c_uint64,
                                   _P(abi.CellStats)]),
@@ -155,13 +159,20 @@ class Oracle:
             fn = getattr(self.lib, f"{kind}_{name}")
             fn.restype = res
             fn.argtypes = args
-            setattr(self, name, fn)
+            setattr(self, name + "_" if name == "make_policy_net" else name, fn)
         _cache[kind] = self
         return self
 
     def check(self, rc: int) -> None:
         if rc != abi.MLOB_OK:
             raise _EXC.get(rc, OracleError)(self.last_error().decode())
+
+    def make_policy_net(self, obs_dim: int, hidden: int, n_actions: int, seed: int) -> abi.NetParams:
+        """ippo::make_policy_net (net.hpp:80-104)."""
+        out = np.zeros(abi.NetParams.param_count(obs_dim, hidden, n_actions), dtype=np.float64)
+        self.check(self.make_policy_net_(obs_dim, hidden, n_actions, seed,
+                                         out.ctypes.data_as(_P(C.c_double))))
+        return abi.NetParams(obs_dim, hidden, n_actions, out)
 
     def evaluate(self, store: "OStore", cfg: EnvConfig, episodes, type0, type1, seed: int):
         """evaluate_matrix (evaluate.hpp:104-217) -> list of CellStats, row-major."""
@@ -416,6 +427,20 @@ class OVecEnv:
 
     def step_all(self):
         self.o.check(self.o.venv_step_all(self.h))
+
+    def collect_rollout(self, nets, rollout_len: int, discount: float, gae_lambda: float,
+                        seed: int, update_index: int):
+        """ippo::collect_rollout (rollout.hpp:41-124); nets: one abi.NetParams per type."""
+        arr = (abi.PolicyNetC * len(nets))(*[n.to_c() for n in nets])
+        c = abi.RolloutConfig(rollout_len=rollout_len, discount=discount, gae_lambda=gae_lambda,
+                              seed=seed)
+        self.o.check(self.o.venv_collect_rollout(self.h, arr, C.byref(c), update_index))
+
+    def rollout(self, t: int, field: int) -> np.ndarray:
+        n = self.o.venv_rollout_field(self.h, t, field, None, 0)
+        out = np.zeros(n, dtype=np.uint8)
+        self.o.venv_rollout_field(self.h, t, field, out.ctypes.data, n)
+        return out.view(abi.RB_DTYPES[field])
 
     def gather(self, t):
         count = self.cfg.specs[t].count

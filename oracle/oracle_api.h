@@ -90,6 +90,11 @@ typedef struct orc_bench_row {
   int P##bench_run(void* store, const mlob_env_config* base, int n_envs, int n_steps,          \
                    int warmup, int workers, uint64_t seed, int messages_per_step,              \
                    int agents_per_type, orc_bench_row* out);                                   \
+  /* networks and rollouts (ippo/net.hpp make_policy_net, rollout.hpp collect_rollout) */     \
+  int P##make_policy_net(int obs_dim, int hidden, int n_actions, uint64_t seed, double* out);  \
+  int P##venv_collect_rollout(void* v, const mlob_policy_net* nets,                           \
+                              const mlob_rollout_config* cfg, uint64_t update_index);         \
+  uint64_t P##venv_rollout_field(void* v, int type, int field, void* out, uint64_t cap);      \
   /* cross-play grid (ippo/evaluate.hpp evaluate_matrix, scripted policies) */                \
   int P##evaluate_matrix(void* store, const mlob_env_config* cfg, const uint64_t* episodes,   \
                          uint64_t n_episodes, const mlob_policy* type0, int n0,               \

@@ -163,7 +163,28 @@ struct VenvH {
   std::unique_ptr<data::EpisodeIndex> index;
   std::unique_ptr<util::ThreadPool> pool;
   std::unique_ptr<ippo::MarketVecEnv> venv;
+  // collect_rollout state (rollout.hpp:41-124): nets, persistent hidden, batches
+  std::vector<ippo::PolicyNet> nets;
+  std::vector<std::vector<double>> hidden;
+  std::vector<ippo::RolloutBatch> batches;
 };
+
+ippo::PolicyNet to_net(const mlob_policy_net& n) {
+  ippo::PolicyNet r;
+  r.obs_dim = n.obs_dim;
+  r.hidden = n.hidden;
+  r.n_actions = n.n_actions;
+  const std::size_t D = n.obs_dim, H = n.hidden, A = n.n_actions;
+  r.w_ih.assign(n.w_ih, n.w_ih + 3 * H * D);
+  r.w_hh.assign(n.w_hh, n.w_hh + 3 * H * H);
+  r.b_ih.assign(n.b_ih, n.b_ih + 3 * H);
+  r.b_hh.assign(n.b_hh, n.b_hh + 3 * H);
+  r.w_actor.assign(n.w_actor, n.w_actor + A * H);
+  r.b_actor.assign(n.b_actor, n.b_actor + A);
+  r.w_critic.assign(n.w_critic, n.w_critic + H);
+  r.b_critic = n.b_critic;
+  return r;
+}
 
 }  // namespace
 
@@ -433,6 +454,62 @@ void* ref_venv_instance(void* v, uint64_t e) {
   return h;
 }
 void ref_venv_free(void* v) { delete static_cast<VenvH*>(v); }
+
+// ---- networks and rollouts (ippo/net.hpp, ippo/rollout.hpp) ----
+int ref_make_policy_net(int obs_dim, int hidden, int n_actions, uint64_t seed, double* out) {
+  return guarded([&] {
+    ippo::PolicyNet n = ippo::make_policy_net(obs_dim, hidden, n_actions, seed);
+    std::size_t i = 0;
+    n.for_each_param([&](double& v) { out[i++] = v; });
+  });
+}
+
+int ref_venv_collect_rollout(void* v, const mlob_policy_net* nets, const mlob_rollout_config* cfg,
+                             uint64_t update_index) {
+  auto* h = static_cast<VenvH*>(v);
+  return guarded([&] {
+    const int T = h->venv->n_types();
+    const bool fresh = h->nets.empty();
+    h->nets.clear();
+    for (int t = 0; t < T; ++t) h->nets.push_back(to_net(nets[t]));
+    if (fresh) {  // train_loop, rollout.hpp:132-135
+      h->hidden.assign(static_cast<std::size_t>(T), {});
+      for (int t = 0; t < T; ++t)
+        h->hidden[t].assign(h->venv->n_streams(t) * static_cast<std::size_t>(nets[t].hidden), 0.0);
+      h->batches.assign(static_cast<std::size_t>(T), {});
+    }
+    ippo::TrainLoopConfig c;
+    c.rollout_len = cfg->rollout_len;
+    c.discount = cfg->discount;
+    c.gae_lambda = cfg->gae_lambda;
+    c.seed = cfg->seed;
+    ippo::collect_rollout(*h->venv, h->nets, h->hidden, h->batches, c, update_index);
+  });
+}
+
+uint64_t ref_venv_rollout_field(void* v, int type, int field, void* out, uint64_t cap) {
+  auto* h = static_cast<VenvH*>(v);
+  const ippo::RolloutBatch& b = h->batches.at(static_cast<std::size_t>(type));
+  const auto put = [&](const auto& vec) -> uint64_t {
+    const uint64_t bytes = vec.size() * sizeof(vec[0]);
+    if (bytes <= cap) std::memcpy(out, vec.data(), bytes);
+    return bytes;
+  };
+  switch (field) {
+    case MLOB_RB_OBS: return put(b.obs);
+    case MLOB_RB_ACTIONS: return put(b.actions);
+    case MLOB_RB_LOG_PROBS: return put(b.log_probs);
+    case MLOB_RB_VALUES: return put(b.values);
+    case MLOB_RB_REWARDS: return put(b.rewards);
+    case MLOB_RB_DONES: return put(b.dones);
+    case MLOB_RB_RESETS: return put(b.resets);
+    case MLOB_RB_H0: return put(b.h0);
+    case MLOB_RB_ADVANTAGES: return put(b.advantages);
+    case MLOB_RB_RETURNS: return put(b.returns);
+    case MLOB_RB_HIDDEN: return put(h->hidden.at(static_cast<std::size_t>(type)));
+  }
+  return 0;
+}
 
 // ---- bench ----
 int ref_bench_run(void* store, const mlob_env_config* base, int n_envs, int n_steps, int warmup,

@@ -137,6 +137,58 @@ class SynthConfig(C.Structure):
                 ("state_depth", u64)]
 
 
+class PolicyNetC(C.Structure):
+    """mlob_policy_net: ippo::PolicyNet (net.hpp:18-30) as host array pointers."""
+    _P = C.POINTER(f64)
+    _fields_ = [("obs_dim", i32), ("hidden", i32), ("n_actions", i32), ("_pad", i32),
+                ("w_ih", _P), ("w_hh", _P), ("b_ih", _P), ("b_hh", _P), ("w_actor", _P),
+                ("b_actor", _P), ("w_critic", _P), ("b_critic", f64)]
+
+
+class RolloutConfig(C.Structure):  # TrainLoopConfig (rollout.hpp:30-37)
+    _fields_ = [("rollout_len", i32), ("_pad", i32), ("discount", f64), ("gae_lambda", f64),
+                ("seed", u64)]
+
+
+# RolloutBatch fields (ppo.hpp:33-48) + the persistent hidden state
+(RB_OBS, RB_ACTIONS, RB_LOG_PROBS, RB_VALUES, RB_REWARDS, RB_DONES, RB_RESETS, RB_H0,
+ RB_ADVANTAGES, RB_RETURNS, RB_HIDDEN) = range(11)
+RB_DTYPES = {RB_OBS: "<f8", RB_ACTIONS: "<i4", RB_LOG_PROBS: "<f8", RB_VALUES: "<f8",
+             RB_REWARDS: "<f8", RB_DONES: "u1", RB_RESETS: "u1", RB_H0: "<f8",
+             RB_ADVANTAGES: "<f8", RB_RETURNS: "<f8", RB_HIDDEN: "<f8"}
+
+
+class NetParams:
+    """A PolicyNet's parameters as numpy arrays, flat order of
+    PolicyNet::for_each_param (net.hpp:36-41): w_ih, w_hh, b_ih, b_hh, w_actor,
+    b_actor, w_critic, b_critic."""
+
+    def __init__(self, obs_dim: int, hidden: int, n_actions: int, flat):
+        import numpy as np
+        D, H, A = obs_dim, hidden, n_actions
+        self.obs_dim, self.hidden, self.n_actions = D, H, A
+        self.flat = np.ascontiguousarray(flat, dtype=np.float64).copy()
+        sizes = [3 * H * D, 3 * H * H, 3 * H, 3 * H, A * H, A, H, 1]
+        if self.flat.size != sum(sizes):
+            raise ValueError(f"expected {sum(sizes)} parameters, got {self.flat.size}")
+        offs = np.cumsum([0] + sizes)
+        self.parts = [self.flat[offs[i]:offs[i + 1]] for i in range(8)]
+
+    @staticmethod
+    def param_count(obs_dim: int, hidden: int, n_actions: int) -> int:
+        return 3 * hidden * (obs_dim + hidden + 2) + n_actions * hidden + n_actions + hidden + 1
+
+    def to_c(self) -> PolicyNetC:
+        n = PolicyNetC()
+        n.obs_dim, n.hidden, n.n_actions = self.obs_dim, self.hidden, self.n_actions
+        P = C.POINTER(f64)
+        for name, arr in zip(("w_ih", "w_hh", "b_ih", "b_hh", "w_actor", "b_actor", "w_critic"),
+                             self.parts[:7]):
+            setattr(n, name, arr.ctypes.data_as(P))
+        n.b_critic = float(self.parts[7][0])
+        return n
+
+
 class Policy(C.Structure):
     """mlob_policy = ippo::PolicyChoice without the network (evaluate.hpp:19-25)."""
     _fields_ = [("kind", i32), ("twap_mode", i32), ("avst_gamma_index", i32), ("n_gamma", i32),

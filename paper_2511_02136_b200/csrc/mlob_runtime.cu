@@ -14,6 +14,7 @@
 
 #include "mlob_dev.h"
 #include "mlob_host.h"
+#include "mlob_policy.h"
 
 namespace mlob {
 size_t step_smem_bytes(const DevCfg& c);
@@ -65,12 +66,6 @@ T* dalloc(size_t n, const char* what) {
   return static_cast<T*>(p);
 }
 
-struct DevFree {
-  void operator()(void* p) const {
-    if (p) cudaFree(p);
-  }
-};
-
 int64_t fits32(int64_t v, const char* what) {
   if (v <= INT32_MIN || v >= INT32_MAX)
     fail(MLOB_E_INVALID_ARGUMENT, std::string(what) + " outside the device int32 range");
@@ -118,6 +113,25 @@ struct mlob_venv {
   uint8_t* d_env_policy = nullptr;
   uint64_t* d_env_cell = nullptr;
   bool has_cells = false;
+  // on-device rollouts (mlob_policy.cu): one network + hidden state per type,
+  // one RolloutBatch arena per type
+  struct NetState {
+    DevNet dn{};
+    double* w = nullptr;  // all weights, transposed layout (mlob_policy.h)
+    double* hidden[2] = {};
+    int cur = 0;
+  };
+  struct Batch {
+    uint64_t T = 0, B = 0;
+    char* arena = nullptr;
+    double *obs = nullptr, *log_probs = nullptr, *values = nullptr, *rewards = nullptr, *h0 = nullptr,
+           *adv = nullptr, *ret = nullptr;
+    int32_t* actions = nullptr;
+    uint8_t *dones = nullptr, *resets = nullptr;
+  };
+  NetState nets[MLOB_MAX_SPECS];
+  Batch batch[MLOB_MAX_SPECS];
+  bool has_nets = false;
   std::vector<uint64_t> starts;
   std::vector<EpState> ep_state;
   std::vector<uint64_t> pool;  // empty = identity
@@ -173,6 +187,12 @@ struct mlob_venv {
         cudaStreamDestroy(s);
       }
     for (cudaEvent_t e : io_events) cudaEventDestroy(e);
+    for (int t = 0; t < MLOB_MAX_SPECS; ++t) {
+      cudaFree(nets[t].w);
+      cudaFree(nets[t].hidden[0]);
+      cudaFree(nets[t].hidden[1]);
+      cudaFree(batch[t].arena);
+    }
     for (void* p : allocs) cudaFree(p);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
@@ -889,6 +909,216 @@ mlob_status mlob_venv_dones(mlob_venv* v, uint8_t* out) {
 }
 mlob_status mlob_venv_infos(mlob_venv* v, mlob_agent_info* out) {
   return guarded([&] { d2h(v, out, v->d_infos, v->n_envs * v->A); });
+}
+
+// ---- on-device policy inference and rollouts -------------------------------
+
+mlob_status mlob_venv_set_nets(mlob_venv* v, const mlob_policy_net* nets) {
+  return guarded([&] {
+    if (!nets) fail(MLOB_E_INVALID_ARGUMENT, "set_nets: null");
+    const int T = v->cfg.n_specs;
+    for (int t = 0; t < T; ++t) {  // shapes first: nothing changes on error
+      const mlob_policy_net& n = nets[t];
+      if (n.obs_dim != v->dcfg.specs[t].obs_dim || n.n_actions != v->dcfg.specs[t].arity)
+        fail(MLOB_E_INVALID_ARGUMENT, "set_nets: type " + std::to_string(t) + " expects obs_dim " +
+                                          std::to_string(v->dcfg.specs[t].obs_dim) + ", n_actions " +
+                                          std::to_string(v->dcfg.specs[t].arity));
+      if (n.hidden < 1 || n.hidden > kPolicyMaxHidden)
+        fail(MLOB_E_INVALID_ARGUMENT, "make_policy_net: hidden size capped at 512");
+      if (n.n_actions > kPolicyMaxActions || n.obs_dim > kPolicyMaxObs)
+        fail(MLOB_E_INVALID_ARGUMENT, "set_nets: network shape beyond the device limits");
+      if (!n.w_ih || !n.w_hh || !n.b_ih || !n.b_hh || !n.w_actor || !n.b_actor || !n.w_critic)
+        fail(MLOB_E_INVALID_ARGUMENT, "set_nets: null weight array");
+    }
+    v->set_device();
+    for (int t = 0; t < T; ++t) {
+      const mlob_policy_net& n = nets[t];
+      const size_t D = n.obs_dim, H = n.hidden, A = n.n_actions, H3 = 3 * H;
+      // transposed copies (mlob_policy.h), then the vectors as they are
+      std::vector<double> w(H3 * D + H3 * H + 2 * H3 + A * H + A + H);
+      double* p = w.data();
+      double* w_ihT = p;
+      for (size_t r = 0; r < H3; ++r)
+        for (size_t d = 0; d < D; ++d) w_ihT[d * H3 + r] = n.w_ih[r * D + d];
+      double* w_hhT = w_ihT + H3 * D;
+      for (size_t r = 0; r < H3; ++r)
+        for (size_t j = 0; j < H; ++j) w_hhT[j * H3 + r] = n.w_hh[r * H + j];
+      double* b_ih = w_hhT + H3 * H;
+      std::memcpy(b_ih, n.b_ih, H3 * 8);
+      double* b_hh = b_ih + H3;
+      std::memcpy(b_hh, n.b_hh, H3 * 8);
+      double* w_aT = b_hh + H3;
+      for (size_t a = 0; a < A; ++a)
+        for (size_t j = 0; j < H; ++j) w_aT[j * A + a] = n.w_actor[a * H + j];
+      double* b_a = w_aT + A * H;
+      std::memcpy(b_a, n.b_actor, A * 8);
+      double* w_c = b_a + A;
+      std::memcpy(w_c, n.w_critic, H * 8);
+      mlob_venv::NetState& ns = v->nets[t];
+      const uint64_t B = v->n_envs * static_cast<uint64_t>(v->cfg.specs[t].count);
+      const bool same_shape = ns.w && ns.dn.D == n.obs_dim && ns.dn.H == n.hidden && ns.dn.A == n.n_actions;
+      if (!same_shape) {
+        cudaFree(ns.w);
+        cudaFree(ns.hidden[0]);
+        cudaFree(ns.hidden[1]);
+        ns = mlob_venv::NetState{};
+        cuda_check(cudaMalloc(&ns.w, w.size() * 8), "cudaMalloc(net)");
+        cuda_check(cudaMalloc(&ns.hidden[0], std::max<uint64_t>(1, B * H) * 8), "cudaMalloc(hidden)");
+        cuda_check(cudaMalloc(&ns.hidden[1], std::max<uint64_t>(1, B * H) * 8), "cudaMalloc(hidden)");
+        cuda_check(cudaMemsetAsync(ns.hidden[0], 0, B * H * 8, v->stream), "memset");
+      }
+      cuda_check(cudaMemcpyAsync(ns.w, w.data(), w.size() * 8, cudaMemcpyHostToDevice, v->stream), "H2D");
+      const double* base = ns.w;
+      ns.dn.D = n.obs_dim;
+      ns.dn.H = n.hidden;
+      ns.dn.A = n.n_actions;
+      ns.dn.w_ihT = base;
+      ns.dn.w_hhT = base + (w_hhT - w.data());
+      ns.dn.b_ih = base + (b_ih - w.data());
+      ns.dn.b_hh = base + (b_hh - w.data());
+      ns.dn.w_actorT = base + (w_aT - w.data());
+      ns.dn.b_actor = base + (b_a - w.data());
+      ns.dn.w_critic = base + (w_c - w.data());
+      ns.dn.b_critic = n.b_critic;
+      cuda_check(cudaStreamSynchronize(v->stream), "sync");  // `w` is a host temporary
+    }
+    v->has_nets = true;
+  });
+}
+
+static void ensure_batch(mlob_venv* v, int t, uint64_t T) {
+  mlob_venv::Batch& b = v->batch[t];
+  const uint64_t B = v->n_envs * static_cast<uint64_t>(v->cfg.specs[t].count);
+  if (b.arena && b.T == T && b.B == B) return;
+  cudaFree(b.arena);
+  b = mlob_venv::Batch{};
+  const uint64_t D = v->nets[t].dn.D, H = v->nets[t].dn.H, TB = T * B;
+  const uint64_t sizes[10] = {TB * D * 8, TB * 8, (TB + B) * 8, TB * 8, B * H * 8, TB * 8, TB * 8, TB * 4, TB, TB};
+  uint64_t total = 0;
+  for (uint64_t z : sizes) total += (z + 255) / 256 * 256;
+  cuda_check(cudaMalloc(&b.arena, std::max<uint64_t>(total, 256)), "cudaMalloc(rollout batch)");
+  char* p = b.arena;
+  void** dst[10] = {(void**)&b.obs, (void**)&b.log_probs, (void**)&b.values, (void**)&b.rewards, (void**)&b.h0,
+                    (void**)&b.adv, (void**)&b.ret, (void**)&b.actions, (void**)&b.dones, (void**)&b.resets};
+  for (int i = 0; i < 10; ++i) {
+    *dst[i] = p;
+    p += (sizes[i] + 255) / 256 * 256;
+  }
+  b.T = T;
+  b.B = B;
+}
+
+static PolicyArgs policy_args(mlob_venv* v, int t, const mlob_rollout_config& c, uint64_t update) {
+  PolicyArgs pa{};
+  mlob_venv::NetState& ns = v->nets[t];
+  pa.net = ns.dn;
+  pa.B = v->n_envs * static_cast<uint64_t>(v->cfg.specs[t].count);
+  pa.count = v->cfg.specs[t].count;
+  pa.offset = v->dcfg.specs[t].flat_offset;
+  pa.agents_per_env = v->A;
+  pa.type = t;
+  pa.seed = c.seed;
+  pa.update_index = update;
+  pa.obs_env = v->d_obs[t];
+  pa.just_reset = v->d_just_reset;
+  pa.env_rewards = v->d_rewards;
+  pa.env_dones = v->d_dones;
+  pa.env_actions = v->d_actions;
+  const mlob_venv::Batch& b = v->batch[t];
+  pa.actions = b.actions;
+  pa.log_probs = b.log_probs;
+  pa.values = b.values;
+  pa.rewards = b.rewards;
+  pa.dones = b.dones;
+  pa.resets = b.resets;
+  return pa;
+}
+
+mlob_status mlob_venv_collect_rollout(mlob_venv* v, const mlob_rollout_config* cfg, uint64_t update_index) {
+  return guarded([&] {
+    if (!cfg || cfg->rollout_len < 1) fail(MLOB_E_INVALID_ARGUMENT, "collect_rollout: rollout_len >= 1");
+    if (!v->has_nets) fail(MLOB_E_LOGIC, "collect_rollout: set_nets first");
+    if (!(v->flags & MLOB_VENV_AUTO_RESET)) fail(MLOB_E_LOGIC, "collect_rollout: needs an auto-reset handle");
+    if (v->step_ctr < 0) fail(MLOB_E_LOGIC, "MarketEnv::step: episode is terminal; reset first");
+    v->set_device();
+    const uint64_t T = static_cast<uint64_t>(cfg->rollout_len);
+    const int NT = v->cfg.n_specs;
+    for (int t = 0; t < NT; ++t) ensure_batch(v, t, T);
+    for (uint64_t step = 0; step < T; ++step) {
+      for (int t = 0; t < NT; ++t) {  // gather + policy_forward + sample + set_action
+        mlob_venv::NetState& ns = v->nets[t];
+        mlob_venv::Batch& b = v->batch[t];
+        PolicyArgs pa = policy_args(v, t, *cfg, update_index);
+        pa.row = static_cast<int32_t>(step);
+        pa.prev_row = static_cast<int32_t>(step) - 1;
+        pa.sample = 1;
+        pa.hidden_in = ns.hidden[ns.cur];
+        pa.hidden_out = ns.hidden[ns.cur ^ 1];
+        pa.h0_out = step == 0 ? b.h0 : nullptr;
+        pa.obs_out = b.obs + step * b.B * static_cast<uint64_t>(ns.dn.D);
+        cuda_check(launch_policy(pa, v->stream), "policy kernel");
+        ++v->launches;
+        ns.cur ^= 1;
+      }
+      do_step(v, kActIds, 0, 0);  // step_all
+    }
+    for (int t = 0; t < NT; ++t) {  // bootstrap values (hidden untouched), then GAE
+      mlob_venv::NetState& ns = v->nets[t];
+      mlob_venv::Batch& b = v->batch[t];
+      PolicyArgs pa = policy_args(v, t, *cfg, update_index);
+      pa.row = static_cast<int32_t>(T);
+      pa.prev_row = static_cast<int32_t>(T) - 1;
+      pa.sample = 0;
+      pa.hidden_in = ns.hidden[ns.cur];
+      cuda_check(launch_policy(pa, v->stream), "policy kernel");
+      cuda_check(launch_gae(b.rewards, b.values, b.dones, T, b.B, cfg->discount, cfg->gae_lambda, b.adv, b.ret,
+                            v->stream), "gae kernel");
+      v->launches += 2;
+    }
+    v->action_mode = kActIds;
+  });
+}
+
+static const void* rollout_field(const mlob_venv* v, int t, int field, uint64_t* bytes) {
+  const mlob_venv::Batch& b = v->batch[t];
+  const mlob_venv::NetState& ns = v->nets[t];
+  const uint64_t TB = b.T * b.B;
+  switch (field) {
+    case MLOB_RB_OBS: *bytes = TB * ns.dn.D * 8; return b.obs;
+    case MLOB_RB_ACTIONS: *bytes = TB * 4; return b.actions;
+    case MLOB_RB_LOG_PROBS: *bytes = TB * 8; return b.log_probs;
+    case MLOB_RB_VALUES: *bytes = (TB + b.B) * 8; return b.values;
+    case MLOB_RB_REWARDS: *bytes = TB * 8; return b.rewards;
+    case MLOB_RB_DONES: *bytes = TB; return b.dones;
+    case MLOB_RB_RESETS: *bytes = TB; return b.resets;
+    case MLOB_RB_H0: *bytes = b.B * ns.dn.H * 8; return b.h0;
+    case MLOB_RB_ADVANTAGES: *bytes = TB * 8; return b.adv;
+    case MLOB_RB_RETURNS: *bytes = TB * 8; return b.ret;
+    case MLOB_RB_HIDDEN:
+      *bytes = v->n_envs * static_cast<uint64_t>(v->cfg.specs[t].count) * ns.dn.H * 8;
+      return ns.hidden[ns.cur];
+  }
+  return nullptr;
+}
+
+mlob_status mlob_venv_rollout_read(mlob_venv* v, int type, int field, void* out, uint64_t cap_bytes) {
+  return guarded([&] {
+    if (type < 0 || type >= v->cfg.n_specs) fail(MLOB_E_OUT_OF_RANGE, "rollout_read: type out of range");
+    if (field < MLOB_RB_OBS || field > MLOB_RB_HIDDEN) fail(MLOB_E_OUT_OF_RANGE, "rollout_read: field");
+    uint64_t bytes = 0;
+    const void* src = rollout_field(v, type, field, &bytes);
+    if (!src) fail(MLOB_E_LOGIC, "rollout_read: no rollout collected");
+    if (cap_bytes < bytes) fail(MLOB_E_OUT_OF_RANGE, "rollout_read: buffer too small");
+    v->set_device();
+    cuda_check(cudaMemcpyAsync(out, src, bytes, cudaMemcpyDeviceToHost, v->stream), "D2H");
+    v->check_device_errors();
+  });
+}
+
+const void* mlob_venv_rollout_device(const mlob_venv* v, int type, int field) {
+  if (type < 0 || type >= v->cfg.n_specs) return nullptr;
+  uint64_t bytes = 0;
+  return rollout_field(v, type, field, &bytes);
 }
 
 // ---- scripted policies and cross-play evaluation ----------------------------

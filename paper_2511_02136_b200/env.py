@@ -91,6 +91,10 @@ _SIGS = {
     "mlob_venv_infos": (C.c_int, [_vp, _vp]),
     "mlob_venv_step_io": (C.c_int, [_vp, _P(abi.StepIO)]),
     "mlob_default_policy": (None, [C.c_int, _P(abi.Policy)]),
+    "mlob_venv_set_nets": (C.c_int, [_vp, _P(abi.PolicyNetC)]),
+    "mlob_venv_collect_rollout": (C.c_int, [_vp, _P(abi.RolloutConfig), C.c_uint64]),
+    "mlob_venv_rollout_read": (C.c_int, [_vp, C.c_int, C.c_int, _vp, C.c_uint64]),
+    "mlob_venv_rollout_device": (_vp, [_vp, C.c_int, C.c_int]),
     "mlob_venv_set_policies": (C.c_int, [_vp, _P(abi.Policy), C.c_int, _vp, _vp]),
     "mlob_evaluate_matrix": (C.c_int, [_vp, _P(EnvConfig), _P(C.c_uint64), C.c_uint64,
                                        _P(abi.Policy), C.c_int, _P(abi.Policy), C.c_int,
@@ -371,6 +375,29 @@ class _Venv:
 
     def synchronize(self) -> None:
         _check(lib().mlob_venv_synchronize(self.h))
+
+    def set_nets(self, nets) -> None:
+        """One abi.NetParams per agent type (mlob_venv_set_nets)."""
+        arr = (abi.PolicyNetC * len(nets))(*[n.to_c() for n in nets])
+        _check(lib().mlob_venv_set_nets(self.h, arr))
+        self._hidden = [n.hidden for n in nets]
+
+    def collect_rollout(self, rollout_len: int, discount: float = 0.99, gae_lambda: float = 0.95,
+                        seed: int = 0, update_index: int = 1) -> None:
+        """collect_rollout (rollout.hpp:41-124) on the device (mlob_venv_collect_rollout)."""
+        c = abi.RolloutConfig(rollout_len=rollout_len, discount=discount, gae_lambda=gae_lambda,
+                              seed=seed)
+        _check(lib().mlob_venv_collect_rollout(self.h, C.byref(c), update_index))
+        self._rollout_len = rollout_len
+
+    def rollout(self, t: int, field: int) -> np.ndarray:
+        """One RolloutBatch field of type t (time-major, flat) in host memory."""
+        T, B = self._rollout_len, self.n_streams(t)
+        n = {abi.RB_OBS: T * B * self.obs_dim(t), abi.RB_VALUES: (T + 1) * B,
+             abi.RB_H0: B * self._hidden[t], abi.RB_HIDDEN: B * self._hidden[t]}.get(field, T * B)
+        out = np.zeros(n, dtype=np.dtype(abi.RB_DTYPES[field]))
+        _check(lib().mlob_venv_rollout_read(self.h, t, field, _vp(out.ctypes.data), out.nbytes))
+        return out
 
     def set_policies(self, policies, env_policy, env_cell=None) -> None:
         """Scripted actions (mlob_venv_set_policies): env e's type-t agents act by

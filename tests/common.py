@@ -123,3 +123,16 @@ def crossplay_case():
     type1 = [A.policy(A.POLICY_TWAP), A.policy(A.POLICY_TWAP, twap_mode=A.TWAP_PASSIVE),
              A.policy(A.POLICY_RANDOM), A.policy(A.POLICY_NOOP), A.policy(A.POLICY_AVST)]
     return cfg, synth_kw, [2, 0, 5], type0, type1
+
+
+def rollout_case(o):
+    """(cfg, synth kwargs, nets) for rollout parity: MM x2 (FixedQuant) + Executor,
+    short episodes so auto-resets fall inside the rollout."""
+    A = abi
+    cfg = A.env_config([A.agent_spec(A.MARKET_MAKER, count=2), A.agent_spec(A.EXECUTOR)],
+                       steps_per_episode=8, messages_per_step=20, start_stride_steps=3)
+    nets = [o.make_policy_net(A.observation_size(cfg.specs[0].obs_space, cfg.obs_depth), 16,
+                              A.action_arity(cfg.specs[0]), 11),
+            o.make_policy_net(A.observation_size(cfg.specs[1].obs_space, cfg.obs_depth), 32,
+                              A.action_arity(cfg.specs[1]), 12)]
+    return cfg, {"state_sample_every": 20}, nets

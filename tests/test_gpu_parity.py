@@ -357,3 +357,34 @@ def test_scripted_policies_per_step(orc):
                                     eps[i % len(eps)]) for a in range(len(r.flat))]
             r.step(acts)
             compare_env_state(b.view(i), r)
+
+
+def test_collect_rollout_matches_oracle(orc):
+    """On-device collect_rollout against the oracle's (pinned to the reference):
+    actions, rewards, dones, resets and observations exact; values, log-probs,
+    advantages, returns and hidden states within 1e-10 relative + 1e-12 absolute (device exp /
+    tanh / log vs glibc; sums in the reference's order, no FMA)."""
+    from tests.common import rollout_case
+    cfg, synth_kw, nets = rollout_case(orc)
+    g = MarketVecEnv(dev_store(synth_kw), cfg, seed=3, n_envs=5)
+    o = OVecEnv(orc, small_store(orc, synth_kw), cfg, 3, 5)
+    g.reset_all()
+    o.reset_all()
+    with pytest.raises(RuntimeError):        # no nets yet
+        g.collect_rollout(12)
+    g.set_nets(nets)
+    exact = (abi.RB_OBS, abi.RB_ACTIONS, abi.RB_REWARDS, abi.RB_DONES, abi.RB_RESETS)
+    for upd in (1, 2, 3):
+        g.collect_rollout(12, 0.99, 0.95, seed=77, update_index=upd)
+        o.collect_rollout(nets, 12, 0.99, 0.95, 77, upd)
+        for t in range(cfg.n_specs):
+            for f in range(11):
+                a, b = g.rollout(t, f), o.rollout(t, f)
+                assert a.shape == b.shape, (t, f)
+                if f in exact:
+                    assert a.tobytes() == b.tobytes(), (upd, t, f)
+                else:
+                    np.testing.assert_allclose(a, b, rtol=1e-10, atol=1e-12, err_msg=f"{upd} {t} {f}")
+    bad = [nets[1], nets[0]]                 # shapes swapped
+    with pytest.raises(ValueError):
+        g.set_nets(bad)

@@ -310,3 +310,23 @@ def test_evaluate_matrix_errors(orc, ref):
                              messages_per_step=25, start_stride_steps=12)
         with pytest.raises(ValueError):   # evaluate.hpp:110-111 (two types)
             o.evaluate(st, one, eps, t0, t1, 0)
+
+
+def test_collect_rollout_matches_reference(orc, ref):
+    """make_policy_net (net.hpp:80-104) and collect_rollout (rollout.hpp:41-124:
+    GRU forward, ActionSample draws, env steps with auto-reset, bootstrap, GAE)
+    of the C restatement against the reference, two consecutive updates."""
+    from tests.common import rollout_case
+    got = {}
+    for o in (orc, ref):
+        cfg, synth_kw, nets = rollout_case(o)
+        v = OVecEnv(o, small_store(o, synth_kw), cfg, 3, 5)
+        v.reset_all()
+        out = [n.flat.tobytes() for n in nets]
+        for upd in (1, 2):
+            v.collect_rollout(nets, 12, 0.99, 0.95, 77, upd)
+            out += [v.rollout(t, f).tobytes() for t in range(2) for f in range(11)]
+        got[o.kind] = out
+    assert got["orc"] == got["ref"]
+    with pytest.raises(ValueError):  # net.hpp:86-87
+        orc.make_policy_net(8, 513, 8, 0)
