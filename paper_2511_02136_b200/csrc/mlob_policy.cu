@@ -39,15 +39,16 @@ __device__ __forceinline__ double sigmoid(double x) { return 1.0 / (1.0 + exp(-x
 // the rollout batch and the env's action buffer, or (bootstrap) the value only.
 // Also files the rewards / dones of the previous env step (rollout.hpp:94-100).
 __global__ void __launch_bounds__(kPolicyWarps * 32) policy_kernel(const PolicyArgs pa) {
-  __shared__ double sx[kPolicyWarps][kPolicyMaxObs];
-  __shared__ double sh[kPolicyWarps][kPolicyMaxHidden];
-  __shared__ double sn[kPolicyWarps][kPolicyMaxHidden];
-  __shared__ double sl[kPolicyWarps][kPolicyMaxActions];
+  extern __shared__ double psm[];  // per warp: x[D], h_prev[H], h_new[H], logits[A]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint64_t s = static_cast<uint64_t>(blockIdx.x) * kPolicyWarps + warp;
   if (s >= pa.B) return;
   const DevNet& nt = pa.net;
   const int D = nt.D, H = nt.H, A = nt.A, H3 = 3 * nt.H;
+  double* const sx = psm + static_cast<size_t>(warp) * (D + 2 * H + A);
+  double* const sh = sx + D;
+  double* const sn = sh + H;
+  double* const sl = sn + H;
   const uint64_t e = s / pa.count, slot = e * pa.agents_per_env + pa.offset + s % pa.count;
   const uint64_t B = pa.B;
   // rewards / dones of the step just taken (row t - 1)
@@ -58,12 +59,12 @@ __global__ void __launch_bounds__(kPolicyWarps * 32) policy_kernel(const PolicyA
   const uint8_t reset = pa.just_reset[e];  // gather's reset flag (rollout.hpp:210)
   const double* x = pa.obs_env + s * D;
   for (int d = lane; d < D; d += 32) {
-    sx[warp][d] = x[d];
+    sx[d] = x[d];
     if (pa.obs_out) pa.obs_out[s * D + d] = x[d];
   }
   const double* hp = pa.hidden_in + s * H;
   for (int j = lane; j < H; j += 32) {
-    sh[warp][j] = hp[j];
+    sh[j] = hp[j];
     if (pa.h0_out) pa.h0_out[s * H + j] = hp[j];
   }
   __syncwarp();
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(kPolicyWarps * 32) policy_kernel(const PolicyA
     double acc_n = nt.b_ih[2 * H + i];
     double acc_hn = nt.b_hh[2 * H + i];
     for (int d = 0; d < D; ++d) {
-      const double xd = sx[warp][d];
+      const double xd = sx[d];
       const double* w = nt.w_ihT + static_cast<size_t>(d) * H3;
       acc_r += w[i] * xd;
       acc_z += w[H + i] * xd;
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(kPolicyWarps * 32) policy_kernel(const PolicyA
     }
     if (!reset) {
       for (int j = 0; j < H; ++j) {
-        const double hj = sh[warp][j];
+        const double hj = sh[j];
         const double* w = nt.w_hhT + static_cast<size_t>(j) * H3;
         acc_r += w[i] * hj;
         acc_z += w[H + i] * hj;
@@ -91,21 +92,21 @@ __global__ void __launch_bounds__(kPolicyWarps * 32) policy_kernel(const PolicyA
     const double r = sigmoid(acc_r);
     const double z = sigmoid(acc_z);
     const double n = tanh(acc_n + r * acc_hn);
-    const double h_old = reset ? 0.0 : sh[warp][i];
+    const double h_old = reset ? 0.0 : sh[i];
     const double h_new = (1.0 - z) * n + z * h_old;
-    sn[warp][i] = h_new;
+    sn[i] = h_new;
     if (pa.hidden_out) pa.hidden_out[s * H + i] = h_new;
   }
   __syncwarp();
   for (int a = lane; a < A; a += 32) {  // actor head, net.hpp:175-179
     double acc = nt.b_actor[a];
-    for (int j = 0; j < H; ++j) acc += nt.w_actorT[static_cast<size_t>(j) * A + a] * sn[warp][j];
-    sl[warp][a] = acc;
+    for (int j = 0; j < H; ++j) acc += nt.w_actorT[static_cast<size_t>(j) * A + a] * sn[j];
+    sl[a] = acc;
   }
   __syncwarp();
   if (lane != 0) return;
   double v = nt.b_critic;  // critic head, net.hpp:180-182
-  for (int j = 0; j < H; ++j) v += nt.w_critic[j] * sn[warp][j];
+  for (int j = 0; j < H; ++j) v += nt.w_critic[j] * sn[j];
   pa.values[static_cast<uint64_t>(pa.row) * B + s] = v;
   if (!pa.sample) return;
   pa.resets[static_cast<uint64_t>(pa.row) * B + s] = reset;
@@ -114,7 +115,7 @@ __global__ void __launch_bounds__(kPolicyWarps * 32) policy_kernel(const PolicyA
   uint64_t key = pol_fold(pol_fold(pol_splitmix64(pa.seed), 3), static_cast<uint64_t>(pa.type));
   key = pol_fold(pol_fold(pol_fold(key, pa.update_index), static_cast<uint64_t>(pa.row)), s);
   const double u = static_cast<double>(pol_splitmix64(key + 0x9E3779B97F4A7C15ull) >> 11) * 0x1.0p-53;
-  const double* lg = sl[warp];
+  const double* lg = sl;
   double max_l = lg[0];
   for (int a = 0; a < A; ++a) max_l = max_l < lg[a] ? lg[a] : max_l;  // std::max(max_l, l)
   double zs = 0.0;
@@ -153,7 +154,13 @@ __global__ void gae_kernel(const double* rewards, const double* values, const ui
 cudaError_t launch_policy(const PolicyArgs& pa, cudaStream_t s) {
   if (pa.B == 0) return cudaSuccess;
   const unsigned blocks = static_cast<unsigned>((pa.B + kPolicyWarps - 1) / kPolicyWarps);
-  policy_kernel<<<blocks, kPolicyWarps * 32, 0, s>>>(pa);
+  const size_t smem = static_cast<size_t>(kPolicyWarps) * (pa.net.D + 2 * pa.net.H + pa.net.A) * sizeof(double);
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(policy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  policy_kernel<<<blocks, kPolicyWarps * 32, smem, s>>>(pa);
   return cudaGetLastError();
 }
 

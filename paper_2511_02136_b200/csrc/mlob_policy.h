@@ -8,7 +8,7 @@
 
 namespace mlob {
 
-constexpr int kPolicyWarps = 4;         // streams per block
+constexpr int kPolicyWarps = 8;         // streams per block
 constexpr int kPolicyMaxObs = 8 + 4 * 64;  // MMFull at obs_depth 64 (observations.hpp:69-76)
 constexpr int kPolicyMaxHidden = 512;   // make_policy_net cap (net.hpp:86-87)
 constexpr int kPolicyMaxActions = 32;   // largest action arity (spread-skew table rows)
