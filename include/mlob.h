@@ -489,10 +489,12 @@ typedef struct mlob_policy {
   double kappa;
   double sigma;
   double horizon;
+  const struct mlob_policy_net* net; /* Learned: argmax of the GRU policy (evaluate.hpp:80-90) */
 } mlob_policy;
 void mlob_default_policy(int kind, mlob_policy* out);
 
-/* Scripted actions for the next steps (evaluate.hpp:56-99 choose_action,
+/* Scripted actions for the next steps (evaluate.hpp:56-99 choose_action; Learned
+ * options only through mlob_evaluate_matrix),
  * twap.hpp:37-58, avst.hpp:19-32): env e's agents of type t act by
  * policies[env_policy[e * n_types + t]] from the env's own state on the
  * device; Random draws CounterRng(make_key(env seed, EpisodeDraw, env_cell[e],
@@ -522,8 +524,10 @@ typedef struct mlob_cell_stats {
  * device batch (env seed = `seed`, env index 0, as the reference's one
  * MarketEnv), stepped to the episode end; the per-cell statistics are then
  * formed on the host in the reference's order.  out[n_rows * n_cols],
- * row-major.  Errors: invalid_argument as the reference (two types, episodes
- * non-empty); a Learned option -> MLOB_E_INVALID_ARGUMENT. */
+ * row-major.  Learned options run their network on the device each step
+ * (hidden state zeroed at the episode start, argmax action).  Errors:
+ * invalid_argument as the reference (two types, episodes non-empty, a
+ * Learned option without a network or with the wrong shape). */
 mlob_status mlob_evaluate_matrix(const mlob_store* store, const mlob_env_config* cfg,
                                  const uint64_t* episodes, uint64_t n_episodes,
                                  const mlob_policy* type0, int n_type0, const mlob_policy* type1,

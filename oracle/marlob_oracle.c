@@ -1716,6 +1716,10 @@ int orc_choose_action(void* e, int a, const mlob_policy* p, int step, uint64_t s
   return choose_action((const env*)e, a, p, step, seed, cell_id, episode, out);
 }
 
+static void policy_forward(const mlob_policy_net* net, const double* obs, const double* hidden,
+                           const uint8_t* reset_mask, uint64_t batch, double* logits, double* values,
+                           double* hidden_out);
+
 static void mean_stderr(const double* xs, uint64_t n, double* mean, double* se) { /* evaluate.hpp:188-197 */
   const double k = (double)n;
   double m = 0.0;
@@ -1734,9 +1738,12 @@ int orc_evaluate_matrix(void* store_, const mlob_env_config* cfg, const uint64_t
     return fail(MLOB_E_INVALID_ARGUMENT, "evaluate_matrix: exactly two agent types required");
   if (n_eps == 0) return fail(MLOB_E_INVALID_ARGUMENT, "evaluate_matrix: empty episode set");
   for (int i = 0; i < n0 + n1; ++i)
-    if ((i < n0 ? t0[i] : t1[i - n0]).kind == MLOB_POLICY_LEARNED)
+    if ((i < n0 ? t0[i] : t1[i - n0]).kind == MLOB_POLICY_LEARNED && !(i < n0 ? t0[i] : t1[i - n0]).net)
       return fail(MLOB_E_INVALID_ARGUMENT, "evaluate_matrix: learned policy without a network");
   int status = MLOB_OK;
+  double* hidden[MLOB_MAX_AGENTS] = {0};
+  double* hidden_scratch[MLOB_MAX_AGENTS] = {0};
+  double logits[64];
   env* e = orc_env_create(store_, cfg, seed, 0, &status);
   if (!e) return status;
   const int A = e->n_agents;
@@ -1752,9 +1759,33 @@ int orc_evaluate_matrix(void* store_, const mlob_env_config* cfg, const uint64_t
       for (uint64_t k = 0; k < n_eps && status == MLOB_OK; ++k) {
         const uint64_t ep = episodes[k];
         if ((status = orc_env_reset(e, ep)) != MLOB_OK) break;
+        for (int a = 0; a < A; ++a) { /* evaluate.hpp:151-154: hidden zeroed per episode */
+          const mlob_policy* p = choice[e->flat_spec[a]];
+          if (p->kind != MLOB_POLICY_LEARNED) continue;
+          free(hidden[a]);
+          free(hidden_scratch[a]);
+          hidden[a] = calloc((size_t)p->net->hidden, 8);
+          hidden_scratch[a] = calloc((size_t)p->net->hidden, 8);
+        }
         for (int step = 0; !e->terminal && status == MLOB_OK; ++step) {
-          for (int a = 0; a < A && status == MLOB_OK; ++a)
-            status = choose_action(e, a, choice[e->flat_spec[a]], step, seed, cell_id, ep, &acts[a]);
+          for (int a = 0; a < A && status == MLOB_OK; ++a) {
+            const mlob_policy* p = choice[e->flat_spec[a]];
+            if (p->kind == MLOB_POLICY_LEARNED) { /* evaluate.hpp:80-90 */
+              const uint8_t reset = 0;
+              double value = 0.0;
+              memset(&acts[a], 0, sizeof acts[a]);
+              policy_forward(p->net, e->ag[a].obs, hidden[a], &reset, 1, logits, &value, hidden_scratch[a]);
+              double* tmp = hidden[a];
+              hidden[a] = hidden_scratch[a];
+              hidden_scratch[a] = tmp;
+              int best = 0; /* argmax_action, ppo.hpp:100-105 */
+              for (int i = 1; i < p->net->n_actions; ++i)
+                if (logits[i] > logits[best]) best = i;
+              acts[a].id = best;
+              continue;
+            }
+            status = choose_action(e, a, p, step, seed, cell_id, ep, &acts[a]);
+          }
           if (status == MLOB_OK) status = orc_env_step(e, acts, (uint64_t)A);
         }
         if (status != MLOB_OK) break;
@@ -1794,6 +1825,10 @@ int orc_evaluate_matrix(void* store_, const mlob_env_config* cfg, const uint64_t
   for (int tau = 0; tau < 2; ++tau) {
     free(pv[tau]);
     free(slip[tau]);
+  }
+  for (int a = 0; a < MLOB_MAX_AGENTS; ++a) {
+    free(hidden[a]);
+    free(hidden_scratch[a]);
   }
   orc_env_free(e);
   return status;

@@ -556,8 +556,17 @@ int ref_evaluate_matrix(void* store, const mlob_env_config* cfg, const uint64_t*
       return c;
     };
     std::vector<ippo::PolicyChoice> o0, o1;
-    for (int i = 0; i < n0; ++i) o0.push_back(to_choice(t0[i]));
-    for (int i = 0; i < n1; ++i) o1.push_back(to_choice(t1[i]));
+    std::vector<std::unique_ptr<ippo::PolicyNet>> owned;  // PolicyChoice::net is non-owning
+    const auto with_net = [&](const mlob_policy& p) {
+      ippo::PolicyChoice c = to_choice(p);
+      if (p.kind == MLOB_POLICY_LEARNED && p.net) {
+        owned.push_back(std::make_unique<ippo::PolicyNet>(to_net(*p.net)));
+        c.net = owned.back().get();
+      }
+      return c;
+    };
+    for (int i = 0; i < n0; ++i) o0.push_back(with_net(t0[i]));
+    for (int i = 0; i < n1; ++i) o1.push_back(with_net(t1[i]));
     const env::EnvConfig c = to_cfg(*cfg);
     const data::MessageStore& st = static_cast<StoreH*>(store)->store;
     const data::EpisodeIndex index =

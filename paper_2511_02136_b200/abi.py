@@ -192,7 +192,8 @@ class NetParams:
 class Policy(C.Structure):
     """mlob_policy = ippo::PolicyChoice without the network (evaluate.hpp:19-25)."""
     _fields_ = [("kind", i32), ("twap_mode", i32), ("avst_gamma_index", i32), ("n_gamma", i32),
-                ("gamma_grid", f64 * MAX_GAMMA), ("kappa", f64), ("sigma", f64), ("horizon", f64)]
+                ("gamma_grid", f64 * MAX_GAMMA), ("kappa", f64), ("sigma", f64), ("horizon", f64),
+                ("net", C.POINTER(PolicyNetC))]
 
 
 class TypeCellStats(C.Structure):  # evaluate.hpp:27-35
@@ -207,10 +208,16 @@ class CellStats(C.Structure):  # evaluate.hpp:37-42 (labels omitted)
 
 def policy(kind: int, twap_mode: int = TWAP_AGGRESSIVE, gamma_index: int = 1,
            gamma_grid=(0.05, 0.1, 0.5, 1.0), kappa: float = 1.5, sigma: float = 2.0,
-           horizon: float = 64.0) -> Policy:
+           horizon: float = 64.0, net: "NetParams | None" = None) -> Policy:
     """A policy option with the reference defaults (AvStBaseline avst.hpp:14-17 over
-    AvStParams actions.hpp:142-147; TwapPriceMode::Aggressive evaluate.hpp:24)."""
+    AvStParams actions.hpp:142-147; TwapPriceMode::Aggressive evaluate.hpp:24);
+    `net` = the network of a POLICY_LEARNED option (kept alive by the returned
+    object)."""
     p = Policy()
+    if net is not None:
+        p._net_c = net.to_c()
+        p._net_params = net
+        p.net = C.pointer(p._net_c)
     p.kind, p.twap_mode, p.avst_gamma_index = kind, twap_mode, gamma_index
     if len(gamma_grid) > MAX_GAMMA:
         raise ValueError(f"at most {MAX_GAMMA} gamma values")

@@ -51,12 +51,13 @@ __global__ void __launch_bounds__(kPolicyWarps * 32) policy_kernel(const PolicyA
   double* const sl = sn + H;
   const uint64_t e = s / pa.count, slot = e * pa.agents_per_env + pa.offset + s % pa.count;
   const uint64_t B = pa.B;
+  if (pa.argmax && pa.env_policy[e * pa.n_specs + pa.type] != pa.filter) return;
   // rewards / dones of the step just taken (row t - 1)
   if (pa.prev_row >= 0 && lane == 0) {
     pa.rewards[static_cast<uint64_t>(pa.prev_row) * B + s] = pa.env_rewards[slot];
     pa.dones[static_cast<uint64_t>(pa.prev_row) * B + s] = pa.env_dones[slot];
   }
-  const uint8_t reset = pa.just_reset[e];  // gather's reset flag (rollout.hpp:210)
+  const uint8_t reset = pa.just_reset ? pa.just_reset[e] : 0;  // gather's reset flag (rollout.hpp:210)
   const double* x = pa.obs_env + s * D;
   for (int d = lane; d < D; d += 32) {
     sx[d] = x[d];
@@ -105,6 +106,13 @@ __global__ void __launch_bounds__(kPolicyWarps * 32) policy_kernel(const PolicyA
   }
   __syncwarp();
   if (lane != 0) return;
+  if (pa.argmax) {  // argmax_action (ppo.hpp:100-105): first maximum
+    int best = 0;
+    for (int a = 1; a < A; ++a)
+      if (sl[a] > sl[best]) best = a;
+    pa.env_actions[slot] = best;
+    return;
+  }
   double v = nt.b_critic;  // critic head, net.hpp:180-182
   for (int j = 0; j < H; ++j) v += nt.w_critic[j] * sn[j];
   pa.values[static_cast<uint64_t>(pa.row) * B + s] = v;

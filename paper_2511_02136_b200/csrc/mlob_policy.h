@@ -37,11 +37,14 @@ struct PolicyArgs {
   int32_t row;                // batch row written (t, or T for the bootstrap value)
   int32_t prev_row;           // row whose rewards / dones are filed (-1: none)
   int32_t sample;             // 1: draw an action (rollout step); 0: value only (bootstrap)
-  int32_t _pad;
+  int32_t argmax;             // 1: argmax_action into env_actions only (evaluate.hpp:80-90)
+  // argmax mode: only envs whose type-`type` policy index equals `filter`
+  const uint8_t* env_policy;  // [env * n_specs + type]
+  int32_t n_specs, filter;
   uint64_t seed, update_index;
   // env side
   const double* obs_env;      // the type's observation buffer, [s * D]
-  const uint8_t* just_reset;  // [env]
+  const uint8_t* just_reset;  // [env]; null = no reset (evaluate.hpp:83)
   const double* env_rewards;  // [env * agents_per_env + a]
   const uint8_t* env_dones;
   int32_t* env_actions;       // the step kernel's action ids

@@ -121,6 +121,12 @@ struct mlob_venv {
     double* hidden[2] = {};
     int cur = 0;
   };
+  static void free_net(NetState& n) {
+    cudaFree(n.w);
+    cudaFree(n.hidden[0]);
+    cudaFree(n.hidden[1]);
+    n = NetState{};
+  }
   struct Batch {
     uint64_t T = 0, B = 0;
     char* arena = nullptr;
@@ -132,6 +138,7 @@ struct mlob_venv {
   NetState nets[MLOB_MAX_SPECS];
   Batch batch[MLOB_MAX_SPECS];
   bool has_nets = false;
+  std::vector<NetState> eval_nets;  // evaluate_matrix: one per Learned option
   std::vector<uint64_t> starts;
   std::vector<EpState> ep_state;
   std::vector<uint64_t> pool;  // empty = identity
@@ -188,11 +195,10 @@ struct mlob_venv {
       }
     for (cudaEvent_t e : io_events) cudaEventDestroy(e);
     for (int t = 0; t < MLOB_MAX_SPECS; ++t) {
-      cudaFree(nets[t].w);
-      cudaFree(nets[t].hidden[0]);
-      cudaFree(nets[t].hidden[1]);
+      free_net(nets[t]);
       cudaFree(batch[t].arena);
     }
+    for (NetState& n : eval_nets) free_net(n);
     for (void* p : allocs) cudaFree(p);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
@@ -913,75 +919,72 @@ mlob_status mlob_venv_infos(mlob_venv* v, mlob_agent_info* out) {
 
 // ---- on-device policy inference and rollouts -------------------------------
 
+static void check_net(const mlob_venv* v, int t, const mlob_policy_net& n) {
+  if (n.obs_dim != v->dcfg.specs[t].obs_dim || n.n_actions != v->dcfg.specs[t].arity)
+    fail(MLOB_E_INVALID_ARGUMENT, "policy net for type " + std::to_string(t) + ": expected obs_dim " +
+                                      std::to_string(v->dcfg.specs[t].obs_dim) + ", n_actions " +
+                                      std::to_string(v->dcfg.specs[t].arity));
+  if (n.hidden < 1 || n.hidden > kPolicyMaxHidden)
+    fail(MLOB_E_INVALID_ARGUMENT, "make_policy_net: hidden size capped at 512");
+  if (n.n_actions > kPolicyMaxActions || n.obs_dim > kPolicyMaxObs)
+    fail(MLOB_E_INVALID_ARGUMENT, "policy net: shape beyond the device limits");
+  if (!n.w_ih || !n.w_hh || !n.b_ih || !n.b_hh || !n.w_actor || !n.b_actor || !n.w_critic)
+    fail(MLOB_E_INVALID_ARGUMENT, "policy net: null weight array");
+}
+
+// Uploads `n` into `ns` (transposed layout, mlob_policy.h) with hidden buffers
+// for B streams; a shape change reallocates and zeroes the hidden state.
+static void upload_net(mlob_venv* v, const mlob_policy_net& n, mlob_venv::NetState& ns, uint64_t B) {
+  const size_t D = n.obs_dim, H = n.hidden, A = n.n_actions, H3 = 3 * H;
+  std::vector<double> w(H3 * D + H3 * H + 2 * H3 + A * H + A + H);
+  double* w_ihT = w.data();
+  for (size_t r = 0; r < H3; ++r)
+    for (size_t d = 0; d < D; ++d) w_ihT[d * H3 + r] = n.w_ih[r * D + d];
+  double* w_hhT = w_ihT + H3 * D;
+  for (size_t r = 0; r < H3; ++r)
+    for (size_t j = 0; j < H; ++j) w_hhT[j * H3 + r] = n.w_hh[r * H + j];
+  double* b_ih = w_hhT + H3 * H;
+  std::memcpy(b_ih, n.b_ih, H3 * 8);
+  double* b_hh = b_ih + H3;
+  std::memcpy(b_hh, n.b_hh, H3 * 8);
+  double* w_aT = b_hh + H3;
+  for (size_t a = 0; a < A; ++a)
+    for (size_t j = 0; j < H; ++j) w_aT[j * A + a] = n.w_actor[a * H + j];
+  double* b_a = w_aT + A * H;
+  std::memcpy(b_a, n.b_actor, A * 8);
+  double* w_c = b_a + A;
+  std::memcpy(w_c, n.w_critic, H * 8);
+  const bool same_shape = ns.w && ns.dn.D == n.obs_dim && ns.dn.H == n.hidden && ns.dn.A == n.n_actions;
+  if (!same_shape) {
+    mlob_venv::free_net(ns);
+    cuda_check(cudaMalloc(&ns.w, w.size() * 8), "cudaMalloc(net)");
+    cuda_check(cudaMalloc(&ns.hidden[0], std::max<uint64_t>(1, B * H) * 8), "cudaMalloc(hidden)");
+    cuda_check(cudaMalloc(&ns.hidden[1], std::max<uint64_t>(1, B * H) * 8), "cudaMalloc(hidden)");
+    cuda_check(cudaMemsetAsync(ns.hidden[0], 0, B * H * 8, v->stream), "memset");
+  }
+  cuda_check(cudaMemcpyAsync(ns.w, w.data(), w.size() * 8, cudaMemcpyHostToDevice, v->stream), "H2D");
+  const double* base = ns.w;
+  ns.dn.D = n.obs_dim;
+  ns.dn.H = n.hidden;
+  ns.dn.A = n.n_actions;
+  ns.dn.w_ihT = base;
+  ns.dn.w_hhT = base + (w_hhT - w.data());
+  ns.dn.b_ih = base + (b_ih - w.data());
+  ns.dn.b_hh = base + (b_hh - w.data());
+  ns.dn.w_actorT = base + (w_aT - w.data());
+  ns.dn.b_actor = base + (b_a - w.data());
+  ns.dn.w_critic = base + (w_c - w.data());
+  ns.dn.b_critic = n.b_critic;
+  cuda_check(cudaStreamSynchronize(v->stream), "sync");  // `w` is a host temporary
+}
+
 mlob_status mlob_venv_set_nets(mlob_venv* v, const mlob_policy_net* nets) {
   return guarded([&] {
     if (!nets) fail(MLOB_E_INVALID_ARGUMENT, "set_nets: null");
-    const int T = v->cfg.n_specs;
-    for (int t = 0; t < T; ++t) {  // shapes first: nothing changes on error
-      const mlob_policy_net& n = nets[t];
-      if (n.obs_dim != v->dcfg.specs[t].obs_dim || n.n_actions != v->dcfg.specs[t].arity)
-        fail(MLOB_E_INVALID_ARGUMENT, "set_nets: type " + std::to_string(t) + " expects obs_dim " +
-                                          std::to_string(v->dcfg.specs[t].obs_dim) + ", n_actions " +
-                                          std::to_string(v->dcfg.specs[t].arity));
-      if (n.hidden < 1 || n.hidden > kPolicyMaxHidden)
-        fail(MLOB_E_INVALID_ARGUMENT, "make_policy_net: hidden size capped at 512");
-      if (n.n_actions > kPolicyMaxActions || n.obs_dim > kPolicyMaxObs)
-        fail(MLOB_E_INVALID_ARGUMENT, "set_nets: network shape beyond the device limits");
-      if (!n.w_ih || !n.w_hh || !n.b_ih || !n.b_hh || !n.w_actor || !n.b_actor || !n.w_critic)
-        fail(MLOB_E_INVALID_ARGUMENT, "set_nets: null weight array");
-    }
+    for (int t = 0; t < v->cfg.n_specs; ++t) check_net(v, t, nets[t]);  // nothing changes on error
     v->set_device();
-    for (int t = 0; t < T; ++t) {
-      const mlob_policy_net& n = nets[t];
-      const size_t D = n.obs_dim, H = n.hidden, A = n.n_actions, H3 = 3 * H;
-      // transposed copies (mlob_policy.h), then the vectors as they are
-      std::vector<double> w(H3 * D + H3 * H + 2 * H3 + A * H + A + H);
-      double* p = w.data();
-      double* w_ihT = p;
-      for (size_t r = 0; r < H3; ++r)
-        for (size_t d = 0; d < D; ++d) w_ihT[d * H3 + r] = n.w_ih[r * D + d];
-      double* w_hhT = w_ihT + H3 * D;
-      for (size_t r = 0; r < H3; ++r)
-        for (size_t j = 0; j < H; ++j) w_hhT[j * H3 + r] = n.w_hh[r * H + j];
-      double* b_ih = w_hhT + H3 * H;
-      std::memcpy(b_ih, n.b_ih, H3 * 8);
-      double* b_hh = b_ih + H3;
-      std::memcpy(b_hh, n.b_hh, H3 * 8);
-      double* w_aT = b_hh + H3;
-      for (size_t a = 0; a < A; ++a)
-        for (size_t j = 0; j < H; ++j) w_aT[j * A + a] = n.w_actor[a * H + j];
-      double* b_a = w_aT + A * H;
-      std::memcpy(b_a, n.b_actor, A * 8);
-      double* w_c = b_a + A;
-      std::memcpy(w_c, n.w_critic, H * 8);
-      mlob_venv::NetState& ns = v->nets[t];
-      const uint64_t B = v->n_envs * static_cast<uint64_t>(v->cfg.specs[t].count);
-      const bool same_shape = ns.w && ns.dn.D == n.obs_dim && ns.dn.H == n.hidden && ns.dn.A == n.n_actions;
-      if (!same_shape) {
-        cudaFree(ns.w);
-        cudaFree(ns.hidden[0]);
-        cudaFree(ns.hidden[1]);
-        ns = mlob_venv::NetState{};
-        cuda_check(cudaMalloc(&ns.w, w.size() * 8), "cudaMalloc(net)");
-        cuda_check(cudaMalloc(&ns.hidden[0], std::max<uint64_t>(1, B * H) * 8), "cudaMalloc(hidden)");
-        cuda_check(cudaMalloc(&ns.hidden[1], std::max<uint64_t>(1, B * H) * 8), "cudaMalloc(hidden)");
-        cuda_check(cudaMemsetAsync(ns.hidden[0], 0, B * H * 8, v->stream), "memset");
-      }
-      cuda_check(cudaMemcpyAsync(ns.w, w.data(), w.size() * 8, cudaMemcpyHostToDevice, v->stream), "H2D");
-      const double* base = ns.w;
-      ns.dn.D = n.obs_dim;
-      ns.dn.H = n.hidden;
-      ns.dn.A = n.n_actions;
-      ns.dn.w_ihT = base;
-      ns.dn.w_hhT = base + (w_hhT - w.data());
-      ns.dn.b_ih = base + (b_ih - w.data());
-      ns.dn.b_hh = base + (b_hh - w.data());
-      ns.dn.w_actorT = base + (w_aT - w.data());
-      ns.dn.b_actor = base + (b_a - w.data());
-      ns.dn.w_critic = base + (w_c - w.data());
-      ns.dn.b_critic = n.b_critic;
-      cuda_check(cudaStreamSynchronize(v->stream), "sync");  // `w` is a host temporary
-    }
+    for (int t = 0; t < v->cfg.n_specs; ++t)
+      upload_net(v, nets[t], v->nets[t], v->n_envs * static_cast<uint64_t>(v->cfg.specs[t].count));
     v->has_nets = true;
   });
 }
@@ -1139,8 +1142,8 @@ void mlob_default_policy(int kind, mlob_policy* out) {
 static DevPolicy resolve_policy(const mlob_policy& p) {
   if (p.kind < MLOB_POLICY_LEARNED || p.kind > MLOB_POLICY_NOOP)
     fail(MLOB_E_INVALID_ARGUMENT, "policy: unknown kind " + std::to_string(p.kind));
-  if (p.kind == MLOB_POLICY_LEARNED)
-    fail(MLOB_E_INVALID_ARGUMENT, "policy: learned policies are not evaluated on the device");
+  if (p.kind == MLOB_POLICY_LEARNED && !p.net)
+    fail(MLOB_E_INVALID_ARGUMENT, "evaluate_matrix: learned policy without a network");
   if (p.kind == MLOB_POLICY_TWAP && p.twap_mode != MLOB_TWAP_AGGRESSIVE && p.twap_mode != MLOB_TWAP_PASSIVE)
     fail(MLOB_E_INVALID_ARGUMENT, "policy: twap_mode");
   DevPolicy d{};
@@ -1160,11 +1163,15 @@ static DevPolicy resolve_policy(const mlob_policy& p) {
 }
 
 static void set_policies(mlob_venv* v, const mlob_policy* policies, int n_policies, const uint8_t* env_policy,
-                         const uint64_t* env_cell) {
+                         const uint64_t* env_cell, bool learned_ok = false) {
   if (n_policies < 1 || n_policies > kMaxPolicies)
     fail(MLOB_E_INVALID_ARGUMENT, "set_policies: 1.." + std::to_string(kMaxPolicies) + " policies");
   std::vector<DevPolicy> dp(n_policies);
-  for (int i = 0; i < n_policies; ++i) dp[i] = resolve_policy(policies[i]);
+  for (int i = 0; i < n_policies; ++i) {
+    if (policies[i].kind == MLOB_POLICY_LEARNED && !learned_ok)
+      fail(MLOB_E_INVALID_ARGUMENT, "set_policies: learned policies run through mlob_evaluate_matrix");
+    dp[i] = resolve_policy(policies[i]);
+  }
   const uint64_t n = v->n_envs * static_cast<uint64_t>(v->cfg.n_specs);
   for (uint64_t i = 0; i < n; ++i)
     if (env_policy[i] >= n_policies) fail(MLOB_E_OUT_OF_RANGE, "set_policies: policy index out of range");
@@ -1197,7 +1204,8 @@ mlob_status mlob_evaluate_matrix(const mlob_store* store, const mlob_env_config*
     if (cfg->n_specs != 2) fail(MLOB_E_INVALID_ARGUMENT, "evaluate_matrix: exactly two agent types required");
     if (n_episodes == 0) fail(MLOB_E_INVALID_ARGUMENT, "evaluate_matrix: empty episode set");
     for (int i = 0; i < n_type0 + n_type1; ++i)
-      if ((i < n_type0 ? type0[i] : type1[i - n_type0]).kind == MLOB_POLICY_LEARNED)
+      if ((i < n_type0 ? type0[i] : type1[i - n_type0]).kind == MLOB_POLICY_LEARNED &&
+          !(i < n_type0 ? type0[i] : type1[i - n_type0]).net)
         fail(MLOB_E_INVALID_ARGUMENT, "evaluate_matrix: learned policy without a network");
     if (n_type0 <= 0 || n_type1 <= 0) return;
     if (n_type0 + n_type1 > kMaxPolicies)
@@ -1228,9 +1236,51 @@ mlob_status mlob_evaluate_matrix(const mlob_store* store, const mlob_env_config*
     const mlob_status st = mlob_venv_create(&d, &raw);
     if (st != MLOB_OK) fail(st, mlob_last_error());
     std::unique_ptr<mlob_venv> v(raw);
+    // Learned options: network + per-stream hidden state, zeroed at the episode
+    // start (evaluate.hpp:151-154); argmax ids are written before each step
+    struct Learned {
+      int option, type;
+    };
+    std::vector<Learned> learned;
+    for (int i = 0; i < static_cast<int>(table.size()); ++i)
+      if (table[i].kind == MLOB_POLICY_LEARNED) {
+        const int tau = i < n_type0 ? 0 : 1;
+        check_net(v.get(), tau, *table[i].net);
+        learned.push_back({i, tau});
+      }
+    v->eval_nets.resize(learned.size());
+    for (size_t k = 0; k < learned.size(); ++k)
+      upload_net(v.get(), *table[learned[k].option].net, v->eval_nets[k],
+                 n * static_cast<uint64_t>(cfg->specs[learned[k].type].count));
     do_reset(v.get(), eps);
-    set_policies(v.get(), table.data(), static_cast<int>(table.size()), pol.data(), cell.data());
-    for (int t = 0; t < cfg->steps_per_episode; ++t) do_step(v.get(), kActScripted, 0, 0);
+    set_policies(v.get(), table.data(), static_cast<int>(table.size()), pol.data(), cell.data(), true);
+    for (int t = 0; t < cfg->steps_per_episode; ++t) {
+      for (size_t k = 0; k < learned.size(); ++k) {
+        mlob_venv::NetState& ns = v->eval_nets[k];
+        const int tau = learned[k].type;
+        PolicyArgs pa{};
+        pa.net = ns.dn;
+        pa.B = n * static_cast<uint64_t>(cfg->specs[tau].count);
+        pa.count = cfg->specs[tau].count;
+        pa.offset = v->dcfg.specs[tau].flat_offset;
+        pa.agents_per_env = v->A;
+        pa.type = tau;
+        pa.argmax = 1;
+        pa.prev_row = -1;
+        pa.env_policy = v->d_env_policy;
+        pa.n_specs = cfg->n_specs;
+        pa.filter = learned[k].option;
+        pa.obs_env = v->d_obs[tau];
+        pa.just_reset = nullptr;  // choose_action passes reset = 0 (evaluate.hpp:83)
+        pa.env_actions = v->d_actions;
+        pa.hidden_in = ns.hidden[ns.cur];
+        pa.hidden_out = ns.hidden[ns.cur ^ 1];
+        cuda_check(launch_policy(pa, v->stream), "policy kernel");
+        ++v->launches;
+        ns.cur ^= 1;
+      }
+      do_step(v.get(), kActScripted, 0, 0);
+    }
     const int A = v->A;
     std::vector<mlob_agent_info> info(n * A);
     std::vector<AgentRec> ag(n * A);

@@ -1026,7 +1026,7 @@ struct WarpEnv {
     q.p0 = q.p1 = q.q0 = q.q1 = 0;
     const DevPolicy* pol =
         kp.action_mode == kActScripted ? &kp.policies[kp.env_policy[env * cfg.n_specs + cfg.flat_spec[a]]] : nullptr;
-    const bool direct = pol ? pol->kind != MLOB_POLICY_RANDOM
+    const bool direct = pol ? pol->kind != MLOB_POLICY_RANDOM && pol->kind != MLOB_POLICY_LEARNED
                             : kp.action_mode == kActDirect && kp.action_direct[env * cfg.n_agents + a].direct;
     if (direct) {  // env.hpp:290-298
       if (pol) {
@@ -1053,6 +1053,8 @@ struct WarpEnv {
                        kp.global_step)};
         for (int b = 0; b < a; ++b) r.next();
         id = static_cast<int>(r.below(static_cast<uint64_t>(sp.arity)));
+      } else if (pol && pol->kind == MLOB_POLICY_LEARNED) {  // argmax id from the policy kernel
+        id = kp.action_ids[env * cfg.n_agents + a];
       } else if (pol) {  // PolicyKind::Random, evaluate.hpp:74-79
         uint64_t h = key_fold(key_fold(splitmix64(seed), kRngEpisodeDraw), kp.env_cell ? kp.env_cell[env] : 0);
         h = key_fold(key_fold(key_fold(h, episode), static_cast<uint64_t>(step)), static_cast<uint64_t>(a));

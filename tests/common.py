@@ -136,3 +136,14 @@ def rollout_case(o):
             o.make_policy_net(A.observation_size(cfg.specs[1].obs_space, cfg.obs_depth), 32,
                               A.action_arity(cfg.specs[1]), 12)]
     return cfg, {"state_sample_every": 20}, nets
+
+
+def crossplay_learned_case(o):
+    """crossplay_case plus Learned options (GRU nets from `o`'s make_policy_net)."""
+    A = abi
+    cfg, synth_kw, eps, t0, t1 = crossplay_case()
+    nets = [o.make_policy_net(A.observation_size(cfg.specs[t].obs_space, cfg.obs_depth), h,
+                              A.action_arity(cfg.specs[t]), 40 + t) for t, h in ((0, 16), (1, 32))]
+    t0 = [A.policy(A.POLICY_LEARNED, net=nets[0]), t0[1], t0[3]]
+    t1 = [t1[0], A.policy(A.POLICY_LEARNED, net=nets[1]), t1[2]]
+    return cfg, synth_kw, eps, t0, t1

@@ -388,3 +388,17 @@ def test_collect_rollout_matches_oracle(orc):
     bad = [nets[1], nets[0]]                 # shapes swapped
     with pytest.raises(ValueError):
         g.set_nets(bad)
+
+
+def test_evaluate_matrix_learned_matches_oracle(orc):
+    """Learned cross-play options on the device (policy kernel in argmax mode per
+    option, then the scripted step) against the oracle's evaluate_matrix."""
+    from paper_2511_02136_b200.env import evaluate_matrix
+    from tests.common import crossplay_learned_case
+    cfg, synth_kw, eps, t0, t1 = crossplay_learned_case(orc)
+    got = evaluate_matrix(dev_store(synth_kw), cfg, eps, t0, t1, 5)
+    want = orc.evaluate(small_store(orc, synth_kw), cfg, eps, t0, t1, 5)
+    assert [bytes(x) for x in got] == [bytes(x) for x in want]
+    wrong = abi.policy(abi.POLICY_LEARNED, net=orc.make_policy_net(3, 8, 4, 0))
+    with pytest.raises(ValueError):
+        evaluate_matrix(dev_store(synth_kw), cfg, eps, [wrong], t1, 5)

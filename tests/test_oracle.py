@@ -330,3 +330,13 @@ def test_collect_rollout_matches_reference(orc, ref):
     assert got["orc"] == got["ref"]
     with pytest.raises(ValueError):  # net.hpp:86-87
         orc.make_policy_net(8, 513, 8, 0)
+
+
+def test_evaluate_matrix_learned_matches_reference(orc, ref):
+    """Learned options (evaluate.hpp:80-90: policy_forward + argmax, hidden zeroed
+    per episode) in the cross-play grid: C restatement vs the reference."""
+    from tests.common import crossplay_learned_case
+    cfg, synth_kw, eps, t0, t1 = crossplay_learned_case(orc)
+    a = orc.evaluate(small_store(orc, synth_kw), cfg, eps, t0, t1, 5)
+    b = ref.evaluate(small_store(ref, synth_kw), cfg, eps, t0, t1, 5)
+    assert [bytes(x) for x in a] == [bytes(x) for x in b]
