@@ -322,6 +322,24 @@ uint64_t mlob_store_n_messages(const mlob_store* s);
 uint64_t mlob_store_device_bytes(const mlob_store* s);
 void mlob_store_free(mlob_store* s);
 
+/* data::load_lobster (data/lobster.hpp:119-193) straight into a device store:
+ * the message / orderbook CSV pair is read once and parsed on the GPU (one
+ * thread per row; sampled orderbook rows -> book states at offsets 0,
+ * sample_every, 2*sample_every, ...).  Same acceptance rules and error texts
+ * as the reference (first failing row wins); invalid_argument for
+ * units_per_tick < 1 / sample_every == 0, runtime_error for file and format
+ * errors, invalid_argument when a value exceeds the device int32 layout. */
+mlob_status mlob_store_load_lobster(const char* message_path, const char* orderbook_path,
+                                    int64_t units_per_tick, uint64_t sample_every, int device,
+                                    mlob_store** out);
+/* Readback of a device store (parity checks): messages widened to the
+ * reference record (price / quantity as the device keeps them: zero for
+ * kinds that do not use them), and book states. */
+mlob_status mlob_store_read_messages(const mlob_store* s, uint64_t first, uint64_t n, mlob_message* out);
+uint64_t mlob_store_n_states(const mlob_store* s);
+mlob_status mlob_store_state(const mlob_store* s, uint64_t i, uint64_t* message_index, mlob_level* bids,
+                             uint32_t* n_bids, mlob_level* asks, uint32_t* n_asks, uint32_t cap);
+
 /* ---- Batched environment (ippo::MarketVecEnv + env::MarketEnv) ----------- */
 
 typedef struct mlob_venv mlob_venv;

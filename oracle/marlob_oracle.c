@@ -2084,3 +2084,259 @@ uint64_t orc_venv_rollout_field(void* v_, int type, int field, void* out, uint64
   if (src && bytes <= cap) memcpy(out, src, bytes);
   return bytes;
 }
+
+/* ------------------------------------------------------------------------ */
+/* data/lobster.hpp load_lobster                                              */
+
+typedef struct linebuf { /* std::getline over a whole file */
+  char* data;
+  size_t size, pos;
+} linebuf;
+
+static int lb_open(linebuf* b, const char* path) {
+  FILE* f = fopen(path, "rb");
+  if (!f) return 0;
+  fseek(f, 0, SEEK_END);
+  const long n = ftell(f);
+  fseek(f, 0, SEEK_SET);
+  b->size = n > 0 ? (size_t)n : 0;
+  b->data = malloc(b->size + 1);
+  b->pos = 0;
+  if (b->size && fread(b->data, 1, b->size, f) != b->size) {
+    fclose(f);
+    free(b->data);
+    return 0;
+  }
+  fclose(f);
+  return 1;
+}
+
+/* next line [*s, *s + *n) without '\n'; 0 at EOF (getline semantics) */
+static int lb_next(linebuf* b, const char** s, size_t* n) {
+  if (b->pos >= b->size) return 0;
+  const char* p = b->data + b->pos;
+  const char* nl = memchr(p, '\n', b->size - b->pos);
+  const size_t len = nl ? (size_t)(nl - p) : b->size - b->pos;
+  b->pos += len + (nl ? 1 : 0);
+  *s = p;
+  *n = len;
+  return 1;
+}
+
+static void strip_cr(const char* s, size_t* n) { /* lobster.hpp:72-75 */
+  if (*n > 0 && s[*n - 1] == '\r') --*n;
+}
+
+/* lobster.hpp:26-37: std::from_chars after leading blanks, whole field */
+static int lob_parse_int(const char* s, size_t n, int64_t* out) {
+  size_t i = 0;
+  while (i < n && (s[i] == ' ' || s[i] == '\t')) ++i;
+  int neg = 0;
+  if (i < n && s[i] == '-') {
+    neg = 1;
+    ++i;
+  }
+  if (i >= n) return 0;
+  uint64_t mag = 0;
+  const uint64_t lim = neg ? (1ull << 63) : (1ull << 63) - 1;
+  for (; i < n; ++i) {
+    if (s[i] < '0' || s[i] > '9') return 0;
+    const uint64_t d = (uint64_t)(s[i] - '0');
+    if (mag > (lim - d) / 10) return 0;
+    mag = mag * 10 + d;
+  }
+  *out = neg ? (int64_t)(0 - mag) : (int64_t)mag;
+  return 1;
+}
+
+#define LOB_FIELD(buf, s, n) snprintf(buf, sizeof buf, "%.*s", (int)(n), s)
+
+static int lob_int(const char* s, size_t n, const char* what, uint64_t row, int64_t* out) {
+  if (lob_parse_int(s, n, out)) return MLOB_OK;
+  char f[512];
+  LOB_FIELD(f, s, n);
+  return fail(MLOB_E_RUNTIME, "lobster: row %llu: malformed %s field '%s'", (unsigned long long)(row + 1), what, f);
+}
+
+static int lob_time(const char* s, size_t n, uint64_t row, int64_t* t) { /* lobster.hpp:41-57 */
+  const char* dot = memchr(s, '.', n);
+  const size_t sec_n = dot ? (size_t)(dot - s) : n;
+  int64_t sec = 0, frac = 0;
+  int rc = lob_int(s, sec_n, "time", row, &sec);
+  if (rc != MLOB_OK) return rc;
+  if (dot) {
+    size_t digits = n - sec_n - 1;
+    if (digits > 9) digits = 9;
+    if (digits == 0)
+      return fail(MLOB_E_RUNTIME, "lobster: row %llu: malformed time field", (unsigned long long)(row + 1));
+    rc = lob_int(dot + 1, digits, "time fraction", row, &frac);
+    if (rc != MLOB_OK) return rc;
+    for (size_t i = digits; i < 9; ++i) frac *= 10;
+  }
+  *t = (int64_t)((uint64_t)sec * 1000000000ull + (uint64_t)frac);
+  return MLOB_OK;
+}
+
+static int lob_ticks(int64_t units, int64_t upt, uint64_t row, int64_t* out) { /* lobster.hpp:77-84 */
+  if (units % upt != 0)
+    return fail(MLOB_E_RUNTIME, "lobster: row %llu: price %lld not divisible by tick size %lld",
+                (unsigned long long)(row + 1), (long long)units, (long long)upt);
+  *out = units / upt;
+  return MLOB_OK;
+}
+
+/* split on ',' (lobster.hpp:59-70): up to cap fields, returns the count */
+static size_t lob_split(const char* s, size_t n, const char** fs, size_t* fn, size_t cap) {
+  size_t k = 0, b = 0;
+  for (size_t i = 0; i <= n; ++i)
+    if (i == n || s[i] == ',') {
+      if (k < cap) {
+        fs[k] = s + b;
+        fn[k] = i - b;
+      }
+      ++k;
+      b = i + 1;
+    }
+  return k;
+}
+
+static int lob_book_row(const char* s, size_t n, int64_t upt, uint64_t row, mlob_level** bids, uint32_t* nb,
+                        mlob_level** asks, uint32_t* na) { /* lobster.hpp:86-103 */
+  const size_t nf = lob_split(s, n, NULL, NULL, 0);
+  if (nf % 4 != 0)
+    return fail(MLOB_E_RUNTIME, "lobster: orderbook row %llu: column count %zu is not a multiple of 4",
+                (unsigned long long)(row + 1), nf);
+  const char** fs = malloc(nf * sizeof(char*));
+  size_t* fn = malloc(nf * sizeof(size_t));
+  lob_split(s, n, fs, fn, nf);
+  *bids = malloc((nf / 4 + 1) * sizeof(mlob_level));
+  *asks = malloc((nf / 4 + 1) * sizeof(mlob_level));
+  *nb = *na = 0;
+  static const char* names[4] = {"ask price", "ask size", "bid price", "bid size"};
+  int rc = MLOB_OK;
+  for (size_t level = 0; level * 4 < nf && rc == MLOB_OK; ++level) {
+    int64_t v[4];
+    for (int c = 0; c < 4 && rc == MLOB_OK; ++c) rc = lob_int(fs[level * 4 + c], fn[level * 4 + c], names[c], row, &v[c]);
+    if (rc != MLOB_OK) break;
+    if (v[1] > 0 && v[0] > 0 && v[0] < 9999999999ll) {
+      int64_t p = 0;
+      if ((rc = lob_ticks(v[0], upt, row, &p)) != MLOB_OK) break;
+      (*asks)[(*na)++] = (mlob_level){p, v[1]};
+    }
+    if (v[3] > 0 && v[2] > 0) {
+      int64_t p = 0;
+      if ((rc = lob_ticks(v[2], upt, row, &p)) != MLOB_OK) break;
+      (*bids)[(*nb)++] = (mlob_level){p, v[3]};
+    }
+  }
+  free(fs);
+  free(fn);
+  return rc;
+}
+
+void* orc_load_lobster(const char* msg_path, const char* book_path, int64_t upt, uint64_t sample_every,
+                       int* status) { /* lobster.hpp:119-193 */
+  if (upt < 1) {
+    *status = fail(MLOB_E_INVALID_ARGUMENT, "load_lobster: units_per_tick >= 1");
+    return NULL;
+  }
+  if (sample_every == 0) {
+    *status = fail(MLOB_E_INVALID_ARGUMENT, "load_lobster: sample_every >= 1");
+    return NULL;
+  }
+  linebuf mf, bf;
+  if (!lb_open(&mf, msg_path)) {
+    *status = fail(MLOB_E_RUNTIME, "load_lobster: cannot open %s", msg_path);
+    return NULL;
+  }
+  if (!lb_open(&bf, book_path)) {
+    free(mf.data);
+    *status = fail(MLOB_E_RUNTIME, "load_lobster: cannot open %s", book_path);
+    return NULL;
+  }
+  store* st = calloc(1, sizeof(store));
+  push_state(st, 0, NULL, 0, NULL, 0);
+  int rc = MLOB_OK;
+  uint64_t row = 0;
+  int64_t prev_time = -1;
+  const char *ml, *bl;
+  size_t mn, bn;
+  static const int kinds[7] = {MLOB_NEW_LIMIT, MLOB_CANCEL_PARTIAL, MLOB_DELETE, MLOB_EXECUTE_VISIBLE,
+                               MLOB_EXECUTE_HIDDEN, MLOB_CROSS, MLOB_HALT};
+  while (rc == MLOB_OK && lb_next(&mf, &ml, &mn)) {
+    strip_cr(ml, &mn);
+    if (mn == 0) continue;
+    if (!lb_next(&bf, &bl, &bn)) {
+      rc = fail(MLOB_E_RUNTIME, "load_lobster: orderbook file has fewer rows than %s", msg_path);
+      break;
+    }
+    const char* fs[6];
+    size_t fn[6];
+    const size_t nf = lob_split(ml, mn, fs, fn, 6);
+    if (nf != 6) {
+      rc = fail(MLOB_E_RUNTIME, "lobster: row %llu: expected 6 fields, got %zu", (unsigned long long)(row + 1), nf);
+      break;
+    }
+    mlob_message m;
+    memset(&m, 0, sizeof m);
+    if ((rc = lob_time(fs[0], fn[0], row, &m.time)) != MLOB_OK) break;
+    if (m.time < prev_time) {
+      rc = fail(MLOB_E_RUNTIME, "lobster: row %llu: non-monotone time", (unsigned long long)(row + 1));
+      break;
+    }
+    prev_time = m.time;
+    int64_t type, id, dir, pu;
+    if ((rc = lob_int(fs[1], fn[1], "type", row, &type)) != MLOB_OK) break;
+    if (type < 1 || type > 7) {
+      rc = fail(MLOB_E_RUNTIME, "lobster: row %llu: unknown event type %lld", (unsigned long long)(row + 1),
+                (long long)type);
+      break;
+    }
+    m.kind = (uint8_t)kinds[type - 1];
+    if ((rc = lob_int(fs[2], fn[2], "order id", row, &id)) != MLOB_OK) break;
+    m.order_id = (uint64_t)id;
+    if ((rc = lob_int(fs[3], fn[3], "size", row, &m.quantity)) != MLOB_OK) break;
+    if (m.quantity < 0) {
+      rc = fail(MLOB_E_RUNTIME, "lobster: row %llu: negative size", (unsigned long long)(row + 1));
+      break;
+    }
+    if ((rc = lob_int(fs[4], fn[4], "price", row, &pu)) != MLOB_OK) break;
+    if ((rc = lob_ticks(pu, upt, row, &m.price)) != MLOB_OK) break;
+    if ((rc = lob_int(fs[5], fn[5], "direction", row, &dir)) != MLOB_OK) break;
+    if (dir != 1 && dir != -1) {
+      rc = fail(MLOB_E_RUNTIME, "lobster: row %llu: direction must be +1 or -1", (unsigned long long)(row + 1));
+      break;
+    }
+    m.side = dir == 1 ? MLOB_BID : MLOB_ASK;
+    m.trader_id = 0;
+    VEC_PUSH(st->msgs, m);
+    if ((row + 1) % sample_every == 0) {
+      strip_cr(bl, &bn);
+      mlob_level *b = NULL, *a = NULL;
+      uint32_t nb = 0, na = 0;
+      rc = lob_book_row(bl, bn, upt, row, &b, &nb, &a, &na);
+      if (rc == MLOB_OK) push_state(st, row + 1, b, nb, a, na);
+      free(b);
+      free(a);
+      if (rc != MLOB_OK) break;
+    }
+    ++row;
+  }
+  while (rc == MLOB_OK && lb_next(&bf, &bl, &bn)) {
+    strip_cr(bl, &bn);
+    if (bn != 0) rc = fail(MLOB_E_RUNTIME, "load_lobster: message file has fewer rows than %s", book_path);
+  }
+  free(mf.data);
+  free(bf.data);
+  if (rc != MLOB_OK) {
+    orc_store_free(st);
+    *status = rc;
+    return NULL;
+  }
+  if (st->states.n > 1 && st->states.v[st->states.n - 1].message_index == st->msgs.n) {
+    free(st->states.v[st->states.n - 1].levels);
+    --st->states.n;
+  }
+  *status = MLOB_OK;
+  return st;
+}

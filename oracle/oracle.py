@@ -71,6 +71,7 @@ _SIG = {
     "store_state": (C.c_int, [C.c_void_p, C.c_uint64, _P(C.c_uint64), _P(Level), _P(C.c_uint32),
                               _P(Level), _P(C.c_uint32), C.c_uint32]),
     "store_free": (None, [C.c_void_p]),
+    "load_lobster": (C.c_void_p, [C.c_char_p, C.c_char_p, C.c_int64, C.c_uint64, _P(C.c_int)]),
     "book_create": (C.c_void_p, [C.c_uint64]),
     "book_init_from_l2": (C.c_int, [C.c_void_p, _P(Level), C.c_uint32, _P(Level), C.c_uint32,
                                     C.c_uint64]),
@@ -189,6 +190,15 @@ class Oracle:
         h = self.store_synth(C.byref(cfg), seed)
         if not h:
             raise ValueError(self.last_error().decode())
+        return OStore(self, h)
+
+    def lobster(self, message_path: str, orderbook_path: str, units_per_tick: int,
+                sample_every: int) -> "OStore":
+        """data::load_lobster (lobster.hpp:119-193)."""
+        st = C.c_int()
+        h = self.load_lobster(str(message_path).encode(), str(orderbook_path).encode(), units_per_tick,
+                              sample_every, C.byref(st))
+        self.check(st.value)
         return OStore(self, h)
 
     def store_from(self, msgs: np.ndarray, states=None) -> "OStore":

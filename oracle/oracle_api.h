@@ -44,6 +44,9 @@ typedef struct orc_bench_row {
   int P##store_state(void* s, uint64_t i, uint64_t* msg_index, mlob_level* bids,              \
                      uint32_t* nb, mlob_level* asks, uint32_t* na, uint32_t cap);              \
   void P##store_free(void* s);                                                                 \
+  /* data/lobster.hpp load_lobster */                                                          \
+  void* P##load_lobster(const char* message_path, const char* orderbook_path,                  \
+                        int64_t units_per_tick, uint64_t sample_every, int* status);           \
   /* book (lob/book.hpp) */                                                                    \
   void* P##book_create(uint64_t capacity);                                                     \
   int P##book_init_from_l2(void* b, const mlob_level* bids, uint32_t nb,                      \

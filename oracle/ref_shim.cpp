@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "marlob/bench/bench.hpp"
+#include "marlob/data/lobster.hpp"
 #include "marlob/data/store.hpp"
 #include "marlob/data/synth.hpp"
 #include "marlob/env/env.hpp"
@@ -454,6 +455,20 @@ void* ref_venv_instance(void* v, uint64_t e) {
   return h;
 }
 void ref_venv_free(void* v) { delete static_cast<VenvH*>(v); }
+
+// ---- LOBSTER ingestion (data/lobster.hpp) ----
+void* ref_load_lobster(const char* message_path, const char* orderbook_path, int64_t units_per_tick,
+                       uint64_t sample_every, int* status) {
+  auto* h = new StoreH;
+  *status = guarded([&] {
+    h->store = data::load_lobster(message_path, orderbook_path, units_per_tick, sample_every);
+  });
+  if (*status != MLOB_OK) {
+    delete h;
+    return nullptr;
+  }
+  return h;
+}
 
 // ---- networks and rollouts (ippo/net.hpp, ippo/rollout.hpp) ----
 int ref_make_policy_net(int obs_dim, int hidden, int n_actions, uint64_t seed, double* out) {

@@ -14,6 +14,7 @@
 
 #include "mlob_dev.h"
 #include "mlob_host.h"
+#include "mlob_lobster.h"
 #include "mlob_policy.h"
 
 namespace mlob {
@@ -545,6 +546,76 @@ mlob_status mlob_store_upload_raw(const mlob_message* msgs, uint64_t n, const ml
   r = upload(msgs, n, hs, device, out);
   delete hs;
   return r;
+}
+
+mlob_status mlob_store_load_lobster(const char* message_path, const char* orderbook_path, int64_t units_per_tick,
+                                    uint64_t sample_every, int device, mlob_store** out) {
+  *out = nullptr;
+  return guarded([&] {
+    if (!message_path || !orderbook_path) fail(MLOB_E_INVALID_ARGUMENT, "load_lobster: null path");
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    cudaStream_t st = nullptr;
+    cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+    lobster::LobsterStore ls;
+    try {
+      lobster::load(message_path, orderbook_path, units_per_tick, sample_every, st, ls);
+    } catch (const lobster::LobsterError& e) {
+      cudaStreamDestroy(st);
+      fail(static_cast<mlob_status>(e.status), e.what());
+    }
+    cudaStreamDestroy(st);
+    auto s = std::make_unique<mlob_store>();
+    s->device = device;
+    s->n_msgs = ls.n_msgs;
+    s->d_msgs = ls.d_msgs;
+    s->d_levels = ls.d_levels;
+    s->st_index = std::move(ls.st_index);
+    s->st_offset = std::move(ls.st_offset);
+    s->st_nb = std::move(ls.st_nb);
+    s->bytes = ls.n_msgs * sizeof(DevMsg) + ls.n_levels * sizeof(DevLevel);
+    *out = s.release();
+  });
+}
+
+mlob_status mlob_store_read_messages(const mlob_store* s, uint64_t first, uint64_t n, mlob_message* out) {
+  return guarded([&] {
+    if (first > s->n_msgs || n > s->n_msgs - first) fail(MLOB_E_OUT_OF_RANGE, "read_messages: range");
+    cuda_check(cudaSetDevice(s->device), "cudaSetDevice");
+    std::vector<DevMsg> d(n);
+    if (n) cuda_check(cudaMemcpy(d.data(), s->d_msgs + first, n * sizeof(DevMsg), cudaMemcpyDeviceToHost), "D2H");
+    for (uint64_t i = 0; i < n; ++i) {
+      mlob_message& m = out[i];
+      std::memset(&m, 0, sizeof m);
+      m.time = d[i].time;
+      m.order_id = d[i].order_id;
+      m.price = d[i].price;
+      m.quantity = d[i].qty;
+      m.kind = d[i].kind;
+      m.side = d[i].side;
+      m.trader_id = d[i].trader;
+    }
+  });
+}
+
+uint64_t mlob_store_n_states(const mlob_store* s) { return s->st_index.size(); }
+
+mlob_status mlob_store_state(const mlob_store* s, uint64_t i, uint64_t* message_index, mlob_level* bids,
+                             uint32_t* n_bids, mlob_level* asks, uint32_t* n_asks, uint32_t cap) {
+  return guarded([&] {
+    if (i >= s->st_index.size()) fail(MLOB_E_OUT_OF_RANGE, "state index out of range");
+    const uint64_t b = s->st_offset[i], e = s->st_offset[i + 1];
+    const uint32_t nb = s->st_nb[i], na = static_cast<uint32_t>(e - b) - nb;
+    *message_index = s->st_index[i];
+    *n_bids = nb;
+    *n_asks = na;
+    if (nb > cap || na > cap) fail(MLOB_E_OUT_OF_RANGE, "state: capacity too small");
+    std::vector<DevLevel> lv(e - b);
+    cuda_check(cudaSetDevice(s->device), "cudaSetDevice");
+    if (e > b) cuda_check(cudaMemcpy(lv.data(), s->d_levels + b, (e - b) * sizeof(DevLevel), cudaMemcpyDeviceToHost),
+                          "D2H");
+    for (uint32_t k = 0; k < nb; ++k) bids[k] = mlob_level{lv[k].price, lv[k].qty};
+    for (uint32_t k = 0; k < na; ++k) asks[k] = mlob_level{lv[nb + k].price, lv[nb + k].qty};
+  });
 }
 
 uint64_t mlob_store_n_messages(const mlob_store* s) { return s->n_msgs; }

@@ -65,6 +65,12 @@ _SIGS = {
     "mlob_store_upload_raw": (C.c_int, [_P(Message), C.c_uint64, _P(abi.BookStates), C.c_int,
                                         _P(_vp)]),
     "mlob_store_n_messages": (C.c_uint64, [_vp]),
+    "mlob_store_load_lobster": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int64, C.c_uint64, C.c_int,
+                                          _P(_vp)]),
+    "mlob_store_read_messages": (C.c_int, [_vp, C.c_uint64, C.c_uint64, _P(Message)]),
+    "mlob_store_n_states": (C.c_uint64, [_vp]),
+    "mlob_store_state": (C.c_int, [_vp, C.c_uint64, _P(C.c_uint64), _P(Level), _P(C.c_uint32),
+                                   _P(Level), _P(C.c_uint32), C.c_uint32]),
     "mlob_store_device_bytes": (C.c_uint64, [_vp]),
     "mlob_store_free": (None, [_vp]),
     "mlob_venv_create": (C.c_int, [_P(VenvDesc), _P(_vp)]),
@@ -280,6 +286,35 @@ class DeviceStore:
     @property
     def device_bytes(self) -> int:
         return lib().mlob_store_device_bytes(self.h)
+
+    @classmethod
+    def load_lobster(cls, message_path: str, orderbook_path: str, units_per_tick: int,
+                     sample_every: int, device: int = 0) -> "DeviceStore":
+        """data::load_lobster (lobster.hpp:119-193) parsed on the GPU straight into HBM."""
+        self = cls.__new__(cls)
+        self.h = _vp()
+        self.device = device
+        _check(lib().mlob_store_load_lobster(str(message_path).encode(), str(orderbook_path).encode(),
+                                             units_per_tick, sample_every, device, C.byref(self.h)))
+        return self
+
+    def messages(self) -> np.ndarray:
+        """Device records widened to lob::Message (price / qty as the device keeps them)."""
+        n = self.n_messages
+        out = np.zeros(n, dtype=MESSAGE_DTYPE)
+        if n:
+            _check(lib().mlob_store_read_messages(self.h, 0, n, out.ctypes.data_as(_P(Message))))
+        return out
+
+    def states(self, cap: int = 4096):
+        out = []
+        bids, asks = (Level * cap)(), (Level * cap)()
+        mi, nb, na = C.c_uint64(), C.c_uint32(), C.c_uint32()
+        for i in range(lib().mlob_store_n_states(self.h)):
+            _check(lib().mlob_store_state(self.h, i, C.byref(mi), bids, C.byref(nb), asks, C.byref(na), cap))
+            out.append((mi.value, [(bids[k].price, bids[k].quantity) for k in range(nb.value)],
+                        [(asks[k].price, asks[k].quantity) for k in range(na.value)]))
+        return out
 
 
 # ---- batched environments ------------------------------------------------------

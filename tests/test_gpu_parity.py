@@ -402,3 +402,59 @@ def test_evaluate_matrix_learned_matches_oracle(orc):
     wrong = abi.policy(abi.POLICY_LEARNED, net=orc.make_policy_net(3, 8, 4, 0))
     with pytest.raises(ValueError):
         evaluate_matrix(dev_store(synth_kw), cfg, eps, [wrong], t1, 5)
+
+
+def test_lobster_device_loader(orc, tmp_path):
+    """mlob_store_load_lobster (GPU parse) against the oracle's load_lobster
+    (pinned to the reference): the device store equals the upload of the
+    oracle's store, malformed inputs raise the same class and text, and an env
+    replaying the loaded store matches the oracle env on the oracle store."""
+    from paper_2511_02136_b200.env import DeviceStore as DS
+    from tests.lobster_util import ACCEPTED, MALFORMED, write_lobster
+
+    def files(name, msg, book):
+        m, b = tmp_path / f"{name}_m.csv", tmp_path / f"{name}_b.csv"
+        m.write_text(msg)
+        b.write_text(book)
+        return str(m), str(b)
+
+    def same(m, b, upt, every):
+        got = DS.load_lobster(m, b, upt, every)
+        o = orc.lobster(m, b, upt, every)
+        want = DS(HostStore.from_messages(o.messages(), o.states()), 0)
+        assert got.messages().tobytes() == want.messages().tobytes()
+        assert got.states() == want.states() == o.states()
+        return got, o
+
+    for name, msg, book, upt, every in ACCEPTED:
+        same(*files(name, msg, book), upt, every)
+    for name, msg, book, upt, every in MALFORMED:
+        m, b = files(name, msg, book)
+        errs = []
+        for load in (lambda: DS.load_lobster(m, b, upt, every), lambda: orc.lobster(m, b, upt, every)):
+            with pytest.raises(Exception) as ei:
+                load()
+            errs.append((type(ei.value), str(ei.value)))
+        assert errs[0] == errs[1], name
+    with pytest.raises(ValueError):
+        DS.load_lobster(m, b, 0, 1)
+    # a synthetic day: parse on the GPU, then replay through the env
+    synth = orc.synth(abi.synth_config(n_messages=20000, state_sample_every=100), 2)
+    m, b = str(tmp_path / "day_m.csv"), str(tmp_path / "day_b.csv")
+    write_lobster(orc, synth.messages(), m, b, upt=100, depth=10)
+    dev, ost = same(m, b, 100, 100)
+    cfg = abi.env_config([abi.agent_spec(abi.MARKET_MAKER), abi.agent_spec(abi.EXECUTOR)],
+                         steps_per_episode=20, messages_per_step=50, start_stride_steps=4)
+    bt = MarketEnvBatch(dev, cfg, n_envs=4, seed=3, env_indices=[0, 1, 2, 3])
+    refs = [OEnv(orc, ost, cfg, 3, i) for i in range(4)]
+    eps = [0, 5, 17, 30]
+    bt.reset(eps)
+    for r, ep in zip(refs, eps):
+        r.reset(ep)
+    rng = kat.CounterRng(kat.make_key(9, 9))
+    for t in range(20):
+        ids = [[rng.below(abi.action_arity(cfg.specs[s])) for s in bt.flat] for _ in range(4)]
+        bt.step_ids(np.array(ids, dtype=np.int32))
+        for i, r in enumerate(refs):
+            r.step_ids(ids[i])
+            compare_env_state(bt.view(i), r)

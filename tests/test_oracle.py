@@ -340,3 +340,48 @@ def test_evaluate_matrix_learned_matches_reference(orc, ref):
     a = orc.evaluate(small_store(orc, synth_kw), cfg, eps, t0, t1, 5)
     b = ref.evaluate(small_store(ref, synth_kw), cfg, eps, t0, t1, 5)
     assert [bytes(x) for x in a] == [bytes(x) for x in b]
+
+
+def _msgs(store):
+    """message records with the (uninitialised in the reference) padding zeroed"""
+    m = store.messages()
+    m["_pad"] = b"\x00\x00"
+    return m.tobytes()
+
+
+def _lobster_files(tmp_path, name, msg, book):
+    m, b = tmp_path / f"{name}_msg.csv", tmp_path / f"{name}_book.csv"
+    m.write_text(msg)
+    b.write_text(book)
+    return str(m), str(b)
+
+
+def test_lobster_matches_reference(orc, ref, tmp_path):
+    """load_lobster (lobster.hpp:119-193): C restatement vs the reference on the
+    test_data.cpp KAT, edge-case inputs and a synthetic day written like
+    write_lobster; malformed inputs raise the same class and text."""
+    from tests.lobster_util import ACCEPTED, MALFORMED, write_lobster
+    for name, msg, book, upt, every in ACCEPTED:
+        m, b = _lobster_files(tmp_path, name, msg, book)
+        a, r = orc.lobster(m, b, upt, every), ref.lobster(m, b, upt, every)
+        assert _msgs(a) == _msgs(r), name
+        assert a.states() == r.states(), name
+    kat = orc.lobster(*_lobster_files(tmp_path, "kat2", ACCEPTED[0][1], ACCEPTED[0][2]), 100, 1)
+    m0 = kat.messages()[0]                    # test_data.cpp:54-82
+    assert (m0["kind"], m0["side"], m0["price"], m0["quantity"], m0["order_id"], m0["time"]) == \
+        (abi.NEW_LIMIT, abi.BID, 31480, 10, 42, 34200000123000)
+    assert kat.states() == [(0, [], []), (1, [(31480, 10)], [(31490, 5)])]
+    for name, msg, book, upt, every in MALFORMED:
+        m, b = _lobster_files(tmp_path, name, msg, book)
+        errs = []
+        for o in (orc, ref):
+            with pytest.raises(Exception) as ei:
+                o.lobster(m, b, upt, every)
+            errs.append((type(ei.value), str(ei.value)))
+        assert errs[0] == errs[1], name
+    synth = orc.synth(abi.synth_config(n_messages=3000, state_sample_every=100), 1)
+    m, b = str(tmp_path / "day_msg.csv"), str(tmp_path / "day_book.csv")
+    write_lobster(orc, synth.messages(), m, b, upt=100, depth=5)
+    a, r = orc.lobster(m, b, 100, 100), ref.lobster(m, b, 100, 100)
+    assert _msgs(a) == _msgs(r)
+    assert a.states() == r.states() and len(a.states()) == 30
