@@ -11,6 +11,15 @@
 
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
+#include <fcntl.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <mutex>
+#include <thread>
+#include <chrono>
+#include <cstdlib>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -23,11 +32,6 @@
 namespace mlob {
 namespace lobster {
 namespace {
-
-struct IsNewline {
-  const char* b;
-  __device__ bool operator()(uint64_t i) const { return b[i] == '\n'; }
-};
 
 // line j = [start, end): starts after the previous '\n'; a final line without
 // '\n' exists when non-empty (std::getline)
@@ -197,31 +201,175 @@ void check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw LobsterError(std::string("CUDA ") + what + ": " + cudaGetErrorString(e), 5);
 }
 
-// newline positions of a device buffer (ordered)
+// newline positions of a device buffer, in order: pass 1 counts '\n' per
+// block segment (16-byte loads, SWAR byte compare), an exclusive scan gives
+// each segment's output offset, pass 2 re-reads the segment tile by tile and
+// writes positions with a block scan.  Two streaming reads of the buffer.
+constexpr int kNlThreads = 256;
+constexpr int kNlBlocks = 2048;
+__device__ __forceinline__ uint32_t nl_mask(uint32_t w) {  // high bit of each '\n' byte
+  const uint32_t x = w ^ 0x0A0A0A0Au;
+  return (x - 0x01010101u) & ~x & 0x80808080u;
+}
+__device__ __forceinline__ int nl_count16(const uint4& v) {
+  return __popc(nl_mask(v.x)) + __popc(nl_mask(v.y)) + __popc(nl_mask(v.z)) + __popc(nl_mask(v.w));
+}
+__device__ __forceinline__ uint4 load16(const char* b, uint64_t size, uint64_t off) {
+  if (off + 16 <= size) return *reinterpret_cast<const uint4*>(b + off);
+  uint32_t w[4] = {0, 0, 0, 0};
+  for (uint64_t i = off; i < size; ++i) w[(i - off) / 4] |= static_cast<uint32_t>(static_cast<uint8_t>(b[i])) << (8 * ((i - off) % 4));
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+__global__ void nl_count_kernel(const char* b, uint64_t size, uint64_t seg, unsigned long long* counts) {
+  const uint64_t lo = blockIdx.x * seg, hi = min(size, lo + seg);
+  unsigned long long c = 0;
+  for (uint64_t off = lo + threadIdx.x * 16ull; off < hi; off += kNlThreads * 16ull) c += nl_count16(load16(b, size, off));
+  typedef cub::BlockReduce<unsigned long long, kNlThreads> R;
+  __shared__ typename R::TempStorage tmp;
+  const unsigned long long t = R(tmp).Sum(c);
+  if (threadIdx.x == 0) counts[blockIdx.x] = t;
+}
+__global__ void nl_write_kernel(const char* b, uint64_t size, uint64_t seg, const unsigned long long* offs,
+                                uint64_t* out) {
+  typedef cub::BlockScan<unsigned int, kNlThreads> S;
+  __shared__ typename S::TempStorage tmp;
+  __shared__ unsigned long long base;
+  const uint64_t lo = blockIdx.x * seg, hi = min(size, lo + seg);
+  if (threadIdx.x == 0) base = offs[blockIdx.x];
+  __syncthreads();
+  for (uint64_t tile = lo; tile < hi; tile += kNlThreads * 16ull) {
+    const uint64_t off = tile + threadIdx.x * 16ull;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (off < hi) v = load16(b, size, off);
+    const unsigned int c = off < hi ? static_cast<unsigned int>(nl_count16(v)) : 0u;
+    unsigned int pre = 0, tot = 0;
+    S(tmp).ExclusiveSum(c, pre, tot);
+    if (c) {
+      uint64_t o = base + pre;
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      for (int i = 0; i < 16; ++i)
+        if (static_cast<uint8_t>(w[i / 4] >> (8 * (i % 4))) == '\n') out[o++] = off + i;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) base += tot;
+    __syncthreads();
+  }
+}
+
 uint64_t newlines(const char* d_buf, uint64_t size, uint64_t** d_nl, void** tmp, size_t* tmp_bytes,
                   cudaStream_t s) {
-  uint64_t* d_cnt = nullptr;
-  check(cudaMallocAsync(reinterpret_cast<void**>(&d_cnt), sizeof(uint64_t), s), "alloc");
-  thrust::counting_iterator<uint64_t> it(0);
-  check(cudaMallocAsync(reinterpret_cast<void**>(d_nl), (size + 1) * sizeof(uint64_t), s), "alloc nl");
+  *d_nl = nullptr;
+  if (size == 0) {
+    check(cudaMallocAsync(reinterpret_cast<void**>(d_nl), 8, s), "alloc nl");
+    return 0;
+  }
+  const uint64_t seg = ((size + kNlBlocks - 1) / kNlBlocks + 15) / 16 * 16;
+  const unsigned blocks = static_cast<unsigned>((size + seg - 1) / seg);
+  unsigned long long* cnt = nullptr;
+  check(cudaMallocAsync(reinterpret_cast<void**>(&cnt), (blocks + 1) * 8, s), "alloc");
+  nl_count_kernel<<<blocks, kNlThreads, 0, s>>>(d_buf, size, seg, cnt);
+  check(cudaGetLastError(), "newline count");
   size_t need = 0;
-  check(cub::DeviceSelect::If(nullptr, need, it, *d_nl, d_cnt, size, IsNewline{d_buf}, s), "select");
+  check(cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, cnt, blocks + 1, s), "scan");
   if (need > *tmp_bytes) {
     if (*tmp) check(cudaFreeAsync(*tmp, s), "free");
     check(cudaMallocAsync(tmp, need, s), "alloc tmp");
     *tmp_bytes = need;
   }
-  check(cub::DeviceSelect::If(*tmp, need, it, *d_nl, d_cnt, size, IsNewline{d_buf}, s), "select");
-  uint64_t n = 0;
-  check(cudaMemcpyAsync(&n, d_cnt, sizeof n, cudaMemcpyDeviceToHost, s), "D2H");
+  check(cudaMemsetAsync(cnt + blocks, 0, 8, s), "memset");
+  check(cub::DeviceScan::ExclusiveSum(*tmp, need, cnt, cnt, blocks + 1, s), "scan");
+  unsigned long long n = 0;
+  check(cudaMemcpyAsync(&n, cnt + blocks, 8, cudaMemcpyDeviceToHost, s), "D2H");
   check(cudaStreamSynchronize(s), "sync");
-  check(cudaFreeAsync(d_cnt, s), "free");
+  check(cudaMallocAsync(reinterpret_cast<void**>(d_nl), (n + 1) * 8, s), "alloc nl");
+  nl_write_kernel<<<blocks, kNlThreads, 0, s>>>(d_buf, size, seg, cnt, *d_nl);
+  check(cudaGetLastError(), "newline write");
+  check(cudaFreeAsync(cnt, s), "free");
   return n;
 }
 
-std::string row_text(const std::string& f, uint64_t b, uint64_t e) {
-  if (e > b && f[e - 1] == '\r') --e;
-  return f.substr(b, e - b);
+// Streams a file into device memory through two page-locked chunk buffers:
+// the read of chunk i+1 overlaps the copy of chunk i.  Returns the size;
+// `last` = the final byte (for std::getline's tail-line rule).
+constexpr size_t kChunkBytes = size_t(16) << 20;
+constexpr int kReaders = 4;  // page-cache reads are memcpy-bound: a few threads in parallel
+struct PinnedPool {
+  char* buf[kReaders][2] = {};
+  cudaEvent_t ev[kReaders][2] = {};
+};
+PinnedPool& pinned_pool() {  // process-lifetime staging buffers (page-locking is slow)
+  static PinnedPool p;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    for (int r = 0; r < kReaders; ++r)
+      for (int i = 0; i < 2; ++i) {
+        check(cudaHostAlloc(reinterpret_cast<void**>(&p.buf[r][i]), kChunkBytes, cudaHostAllocDefault), "pinned");
+        check(cudaEventCreateWithFlags(&p.ev[r][i], cudaEventDisableTiming), "event");
+      }
+  });
+  return p;
+}
+uint64_t file_size(const std::string& path) {
+  FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) throw LobsterError("load_lobster: cannot open " + path, 4);
+  std::fseek(f, 0, SEEK_END);
+  const long n = std::ftell(f);
+  std::fclose(f);
+  return n > 0 ? static_cast<uint64_t>(n) : 0;
+}
+// Reader r takes chunks r, r + kReaders, ...: pread into one of its two
+// page-locked buffers while the other's copy is in flight on stream s.
+void stream_file(const std::string& path, char* d_dst, uint64_t size, char& last, cudaStream_t s) {
+  last = '\n';
+  if (size == 0) return;
+  const int fd = ::open(path.c_str(), O_RDONLY);
+  if (fd < 0) throw LobsterError("load_lobster: cannot open " + path, 4);
+  PinnedPool& pp = pinned_pool();
+  const uint64_t n_chunks = (size + kChunkBytes - 1) / kChunkBytes;
+  std::atomic<bool> failed{false};
+  std::vector<std::thread> th;
+  for (int r = 0; r < kReaders; ++r)
+    th.emplace_back([&, r] {
+      int i = 0;
+      for (uint64_t c = r; c < n_chunks && !failed; c += kReaders, i ^= 1) {
+        if (cudaEventSynchronize(pp.ev[r][i]) != cudaSuccess) {
+          failed = true;
+          return;
+        }
+        const uint64_t off = c * kChunkBytes;
+        const size_t n = static_cast<size_t>(std::min<uint64_t>(kChunkBytes, size - off));
+        size_t got = 0;
+        while (got < n) {
+          const ssize_t k = ::pread(fd, pp.buf[r][i] + got, n - got, static_cast<off_t>(off + got));
+          if (k <= 0) {
+            failed = true;
+            return;
+          }
+          got += static_cast<size_t>(k);
+        }
+        if (off + n == size) last = pp.buf[r][i][n - 1];
+        if (cudaMemcpyAsync(d_dst + off, pp.buf[r][i], n, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+            cudaEventRecord(pp.ev[r][i], s) != cudaSuccess)
+          failed = true;
+      }
+    });
+  for (auto& t : th) t.join();
+  ::close(fd);
+  if (failed) throw LobsterError("load_lobster: cannot open " + path, 4);
+}
+
+// text of line j of a device buffer (strip_cr applied), for error messages
+std::string device_line(const char* d_buf, uint64_t size, const uint64_t* d_nl, uint64_t n_nl, uint64_t j) {
+  uint64_t b = 0, e = size;
+  if (j > 0) {
+    check(cudaMemcpy(&b, d_nl + j - 1, 8, cudaMemcpyDeviceToHost), "D2H");
+    ++b;
+  }
+  if (j < n_nl) check(cudaMemcpy(&e, d_nl + j, 8, cudaMemcpyDeviceToHost), "D2H");
+  std::string t(e - b, '\0');
+  if (e > b) check(cudaMemcpy(&t[0], d_buf + b, e - b, cudaMemcpyDeviceToHost), "D2H");
+  if (!t.empty() && t.back() == '\r') t.pop_back();
+  return t;
 }
 
 }  // namespace
@@ -294,22 +442,16 @@ void load(const std::string& msg_path, const std::string& book_path, int64_t upt
           cudaStream_t s, LobsterStore& out) {
   if (upt < 1) throw LobsterError("load_lobster: units_per_tick >= 1", 1);
   if (sample_every == 0) throw LobsterError("load_lobster: sample_every >= 1", 1);
-  const auto slurp = [](const std::string& path, std::string& buf, const char* err) {
-    FILE* f = std::fopen(path.c_str(), "rb");
-    if (!f) throw LobsterError(std::string(err) + path, 4);
-    std::fseek(f, 0, SEEK_END);
-    const long n = std::ftell(f);
-    std::fseek(f, 0, SEEK_SET);
-    buf.resize(n > 0 ? static_cast<size_t>(n) : 0);
-    if (n > 0 && std::fread(&buf[0], 1, buf.size(), f) != buf.size()) {
-      std::fclose(f);
-      throw LobsterError(std::string(err) + path, 4);
-    }
-    std::fclose(f);
+  const uint64_t ms = file_size(msg_path), bs = file_size(book_path);
+  const bool timing = std::getenv("MLOB_LOBSTER_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  const auto mark = [&](const char* what) {
+    if (!timing) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "lobster %-10s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
   };
-  std::string hm, hb;
-  slurp(msg_path, hm, "load_lobster: cannot open ");
-  slurp(book_path, hb, "load_lobster: cannot open ");
 
   char *d_msg = nullptr, *d_book = nullptr;
   uint64_t *m_nl = nullptr, *b_nl = nullptr, *rows = nullptr, *d_cnt = nullptr;
@@ -331,20 +473,22 @@ void load(const std::string& msg_path, const std::string& book_path, int64_t upt
     cudaGetLastError();  // no stale (non-sticky) error left for the next call
   };
   try {
-    const uint64_t ms = hm.size(), bs = hb.size();
     check(cudaMallocAsync(reinterpret_cast<void**>(&d_msg), ms + 1, s), "alloc");
     owned.push_back(d_msg);
     check(cudaMallocAsync(reinterpret_cast<void**>(&d_book), bs + 1, s), "alloc");
     owned.push_back(d_book);
-    if (ms) check(cudaMemcpyAsync(d_msg, hm.data(), ms, cudaMemcpyHostToDevice, s), "H2D");
-    if (bs) check(cudaMemcpyAsync(d_book, hb.data(), bs, cudaMemcpyHostToDevice, s), "H2D");
+    char m_last = '\n', b_last = '\n';
+    stream_file(msg_path, d_msg, ms, m_last, s);
+    stream_file(book_path, d_book, bs, b_last, s);
+    mark("read+H2D");
     const uint64_t m_nl_n = newlines(d_msg, ms, &m_nl, &tmp, &tmp_bytes, s);
     owned.push_back(m_nl);
     const uint64_t b_nl_n = newlines(d_book, bs, &b_nl, &tmp, &tmp_bytes, s);
     owned.push_back(b_nl);
+    mark("newlines");
     // std::getline line counts: a tail without '\n' counts when non-empty
-    const uint64_t m_lines = m_nl_n + ((ms > 0 && hm.back() != '\n') ? 1 : 0);
-    const uint64_t b_lines = b_nl_n + ((bs > 0 && hb.back() != '\n') ? 1 : 0);
+    const uint64_t m_lines = m_nl_n + ((ms > 0 && m_last != '\n') ? 1 : 0);
+    const uint64_t b_lines = b_nl_n + ((bs > 0 && b_last != '\n') ? 1 : 0);
     // non-empty message lines = message rows
     check(cudaMallocAsync(reinterpret_cast<void**>(&rows), (m_lines + 1) * sizeof(uint64_t), s), "alloc");
     owned.push_back(rows);
@@ -416,6 +560,7 @@ void load(const std::string& msg_path, const std::string& book_path, int64_t upt
     unsigned long long flags[4];
     check(cudaMemcpyAsync(flags, d_flags, sizeof flags, cudaMemcpyDeviceToHost, s), "D2H");
     check(cudaStreamSynchronize(s), "sync");
+    mark("rows+parse");
     out.n_lines_msg = m_lines;
     if (flags[0] != ~0ull) {  // the reference throws at this row
       const uint64_t k = flags[0];
@@ -423,17 +568,10 @@ void load(const std::string& msg_path, const std::string& book_path, int64_t upt
       uint64_t line_idx = 0;
       check(cudaMemcpy(&code, d_err + k, 4, cudaMemcpyDeviceToHost), "D2H");
       check(cudaMemcpy(&line_idx, rows + k, 8, cudaMemcpyDeviceToHost), "D2H");
-      std::vector<uint64_t> mnl(m_nl_n), bnl(b_nl_n);
-      if (m_nl_n) check(cudaMemcpy(mnl.data(), m_nl, m_nl_n * 8, cudaMemcpyDeviceToHost), "D2H");
-      if (b_nl_n) check(cudaMemcpy(bnl.data(), b_nl, b_nl_n * 8, cudaMemcpyDeviceToHost), "D2H");
-      const auto host_line = [](const std::string& f, const std::vector<uint64_t>& nl, uint64_t j) {
-        const uint64_t b = j == 0 ? 0 : nl[j - 1] + 1, e = j < nl.size() ? nl[j] : f.size();
-        return row_text(f, b, e);
-      };
-      const std::string line = host_line(hm, mnl, line_idx);
+      const std::string line = device_line(d_msg, ms, m_nl, m_nl_n, line_idx);
       std::string bl;
       const bool have_book = k < b_lines;
-      if (have_book) bl = host_line(hb, bnl, k);
+      if (have_book) bl = device_line(d_book, bs, b_nl, b_nl_n, k);
       cleanup();
       throw LobsterError(format_row_error(line, have_book ? &bl : nullptr, k, upt, (k + 1) % sample_every == 0,
                                           code, msg_path),
@@ -493,6 +631,7 @@ void load(const std::string& msg_path, const std::string& book_path, int64_t upt
         throw LobsterError("book-state price or quantity outside the device int32 range", 1);
       }
     }
+    mark("states");
     cleanup();
   } catch (...) {
     cleanup();
