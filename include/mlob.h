@@ -486,6 +486,44 @@ mlob_status mlob_venv_rollout_read(mlob_venv* v, int type, int field, void* out,
 /* Device pointer of the same field (NULL before the first rollout). */
 const void* mlob_venv_rollout_device(const mlob_venv* v, int type, int field);
 
+/* ippo::PpoConfig (ppo.hpp:19-28) */
+typedef struct mlob_ppo_config {
+  int32_t epochs;
+  int32_t minibatches;
+  double clip_eps;
+  double vf_coef;
+  double ent_coef;
+  double lr;
+  double max_grad_norm;
+  int32_t normalize_adv;
+  int32_t _pad;
+} mlob_ppo_config;
+void mlob_default_ppo_config(mlob_ppo_config* out);
+
+/* ippo::UpdateMetrics (ppo.hpp:69-77) */
+typedef struct mlob_update_metrics {
+  double pg_loss;
+  double v_loss;
+  double entropy;
+  double approx_kl;
+  double clip_frac;
+  double grad_norm;
+  double mean_reward;
+} mlob_update_metrics;
+
+/* ppo_update (ppo.hpp:263-310) of type `type` on the device over the batch of
+ * the last collect_rollout: `epochs` passes over a CounterRng-shuffled
+ * partition of the streams (key (seed, Minibatch, update_index, epoch,
+ * type)), each minibatch a BPTT forward/backward of the GRU, global-norm
+ * clipping and an Adam step (net.hpp:281-331; the Adam state lives in the
+ * handle, reset by set_nets).  The updated weights are used by the next
+ * rollout; read them with mlob_venv_read_net.  runtime_error on a non-finite
+ * loss, as the reference. */
+mlob_status mlob_venv_ppo_update(mlob_venv* v, int type, const mlob_ppo_config* cfg, uint64_t seed,
+                                 uint64_t update_index, mlob_update_metrics* out);
+/* The type's current parameters, PolicyNet::for_each_param order (net.hpp:36-41). */
+mlob_status mlob_venv_read_net(mlob_venv* v, int type, double* flat, uint64_t cap);
+
 /* ---- Scripted policies and cross-play evaluation (ippo/evaluate.hpp) ------ */
 
 /* ippo::PolicyKind (evaluate.hpp:17); Learned is not available on the device. */

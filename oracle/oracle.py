@@ -122,6 +122,9 @@ _SIG = {
                                   _P(abi.CellStats)]),
 }
 _REF_ONLY = {
+    "venv_ppo_update": (C.c_int, [C.c_void_p, C.c_int, _P(abi.PpoConfig), C.c_uint64, C.c_uint64,
+                                  _P(abi.UpdateMetrics)]),
+    "venv_read_net": (C.c_uint64, [C.c_void_p, C.c_int, _P(C.c_double), C.c_uint64]),
     "naive_create": (C.c_void_p, []),
     "naive_process": (C.c_uint64, [C.c_void_p, _P(Message), _P(Trade), C.c_uint64]),
     "naive_best": (C.c_int, [C.c_void_p, C.c_int, _P(C.c_int64)]),
@@ -441,10 +444,22 @@ class OVecEnv:
     def collect_rollout(self, nets, rollout_len: int, discount: float, gae_lambda: float,
                         seed: int, update_index: int):
         """ippo::collect_rollout (rollout.hpp:41-124); nets: one abi.NetParams per type."""
-        arr = (abi.PolicyNetC * len(nets))(*[n.to_c() for n in nets])
+        arr = None if nets is None else (abi.PolicyNetC * len(nets))(*[n.to_c() for n in nets])
         c = abi.RolloutConfig(rollout_len=rollout_len, discount=discount, gae_lambda=gae_lambda,
                               seed=seed)
         self.o.check(self.o.venv_collect_rollout(self.h, arr, C.byref(c), update_index))
+
+    def ppo_update(self, t: int, cfg, seed: int, update_index: int):
+        """ippo::ppo_update (ppo.hpp:263-310) of type t (reference only)."""
+        m = abi.UpdateMetrics()
+        self.o.check(self.o.venv_ppo_update(self.h, t, C.byref(cfg), seed, update_index, C.byref(m)))
+        return m
+
+    def read_net(self, t: int) -> np.ndarray:
+        n = self.o.venv_read_net(self.h, t, None, 0)
+        out = np.zeros(n, dtype=np.float64)
+        self.o.venv_read_net(self.h, t, out.ctypes.data_as(_P(C.c_double)), n)
+        return out
 
     def rollout(self, t: int, field: int) -> np.ndarray:
         n = self.o.venv_rollout_field(self.h, t, field, None, 0)

@@ -121,6 +121,11 @@ uint64_t orc_splitmix64(uint64_t z);
 uint64_t orc_make_key(uint64_t seed, int n, const uint64_t* words);
 void orc_crng_draws(uint64_t key, uint64_t n, uint64_t* out);
 void orc_random_stream(const orc_stream_config* cfg, uint64_t seed, mlob_message* out);
+/* ppo_update (ppo.hpp:263-310) over the last ref_venv_collect_rollout batch; the
+ * device update is pinned to the reference directly (reference-side only) */
+int ref_venv_ppo_update(void* v, int type, const mlob_ppo_config* cfg, uint64_t seed, uint64_t update_index,
+                        mlob_update_metrics* out);
+uint64_t ref_venv_read_net(void* v, int type, double* out, uint64_t cap);
 /* evaluate.hpp:56-99 choose_action (scripted kinds) on an orc env */
 int orc_choose_action(void* env, int agent, const mlob_policy* p, int step, uint64_t seed,
                       uint64_t cell_id, uint64_t episode, mlob_agent_action* out);

@@ -168,6 +168,7 @@ struct VenvH {
   std::vector<ippo::PolicyNet> nets;
   std::vector<std::vector<double>> hidden;
   std::vector<ippo::RolloutBatch> batches;
+  std::vector<ippo::AdamState> adams;  // one per type (train_loop's adams)
 };
 
 ippo::PolicyNet to_net(const mlob_policy_net& n) {
@@ -485,13 +486,16 @@ int ref_venv_collect_rollout(void* v, const mlob_policy_net* nets, const mlob_ro
   return guarded([&] {
     const int T = h->venv->n_types();
     const bool fresh = h->nets.empty();
-    h->nets.clear();
-    for (int t = 0; t < T; ++t) h->nets.push_back(to_net(nets[t]));
+    if (nets) {  // null: keep the networks (as updated by ref_venv_ppo_update)
+      h->nets.clear();
+      for (int t = 0; t < T; ++t) h->nets.push_back(to_net(nets[t]));
+    }
     if (fresh) {  // train_loop, rollout.hpp:132-135
       h->hidden.assign(static_cast<std::size_t>(T), {});
       for (int t = 0; t < T; ++t)
-        h->hidden[t].assign(h->venv->n_streams(t) * static_cast<std::size_t>(nets[t].hidden), 0.0);
+        h->hidden[t].assign(h->venv->n_streams(t) * static_cast<std::size_t>(h->nets[t].hidden), 0.0);
       h->batches.assign(static_cast<std::size_t>(T), {});
+      h->adams.assign(static_cast<std::size_t>(T), {});
     }
     ippo::TrainLoopConfig c;
     c.rollout_len = cfg->rollout_len;
@@ -500,6 +504,38 @@ int ref_venv_collect_rollout(void* v, const mlob_policy_net* nets, const mlob_ro
     c.seed = cfg->seed;
     ippo::collect_rollout(*h->venv, h->nets, h->hidden, h->batches, c, update_index);
   });
+}
+
+int ref_venv_ppo_update(void* v, int type, const mlob_ppo_config* cfg, uint64_t seed, uint64_t update_index,
+                        mlob_update_metrics* out) {
+  auto* h = static_cast<VenvH*>(v);
+  return guarded([&] {
+    ippo::PpoConfig c;
+    c.epochs = cfg->epochs;
+    c.minibatches = cfg->minibatches;
+    c.clip_eps = cfg->clip_eps;
+    c.vf_coef = cfg->vf_coef;
+    c.ent_coef = cfg->ent_coef;
+    c.lr = cfg->lr;
+    c.max_grad_norm = cfg->max_grad_norm;
+    c.normalize_adv = cfg->normalize_adv != 0;
+    const auto t = static_cast<std::size_t>(type);
+    const ippo::UpdateMetrics m =
+        ippo::ppo_update(h->nets.at(t), h->adams.at(t), h->batches.at(t), c, seed, update_index, t);
+    *out = mlob_update_metrics{m.pg_loss, m.v_loss, m.entropy, m.approx_kl, m.clip_frac, m.grad_norm,
+                               m.mean_reward};
+  });
+}
+
+uint64_t ref_venv_read_net(void* v, int type, double* out, uint64_t cap) {
+  auto* h = static_cast<VenvH*>(v);
+  ippo::PolicyNet& n = h->nets.at(static_cast<std::size_t>(type));
+  const uint64_t P = n.param_count();
+  if (P <= cap) {
+    std::size_t i = 0;
+    n.for_each_param([&](double& x) { out[i++] = x; });
+  }
+  return P;
 }
 
 uint64_t ref_venv_rollout_field(void* v, int type, int field, void* out, uint64_t cap) {

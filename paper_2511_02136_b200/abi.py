@@ -189,6 +189,26 @@ class NetParams:
         return n
 
 
+class PpoConfig(C.Structure):  # ippo::PpoConfig (ppo.hpp:19-28)
+    _fields_ = [("epochs", i32), ("minibatches", i32), ("clip_eps", f64), ("vf_coef", f64),
+                ("ent_coef", f64), ("lr", f64), ("max_grad_norm", f64), ("normalize_adv", i32),
+                ("_pad", i32)]
+
+
+def ppo_config(**kw) -> PpoConfig:
+    """PpoConfig with the reference defaults (ppo.hpp:19-28), overridden by kw."""
+    c = PpoConfig(epochs=4, minibatches=4, clip_eps=0.2, vf_coef=0.5, ent_coef=0.01, lr=3e-4,
+                  max_grad_norm=0.5, normalize_adv=1)
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+class UpdateMetrics(C.Structure):  # ippo::UpdateMetrics (ppo.hpp:69-77)
+    _fields_ = [("pg_loss", f64), ("v_loss", f64), ("entropy", f64), ("approx_kl", f64),
+                ("clip_frac", f64), ("grad_norm", f64), ("mean_reward", f64)]
+
+
 class Policy(C.Structure):
     """mlob_policy = ippo::PolicyChoice without the network (evaluate.hpp:19-25)."""
     _fields_ = [("kind", i32), ("twap_mode", i32), ("avst_gamma_index", i32), ("n_gamma", i32),

@@ -16,6 +16,10 @@
 #include "mlob_host.h"
 #include "mlob_lobster.h"
 #include "mlob_policy.h"
+#include "mlob_ppo.h"
+
+#include <cublas_v2.h>
+#include <sstream>
 
 namespace mlob {
 size_t step_smem_bytes(const DevCfg& c);
@@ -65,6 +69,16 @@ T* dalloc(size_t n, const char* what) {
   cuda_check(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), what);
   cuda_check(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)), what);
   return static_cast<T*>(p);
+}
+
+uint64_t host_splitmix(uint64_t z) {  // rng.hpp:11-16
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+uint64_t host_fold(uint64_t h, uint64_t w) {  // rng.hpp:18-20
+  return host_splitmix(h ^ (w + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2)));
 }
 
 int64_t fits32(int64_t v, const char* what) {
@@ -121,13 +135,25 @@ struct mlob_venv {
     double* w = nullptr;  // all weights, transposed layout (mlob_policy.h)
     double* hidden[2] = {};
     int cur = 0;
+    // reference layout + gradient + Adam moments (ppo_update), P doubles each
+    double *p = nullptr, *g = nullptr, *m = nullptr, *v = nullptr;
+    uint64_t P = 0;
+    int64_t adam_t = 0;
   };
   static void free_net(NetState& n) {
     cudaFree(n.w);
     cudaFree(n.hidden[0]);
     cudaFree(n.hidden[1]);
+    cudaFree(n.p);
+    cudaFree(n.g);
+    cudaFree(n.m);
+    cudaFree(n.v);
     n = NetState{};
   }
+  // ppo_update workspace (mlob_ppo.cu), grown on demand
+  char* ppo_ws = nullptr;
+  uint64_t ppo_ws_bytes = 0;
+  cublasHandle_t blas = nullptr;
   struct Batch {
     uint64_t T = 0, B = 0;
     char* arena = nullptr;
@@ -200,6 +226,8 @@ struct mlob_venv {
       cudaFree(batch[t].arena);
     }
     for (NetState& n : eval_nets) free_net(n);
+    cudaFree(ppo_ws);
+    if (blas) cublasDestroy(blas);
     for (void* p : allocs) cudaFree(p);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
@@ -1026,14 +1054,35 @@ static void upload_net(mlob_venv* v, const mlob_policy_net& n, mlob_venv::NetSta
   double* w_c = b_a + A;
   std::memcpy(w_c, n.w_critic, H * 8);
   const bool same_shape = ns.w && ns.dn.D == n.obs_dim && ns.dn.H == n.hidden && ns.dn.A == n.n_actions;
+  // the reference layout (for_each_param order) for ppo_update
+  const uint64_t P = H3 * D + H3 * H + 2 * H3 + A * H + A + H + 1;
+  std::vector<double> flat;
+  flat.reserve(P);
+  flat.insert(flat.end(), n.w_ih, n.w_ih + H3 * D);
+  flat.insert(flat.end(), n.w_hh, n.w_hh + H3 * H);
+  flat.insert(flat.end(), n.b_ih, n.b_ih + H3);
+  flat.insert(flat.end(), n.b_hh, n.b_hh + H3);
+  flat.insert(flat.end(), n.w_actor, n.w_actor + A * H);
+  flat.insert(flat.end(), n.b_actor, n.b_actor + A);
+  flat.insert(flat.end(), n.w_critic, n.w_critic + H);
+  flat.push_back(n.b_critic);
   if (!same_shape) {
     mlob_venv::free_net(ns);
+    cuda_check(cudaMalloc(&ns.p, P * 8), "cudaMalloc(params)");
+    cuda_check(cudaMalloc(&ns.g, P * 8), "cudaMalloc(grad)");
+    cuda_check(cudaMalloc(&ns.m, P * 8), "cudaMalloc(adam)");
+    cuda_check(cudaMalloc(&ns.v, P * 8), "cudaMalloc(adam)");
+    ns.P = P;
     cuda_check(cudaMalloc(&ns.w, w.size() * 8), "cudaMalloc(net)");
     cuda_check(cudaMalloc(&ns.hidden[0], std::max<uint64_t>(1, B * H) * 8), "cudaMalloc(hidden)");
     cuda_check(cudaMalloc(&ns.hidden[1], std::max<uint64_t>(1, B * H) * 8), "cudaMalloc(hidden)");
     cuda_check(cudaMemsetAsync(ns.hidden[0], 0, B * H * 8, v->stream), "memset");
   }
   cuda_check(cudaMemcpyAsync(ns.w, w.data(), w.size() * 8, cudaMemcpyHostToDevice, v->stream), "H2D");
+  cuda_check(cudaMemcpyAsync(ns.p, flat.data(), P * 8, cudaMemcpyHostToDevice, v->stream), "H2D");
+  cuda_check(cudaMemsetAsync(ns.m, 0, P * 8, v->stream), "memset");  // AdamState::init
+  cuda_check(cudaMemsetAsync(ns.v, 0, P * 8, v->stream), "memset");
+  ns.adam_t = 0;
   const double* base = ns.w;
   ns.dn.D = n.obs_dim;
   ns.dn.H = n.hidden;
@@ -1193,6 +1242,195 @@ const void* mlob_venv_rollout_device(const mlob_venv* v, int type, int field) {
   if (type < 0 || type >= v->cfg.n_specs) return nullptr;
   uint64_t bytes = 0;
   return rollout_field(v, type, field, &bytes);
+}
+
+// ---- PPO update (ppo.hpp:263-310) --------------------------------------------
+
+void mlob_default_ppo_config(mlob_ppo_config* c) {  // PpoConfig defaults, ppo.hpp:19-28
+  std::memset(c, 0, sizeof *c);
+  c->epochs = 4;
+  c->minibatches = 4;
+  c->clip_eps = 0.2;
+  c->vf_coef = 0.5;
+  c->ent_coef = 0.01;
+  c->lr = 3e-4;
+  c->max_grad_norm = 0.5;
+  c->normalize_adv = 1;
+}
+
+mlob_status mlob_venv_ppo_update(mlob_venv* v, int type, const mlob_ppo_config* cfg, uint64_t seed,
+                                 uint64_t update_index, mlob_update_metrics* out) {
+  return guarded([&] {
+    if (type < 0 || type >= v->cfg.n_specs) fail(MLOB_E_OUT_OF_RANGE, "ppo_update: type out of range");
+    if (!v->has_nets) fail(MLOB_E_LOGIC, "ppo_update: set_nets first");
+    mlob_venv::Batch& bt = v->batch[type];
+    if (!bt.arena || bt.B == 0 || bt.T == 0) fail(MLOB_E_INVALID_ARGUMENT, "ppo_update: empty batch");
+    v->set_device();
+    mlob_venv::NetState& ns = v->nets[type];
+    const int D = ns.dn.D, H = ns.dn.H, A = ns.dn.A, H3 = 3 * H;
+    const uint64_t T = bt.T, B = bt.B;
+    const int n_mb = std::max(1, std::min<int>(cfg->minibatches, static_cast<int>(std::min<uint64_t>(B, INT32_MAX))));
+    if (!v->blas) {
+      if (cublasCreate(&v->blas) != CUBLAS_STATUS_SUCCESS) fail(MLOB_E_CUDA, "cublasCreate failed");
+    }
+    cublasSetStream(v->blas, v->stream);
+    // workspace for the largest minibatch
+    const uint64_t Kmax = T * ((B + n_mb - 1) / n_mb + 1);
+    const uint64_t ones_n = std::max(Kmax, T * B);
+    const uint64_t cols = static_cast<uint64_t>(D) + 6ull * H + A + 1 + 5 + 2ull * H3 + 1;  // per row
+    const uint64_t need = (Kmax * cols + ones_n + 16) * 8 + B * 4 + 4096;
+    if (need > v->ppo_ws_bytes) {
+      cudaFree(v->ppo_ws);
+      v->ppo_ws = nullptr;
+      cuda_check(cudaMalloc(&v->ppo_ws, need), "cudaMalloc(ppo workspace)");
+      v->ppo_ws_bytes = need;
+    }
+    double* wsd = reinterpret_cast<double*>(v->ppo_ws);
+    double* ones = wsd;
+    double* sums = ones + ones_n;  // [0..4] terms, [5] grad norm, [6] reward sum
+    double* rows = sums + 16;
+    int32_t* d_order = reinterpret_cast<int32_t*>(rows + Kmax * cols);
+    cuda_check(launch_fill(ones, ones_n, 1.0, v->stream), "fill");
+    // reference-layout offsets (PolicyGrad mirrors PolicyNet)
+    const uint64_t o_wih = 0, o_whh = o_wih + static_cast<uint64_t>(H3) * D, o_bih = o_whh + static_cast<uint64_t>(H3) * H,
+                   o_bhh = o_bih + H3, o_wa = o_bhh + H3, o_ba = o_wa + static_cast<uint64_t>(A) * H, o_wc = o_ba + A,
+                   o_bc = o_wc + H;
+    std::vector<int32_t> order(B);
+    for (uint64_t i = 0; i < B; ++i) order[i] = static_cast<int32_t>(i);
+    mlob_update_metrics mt{};
+    int n_updates = 0;
+    for (int epoch = 0; epoch < cfg->epochs; ++epoch) {
+      // CounterRng(make_key(seed, Minibatch, update, epoch, type)) + fisher_yates (ppo.hpp:275-278, rng.hpp:63-71)
+      uint64_t st = host_splitmix(seed);
+      st = host_fold(host_fold(host_fold(host_fold(st, 6), update_index), static_cast<uint64_t>(epoch)),
+                     static_cast<uint64_t>(type));
+      for (uint64_t i = B - 1; i > 0; --i) {
+        st += 0x9E3779B97F4A7C15ull;
+        const uint64_t j = host_splitmix(st) % (i + 1);
+        if (i != j) std::swap(order[i], order[j]);
+      }
+      cuda_check(cudaMemcpyAsync(d_order, order.data(), B * 4, cudaMemcpyHostToDevice, v->stream), "H2D");
+      for (int mb = 0; mb < n_mb; ++mb) {
+        const uint64_t begin = B * static_cast<uint64_t>(mb) / n_mb, end = B * static_cast<uint64_t>(mb + 1) / n_mb;
+        if (end == begin) continue;
+        const uint64_t S = end - begin, K = T * S;
+        PpoArgs a{};
+        a.D = D;
+        a.H = H;
+        a.A = A;
+        a.T = T;
+        a.B = B;
+        a.S = S;
+        a.mb = d_order + begin;
+        a.obs = bt.obs;
+        a.resets = bt.resets;
+        a.actions = bt.actions;
+        a.logp_old = bt.log_probs;
+        a.returns = bt.ret;
+        a.h0 = bt.h0;
+        a.w_ih = ns.p + o_wih;
+        a.w_hh = ns.p + o_whh;
+        a.b_ih = ns.p + o_bih;
+        a.b_hh = ns.p + o_bhh;
+        a.w_actor = ns.p + o_wa;
+        a.b_actor = ns.p + o_ba;
+        a.w_critic = ns.p + o_wc;
+        cuda_check(cudaMemcpyAsync(&a.b_critic, ns.p + o_bc, 8, cudaMemcpyDeviceToHost, v->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(v->stream), "sync");
+        a.clip_eps = cfg->clip_eps;
+        a.vf_coef = cfg->vf_coef;
+        a.ent_coef = cfg->ent_coef;
+        double* r = rows;
+        const auto carve = [&](uint64_t n) {
+          double* p = r;
+          r += n;
+          return p;
+        };
+        double* adv = carve(K);
+        a.adv = adv;
+        a.X = carve(K * D);
+        a.Hin = carve(K * H);
+        a.R = carve(K * H);
+        a.Z = carve(K * H);
+        a.N = carve(K * H);
+        a.HN = carve(K * H);
+        a.Hout = carve(K * H);
+        a.dL = carve(K * A);
+        a.dV = carve(K);
+        a.terms = carve(K * 5);
+        a.dA = carve(K * H3);
+        a.dB = carve(K * H3);
+        cuda_check(launch_gather_adv(bt.adv, a.mb, T, B, S, adv, cfg->normalize_adv != 0, v->stream), "advantages");
+        cuda_check(launch_ppo_forward(a, v->stream), "ppo forward");
+        cuda_check(launch_ppo_backward(a, v->stream), "ppo backward");
+        cublasHandle_t hb = v->blas;
+        double* g = ns.g;
+        if (!gemm_tn(hb, a.dA, a.X, K, H3, D, g + o_wih) || !gemm_tn(hb, a.dB, a.Hin, K, H3, H, g + o_whh) ||
+            !colsum(hb, a.dA, ones, K, H3, g + o_bih) || !colsum(hb, a.dB, ones, K, H3, g + o_bhh) ||
+            !gemm_tn(hb, a.dL, a.Hout, K, A, H, g + o_wa) || !colsum(hb, a.dL, ones, K, A, g + o_ba) ||
+            !gemm_tn(hb, a.dV, a.Hout, K, 1, H, g + o_wc) || !colsum(hb, a.dV, ones, K, 1, g + o_bc) ||
+            !colsum(hb, a.terms, ones, K, 5, sums))
+          fail(MLOB_E_CUDA, "cuBLAS gradient GEMM failed");
+        double tsum[5];
+        cuda_check(cudaMemcpyAsync(tsum, sums, sizeof tsum, cudaMemcpyDeviceToHost, v->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(v->stream), "sync");
+        const double n_el = static_cast<double>(K);
+        const double pg = tsum[0] / n_el, vl = tsum[1] / n_el, ent = tsum[2] / n_el, kl = tsum[3] / n_el,
+                     cf = tsum[4] / n_el;
+        const double loss = pg + cfg->vf_coef * vl - cfg->ent_coef * ent;
+        if (!std::isfinite(loss)) {  // ppo.hpp:233-238
+          std::ostringstream oss;
+          oss << "ppo_update: non-finite loss (pg=" << pg << " v=" << vl << " ent=" << ent << " kl=" << kl << ")";
+          fail(MLOB_E_RUNTIME, oss.str());
+        }
+        ++ns.adam_t;
+        const double c1 = 1.0 - std::pow(0.9, static_cast<double>(ns.adam_t));
+        const double c2 = 1.0 - std::pow(0.999, static_cast<double>(ns.adam_t));
+        cuda_check(launch_clip_adam(ns.p, ns.g, ns.m, ns.v, ns.P, cfg->max_grad_norm, cfg->lr, c1, c2, sums + 5,
+                                    v->stream),
+                   "adam");
+        double norm = 0.0;
+        cuda_check(cudaMemcpyAsync(&norm, sums + 5, 8, cudaMemcpyDeviceToHost, v->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(v->stream), "sync");
+        mt.grad_norm += norm;
+        mt.pg_loss += pg;
+        mt.v_loss += vl;
+        mt.entropy += ent;
+        mt.approx_kl += kl;
+        mt.clip_frac += cf;
+        ++n_updates;
+        v->launches += 4;
+      }
+    }
+    const double inv = 1.0 / static_cast<double>(std::max(1, n_updates));
+    mt.pg_loss *= inv;
+    mt.v_loss *= inv;
+    mt.entropy *= inv;
+    mt.approx_kl *= inv;
+    mt.clip_frac *= inv;
+    mt.grad_norm *= inv;
+    if (!colsum(v->blas, bt.rewards, ones, T * B, 1, sums + 6)) fail(MLOB_E_CUDA, "cuBLAS reduction failed");
+    double rsum = 0.0;
+    cuda_check(cudaMemcpyAsync(&rsum, sums + 6, 8, cudaMemcpyDeviceToHost, v->stream), "D2H");
+    // the next rollout's network: transposed copy + b_critic
+    cuda_check(launch_to_inference(ns.p, D, H, A, ns.w, v->stream), "to_inference");
+    cuda_check(cudaMemcpyAsync(&ns.dn.b_critic, ns.p + o_bc, 8, cudaMemcpyDeviceToHost, v->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(v->stream), "sync");
+    mt.mean_reward = rsum / static_cast<double>(T * B);
+    if (out) *out = mt;
+  });
+}
+
+mlob_status mlob_venv_read_net(mlob_venv* v, int type, double* flat, uint64_t cap) {
+  return guarded([&] {
+    if (type < 0 || type >= v->cfg.n_specs) fail(MLOB_E_OUT_OF_RANGE, "read_net: type out of range");
+    const mlob_venv::NetState& ns = v->nets[type];
+    if (!ns.p) fail(MLOB_E_LOGIC, "read_net: set_nets first");
+    if (cap < ns.P) fail(MLOB_E_OUT_OF_RANGE, "read_net: buffer too small");
+    v->set_device();
+    cuda_check(cudaMemcpyAsync(flat, ns.p, ns.P * 8, cudaMemcpyDeviceToHost, v->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(v->stream), "sync");
+  });
 }
 
 // ---- scripted policies and cross-play evaluation ----------------------------

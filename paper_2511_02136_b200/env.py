@@ -98,6 +98,10 @@ _SIGS = {
     "mlob_venv_step_io": (C.c_int, [_vp, _P(abi.StepIO)]),
     "mlob_default_policy": (None, [C.c_int, _P(abi.Policy)]),
     "mlob_venv_set_nets": (C.c_int, [_vp, _P(abi.PolicyNetC)]),
+    "mlob_venv_ppo_update": (C.c_int, [_vp, C.c_int, _P(abi.PpoConfig), C.c_uint64, C.c_uint64,
+                                       _P(abi.UpdateMetrics)]),
+    "mlob_venv_read_net": (C.c_int, [_vp, C.c_int, _P(C.c_double), C.c_uint64]),
+    "mlob_default_ppo_config": (None, [_P(abi.PpoConfig)]),
     "mlob_venv_collect_rollout": (C.c_int, [_vp, _P(abi.RolloutConfig), C.c_uint64]),
     "mlob_venv_rollout_read": (C.c_int, [_vp, C.c_int, C.c_int, _vp, C.c_uint64]),
     "mlob_venv_rollout_device": (_vp, [_vp, C.c_int, C.c_int]),
@@ -424,6 +428,20 @@ class _Venv:
                               seed=seed)
         _check(lib().mlob_venv_collect_rollout(self.h, C.byref(c), update_index))
         self._rollout_len = rollout_len
+
+    def ppo_update(self, t: int, cfg=None, seed: int = 0, update_index: int = 1) -> abi.UpdateMetrics:
+        """ppo_update (ppo.hpp:263-310) of type t on the device (mlob_venv_ppo_update)."""
+        cfg = cfg if cfg is not None else abi.ppo_config()
+        m = abi.UpdateMetrics()
+        _check(lib().mlob_venv_ppo_update(self.h, t, C.byref(cfg), seed, update_index, C.byref(m)))
+        return m
+
+    def read_net(self, t: int) -> np.ndarray:
+        """Type t's parameters, PolicyNet::for_each_param order."""
+        D, H, A = self.obs_dim(t), self._hidden[t], self.n_actions(t)
+        out = np.zeros(abi.NetParams.param_count(D, H, A), dtype=np.float64)
+        _check(lib().mlob_venv_read_net(self.h, t, out.ctypes.data_as(_P(C.c_double)), out.size))
+        return out
 
     def rollout(self, t: int, field: int) -> np.ndarray:
         """One RolloutBatch field of type t (time-major, flat) in host memory."""

@@ -458,3 +458,32 @@ def test_lobster_device_loader(orc, tmp_path):
         for i, r in enumerate(refs):
             r.step_ids(ids[i])
             compare_env_state(bt.view(i), r)
+
+
+def test_ppo_update_matches_reference(ref):
+    """Device train_loop iterations (collect_rollout + ppo_update per type,
+    rollout.hpp:127-145 / ppo.hpp:263-310) against the reference's: metrics and
+    parameters after each update, and the next rollout with the updated nets.
+    Reductions are ordered differently (GEMMs over T x streams), so the bar is
+    1e-8 relative (+1e-12 absolute)."""
+    from tests.common import rollout_case
+    cfg, synth_kw, nets = rollout_case(ref)
+    g = MarketVecEnv(dev_store(synth_kw), cfg, seed=3, n_envs=5)
+    o = OVecEnv(ref, small_store(ref, synth_kw), cfg, 3, 5)
+    g.reset_all()
+    o.reset_all()
+    g.set_nets(nets)
+    pcfg = abi.ppo_config(minibatches=2)
+    for upd in (1, 2):
+        g.collect_rollout(12, 0.99, 0.95, seed=77, update_index=upd)
+        o.collect_rollout(nets if upd == 1 else None, 12, 0.99, 0.95, 77, upd)
+        assert g.rollout(0, abi.RB_ACTIONS).tobytes() == o.rollout(0, abi.RB_ACTIONS).tobytes()
+        assert g.rollout(1, abi.RB_ACTIONS).tobytes() == o.rollout(1, abi.RB_ACTIONS).tobytes()
+        for t in range(cfg.n_specs):
+            gm = g.ppo_update(t, pcfg, seed=77, update_index=upd)
+            om = o.ppo_update(t, pcfg, 77, upd)
+            for f, _ in abi.UpdateMetrics._fields_:
+                np.testing.assert_allclose(getattr(gm, f), getattr(om, f), rtol=1e-8, atol=1e-12,
+                                           err_msg=f"{upd} {t} {f}")
+            np.testing.assert_allclose(g.read_net(t), o.read_net(t), rtol=1e-8, atol=1e-12,
+                                       err_msg=f"params {upd} {t}")
