@@ -77,7 +77,7 @@ __device__ inline uint32_t* book_region(char* base, const DevCfg& c) {
 #define MLOB_PHASE_SYNC 1
 #endif
 #ifndef MLOB_SYNC_WARPS
-#define MLOB_SYNC_WARPS 10
+#define MLOB_SYNC_WARPS 24
 #endif
 #ifndef MLOB_SYNC_A  // barrier before the message loop (measured: no gain)
 #define MLOB_SYNC_A 0
@@ -89,7 +89,7 @@ __device__ inline uint32_t* book_region(char* base, const DevCfg& c) {
 #define MLOB_DEEP_SYNC 0
 #endif
 #ifndef MLOB_SYNC_REGS
-#define MLOB_SYNC_REGS 96
+#define MLOB_SYNC_REGS 80
 #endif
 template <int SPL>
 __host__ __device__ constexpr bool phase_sync() {
@@ -153,7 +153,9 @@ static_assert(sizeof(KParams) % 16 == 0, "KParams must be int4-copyable");
 template <int SPL>
 __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL>())
     step_kernel(const __grid_constant__ KParams kparam) {
-  constexpr int kWarpsPerBlock = warps_per_block<SPL>();
+  // warps per block: warps_per_block<SPL>() unless the config's shared memory
+  // per warp needs a smaller block (step_warps)
+  const int kWarpsPerBlock = static_cast<int>(blockDim.x) / kWarp;
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(16) StagedParams sp_;
   stage_params(sp_, kparam);
@@ -415,9 +417,19 @@ __global__ void clear_finished_kernel(EnvHdr* hdr, uint64_t n) {
 // ---------------------------------------------------------------------------
 // host-side launchers
 
+// warps per step-kernel block: the phase-sync width for register books, 4 for
+// shared-memory books, fewer when the config's per-warp shared memory
+// (obs depth, agents) would not fit the 227 KB block limit
+constexpr size_t kBlockSmemLimit = 227 * 1024 - sizeof(StagedParams) - 1024;
+static int step_warps(const DevCfg& c) {
+  const int want = spl_of(c.capacity) <= 8 && MLOB_PHASE_SYNC ? MLOB_SYNC_WARPS : 4;
+  const size_t per = warp_smem_bytes(c);
+  const int fit = static_cast<int>(kBlockSmemLimit / (per > 0 ? per : 1));
+  return fit < 1 ? 1 : (fit < want ? fit : want);
+}
+
 size_t step_smem_bytes(const DevCfg& c) {  // dynamic smem of the step kernel's block
-  const int wpb = spl_of(c.capacity) <= 8 && MLOB_PHASE_SYNC ? MLOB_SYNC_WARPS : 4;
-  return warp_smem_bytes(c) * wpb;
+  return warp_smem_bytes(c) * step_warps(c);
 }
 
 static unsigned grid_for(uint64_t n) {
@@ -427,7 +439,7 @@ static unsigned grid_for(uint64_t n) {
 
 template <int SPL>
 static cudaError_t launch_step_t(const KParams& kp, const DevCfg& cfg, cudaStream_t s) {
-  constexpr int kWarpsPerBlock = warps_per_block<SPL>();
+  const int kWarpsPerBlock = step_warps(cfg);
   const size_t sm = warp_smem_bytes(cfg) * kWarpsPerBlock;
   cudaError_t e = cudaFuncSetAttribute(step_kernel<SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sm));

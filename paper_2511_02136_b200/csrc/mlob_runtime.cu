@@ -829,8 +829,8 @@ mlob_status mlob_venv_create(const mlob_venv_desc* desc, mlob_venv** out) {
       v->d_env_index = v->alloc<uint64_t>(n, "env_index");
       cuda_check(cudaMemcpy(v->d_env_index, v->genv.data(), n * 8, cudaMemcpyHostToDevice), "H2D");
     }
-    if (step_smem_bytes(v->dcfg) > 227 * 1024)
-      fail(MLOB_E_INVALID_ARGUMENT, "configuration needs more shared memory than an SM has");
+    if (step_smem_bytes(v->dcfg) > 226 * 1024)
+      fail(MLOB_E_INVALID_ARGUMENT, "configuration needs more shared memory per env than an SM has");
     cuda_check(cudaDeviceSynchronize(), "create");
     *out = v.release();
   });

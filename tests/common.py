@@ -56,6 +56,13 @@ def scenario_configs():
     out["many_agents"] = (A.env_config(
         [A.agent_spec(A.MARKET_MAKER, count=5), A.agent_spec(A.EXECUTOR, count=5, task_size=200)],
         steps_per_episode=10, messages_per_step=100, start_stride_steps=10), {}, 10)
+    # 200 msgs/step (two replay chunks), MMFull at depth 64, 8 agents: ~15 KB of
+    # shared memory per warp forces the step kernel below its full block width
+    out["wide_smem"] = (A.env_config(
+        [A.agent_spec(A.MARKET_MAKER, count=4, obs_space=A.OBS_MM_FULL),
+         A.agent_spec(A.EXECUTOR, count=4, task_size=300)],
+        steps_per_episode=5, messages_per_step=200, start_stride_steps=5, obs_depth=64),
+        {"state_sample_every": 1000, "n_messages": 40000}, 5)
     out["deep_book"] = (A.env_config([mm, ex], steps_per_episode=8, messages_per_step=100,
                                      start_stride_steps=64, book_capacity=1000),
                         dict(DEEP_SYNTH, n_messages=80000, state_sample_every=6400), 8)
