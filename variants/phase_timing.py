@@ -22,3 +22,11 @@ d = np.diff(t[:, :10], axis=1)
 print(f"mps={mps}  total cycles/env-step (mean) {np.mean(t[:,9]-t[:,0]):.0f}")
 for i, nm in enumerate(names):
     print(f"  {nm:26s} mean {d[:, i].mean():9.0f}  p50 {np.median(d[:, i]):9.0f}")
+# barrier share: within each block (consecutive warps), the barrier releases at
+# about the latest pre-barrier stamp (clock64 is per SM, so comparable in-block)
+W = int(os.environ.get("MLOB_WPB", "24"))
+nb = n // W
+pre = t[: nb * W, 7].reshape(nb, W)
+rel = pre.max(axis=1, keepdims=True)
+wait = (rel - pre).mean()
+print(f"  barrier wait (est.)        mean {wait:9.0f}   outcomes after barrier {(t[:nb*W, 8] - np.repeat(rel, W, axis=1).reshape(-1)).mean():9.0f}")
