@@ -22,6 +22,10 @@ struct PpoArgs {
   const double* returns;
   const double* h0;
   const double* adv;  // [K] gathered (and normalized) advantages
+  // transposed copies for the forward's lane-coalesced reads (mlob_policy.h layout)
+  const double* w_ihT;
+  const double* w_hhT;
+  const double* w_actorT;
   // parameters, reference layout (net.hpp:18-30)
   const double* w_ih;
   const double* w_hh;

@@ -1328,6 +1328,9 @@ mlob_status mlob_venv_ppo_update(mlob_venv* v, int type, const mlob_ppo_config* 
         a.logp_old = bt.log_probs;
         a.returns = bt.ret;
         a.h0 = bt.h0;
+        a.w_ihT = ns.dn.w_ihT;
+        a.w_hhT = ns.dn.w_hhT;
+        a.w_actorT = ns.dn.w_actorT;
         a.w_ih = ns.p + o_wih;
         a.w_hh = ns.p + o_whh;
         a.b_ih = ns.p + o_bih;
@@ -1389,6 +1392,8 @@ mlob_status mlob_venv_ppo_update(mlob_venv* v, int type, const mlob_ppo_config* 
         cuda_check(launch_clip_adam(ns.p, ns.g, ns.m, ns.v, ns.P, cfg->max_grad_norm, cfg->lr, c1, c2, sums + 5,
                                     v->stream),
                    "adam");
+        // the next minibatch's forward reads the transposed copy
+        cuda_check(launch_to_inference(ns.p, D, H, A, ns.w, v->stream), "to_inference");
         double norm = 0.0;
         cuda_check(cudaMemcpyAsync(&norm, sums + 5, 8, cudaMemcpyDeviceToHost, v->stream), "D2H");
         cuda_check(cudaStreamSynchronize(v->stream), "sync");
