@@ -586,10 +586,26 @@ struct WarpEnv {
     SideT& d = sd<S>();
     m = kEmptySt;
     lk = 0;
-    MLOB_ROWS(k) {
-      const bool c = d.P(k) == price && d.ST(k) < m;
-      m = c ? d.ST(k) : m;
-      lk = c ? k : lk;
+    if constexpr (SMEM && SPL <= 32) {
+      // shared-memory book: one load per row for the price, the arrival word
+      // only for the (few) rows at that price
+      uint32_t cand = 0;
+      MLOB_ROWS(k) cand |= (d.P(k) == price ? 1u : 0u) << k;
+      while (cand) {
+        const int k = __ffs(cand) - 1;
+        cand &= cand - 1;
+        const uint32_t st = d.ST(k);
+        if (st < m) {
+          m = st;
+          lk = k;
+        }
+      }
+    } else {
+      MLOB_ROWS(k) {
+        const bool c = d.P(k) == price && d.ST(k) < m;
+        m = c ? d.ST(k) : m;
+        lk = c ? k : lk;
+      }
     }
   }
   // lane-local id match: first matching row and match count
@@ -598,10 +614,25 @@ struct WarpEnv {
     SideT& d = sd<S>();
     nm = 0;
     lk = 0;
-    MLOB_ROWS(k) {
-      const bool c = d.Q(k) > 0 && d.LO(k) == lo && d.HI(k) == hi;
-      lk = (c && nm == 0) ? k : lk;
-      nm += c ? 1 : 0;
+    if constexpr (SMEM && SPL <= 32) {
+      // shared-memory book: filter rows on the low id word (one load per row),
+      // then check the high word and liveness of the candidates only
+      uint32_t cand = 0;
+      MLOB_ROWS(k) cand |= (d.LO(k) == lo ? 1u : 0u) << k;
+      while (cand) {
+        const int k = __ffs(cand) - 1;
+        cand &= cand - 1;
+        if (d.HI(k) == hi && d.Q(k) > 0) {
+          if (nm == 0) lk = k;
+          ++nm;
+        }
+      }
+    } else {
+      MLOB_ROWS(k) {
+        const bool c = d.Q(k) > 0 && d.LO(k) == lo && d.HI(k) == hi;
+        lk = (c && nm == 0) ? k : lk;
+        nm += c ? 1 : 0;
+      }
     }
   }
   // lowest free position (row-major: row * 32 + lane) -> (row, lane), one
@@ -648,8 +679,12 @@ struct WarpEnv {
   __device__ __forceinline__ bool evict_t(int32_t price) {
     SideT& d = sd<S>();
     int32_t lw = S == 0 ? INT_MAX : INT_MIN;
-    MLOB_ROWS(k)
-      if (d.Q(k) > 0) lw = S == 0 ? min(lw, d.P(k)) : max(lw, d.P(k));
+    // live <=> price != the empty sentinel (live prices are range-checked to
+    // exclude INT_MIN / INT_MAX), so the shared-memory book reads one word per row
+    MLOB_ROWS(k) {
+      const int32_t pk = d.P(k);
+      if (SMEM ? pk != empty_price<S>() : d.Q(k) > 0) lw = S == 0 ? min(lw, pk) : max(lw, pk);
+    }
     const int32_t worst = S == 0 ? __reduce_min_sync(FULLMASK, lw) : __reduce_max_sync(FULLMASK, lw);
     const bool better = S == 0 ? price > worst : price < worst;
     if (!better) return false;

@@ -6,9 +6,15 @@ os.environ["MLOB_TIMING"] = "1"
 from paper_2511_02136_b200 import abi, env as E
 from bench import workload
 mps = int(sys.argv[1]) if len(sys.argv) > 1 else 100
-n, cfg, synth, _ = workload("C")
-cfg.messages_per_step = mps; synth.n_messages = (n + 64) * mps; synth.state_sample_every = mps
-dev = E.DeviceStore(E.HostStore.synth(synth, 0), 0)
+WL = os.environ.get("WL", "C")
+n, cfg, synth, _ = workload(WL)
+if WL != "D":
+    cfg.messages_per_step = mps; synth.n_messages = (n + 64) * mps; synth.state_sample_every = mps
+hs = E.HostStore.synth(synth, 0)
+if WL == "D":
+    hs.trim_front(16 * 6400)
+    n = int(os.environ.get("ENVS", "65536"))
+dev = E.DeviceStore(hs, 0)
 v = E.MarketVecEnv(dev, cfg, seed=0, n_envs=n)
 v.reset_all()
 L = E.lib(); L.mlob_venv_read_timing.argtypes = [C.c_void_p, C.c_void_p]
