@@ -19,7 +19,7 @@ __host__ __device__ inline size_t warp_smem_bytes(const DevCfg& c) {
   const int nbuf = c.mps > kChunk ? 2 : 1;
   size_t b = 0;
   b += static_cast<size_t>(nbuf) * chunk * sizeof(DevMsg);
-  b += 16;  // mbarriers
+  b += 32;  // 3 mbarriers
   b += static_cast<size_t>(4 * c.n_agents + 4) * sizeof(DevMsg);
   b += static_cast<size_t>(c.n_agents) * sizeof(AgentRec);
   b += static_cast<size_t>(c.n_agents) * kMaxActive * sizeof(ActiveRec);
@@ -42,7 +42,7 @@ __device__ WarpSmem carve(char* base, const DevCfg& c) {
   s.chunk1 = nbuf == 2 ? s.chunk0 + chunk : s.chunk0;
   p += static_cast<size_t>(nbuf) * chunk * sizeof(DevMsg);
   s.bar = reinterpret_cast<uint64_t*>(p);
-  p += 16;
+  p += 32;
   s.amsg = reinterpret_cast<DevMsg*>(p);
   p += static_cast<size_t>(4 * c.n_agents + 4) * sizeof(DevMsg);
   s.ag = reinterpret_cast<AgentRec*>(p);
@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL
   if (lane == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.bar[0])));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.bar[1])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.bar[2])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
@@ -204,6 +205,7 @@ __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL
       w.bind(env);
       PHASE(0);
       w.load_hdr();
+      w.book_load_issue();  // shared-memory books: bulk loads in flight during phase 1
       slice = kp.msgs + kp.ep_start[w.episode] + static_cast<uint64_t>(w.step) * mps;
       if (nch >= 2) w.stage(slice + kChunk, min(kChunk, mps - kChunk));
       if (has_next) {
@@ -255,7 +257,7 @@ __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL
     if (!idle) {  // ---- phase 2: book in registers, message loop, book out
       // book registers are loaded only now: nothing above needs them (tops are
       // in the header) and they must not be live across subroutine calls
-      w.load_book();
+      w.book_load_wait();
       // (3) + (4): agent messages, then the replay slice
       w.prev_mid_half = w.mid_half;
       w.mid_sum = 0;
@@ -317,6 +319,7 @@ __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL
     env = nenv;
     if (has_next) nenv = ticket();
   }
+  w.book_store_drain();
   w.report_errors();
 }
 
@@ -347,6 +350,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * kWarp)
   }
   w.cursor = 1;
   w.store_state(1);
+  w.book_store_drain();
   w.report_errors();
 }
 

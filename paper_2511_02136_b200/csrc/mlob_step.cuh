@@ -159,22 +159,23 @@ struct RegSide {
 // plain indexed accesses.
 template <int SPL>
 struct SmemSide {
+  // the HBM book layout of one side (KParams::bk_*): p[SPL*32], q[SPL*32],
+  // id[SPL*32] as uint2, st[SPL*32] — so whole arrays move with bulk copies
+  uint32_t* base_;
   int32_t* p_;
   int32_t* q_;
-  uint32_t* lo_;
-  uint32_t* hi_;
+  uint2* id_;
   uint32_t* st_;
   __device__ __forceinline__ int32_t P(int k) const { return p_[k * 32]; }
   __device__ __forceinline__ int32_t Q(int k) const { return q_[k * 32]; }
-  __device__ __forceinline__ uint32_t LO(int k) const { return lo_[k * 32]; }
-  __device__ __forceinline__ uint32_t HI(int k) const { return hi_[k * 32]; }
+  __device__ __forceinline__ uint32_t LO(int k) const { return id_[k * 32].x; }
+  __device__ __forceinline__ uint32_t HI(int k) const { return id_[k * 32].y; }
   __device__ __forceinline__ uint32_t ST(int k) const { return st_[k * 32]; }
   __device__ __forceinline__ void put(int k, int32_t p, int32_t q, uint32_t lo, uint32_t hi,
                                       uint32_t st) {
     p_[k * 32] = p;
     q_[k * 32] = q;
-    lo_[k * 32] = lo;
-    hi_[k * 32] = hi;
+    id_[k * 32] = make_uint2(lo, hi);
     st_[k * 32] = st;
   }
   __device__ __forceinline__ void get_pq(int k, int32_t& p, int32_t& q) const {
@@ -183,8 +184,9 @@ struct SmemSide {
   }
   __device__ __forceinline__ void get_qid(int k, int32_t& q, uint32_t& lo, uint32_t& hi) const {
     q = q_[k * 32];
-    lo = lo_[k * 32];
-    hi = hi_[k * 32];
+    const uint2 id = id_[k * 32];
+    lo = id.x;
+    hi = id.y;
   }
   __device__ __forceinline__ void set(int k, bool pred, int32_t p, int32_t q, uint32_t lo,
                                       uint32_t hi, uint32_t st) {
@@ -204,11 +206,11 @@ struct SmemSide {
       st_[k * 32] = kEmptySt;
     }
   }
-  __device__ __forceinline__ void bind(uint32_t* base, int lane) {  // 5 arrays of SPL*32 words
+  __device__ __forceinline__ void bind(uint32_t* base, int lane) {  // 5 x SPL*32 words
+    base_ = base;
     p_ = reinterpret_cast<int32_t*>(base) + lane;
     q_ = reinterpret_cast<int32_t*>(base + SPL * 32) + lane;
-    lo_ = base + 2 * SPL * 32 + lane;
-    hi_ = base + 3 * SPL * 32 + lane;
+    id_ = reinterpret_cast<uint2*>(base + 2 * SPL * 32) + lane;
     st_ = base + 4 * SPL * 32 + lane;
   }
 };
@@ -259,7 +261,7 @@ struct L2Lvl {
 struct WarpSmem {
   DevMsg* chunk0;  // replay chunk buffers (no array: keeps WarpEnv promotable to registers)
   DevMsg* chunk1;
-  uint64_t* bar;  // 2 mbarriers
+  uint64_t* bar;  // mbarriers: [0], [1] replay chunks, [2] shared-memory book load
   DevMsg* amsg;   // agent messages (<= 4 * A)
   AgentRec* ag;
   ActiveRec* act;
@@ -303,6 +305,24 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
+// bulk copy global -> shared completing on `bar` without an arrive (the
+// caller arrives once with the total byte count)
+__device__ __forceinline__ void bulk_load_tx(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// bulk copy shared -> global (bulk async-group)
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n.reg .pred p;\nWAIT_%=:\n"
@@ -453,13 +473,27 @@ struct WarpEnv {
       const uint32_t b = __ballot_sync(FULLMASK, d.Q(k) > 0);
       if (b) hwm = k * kWarp + 32 - __clz(b);
     }
-    MLOB_ROWS(k) {
-      if (k * kWarp < hwm) {
-        const size_t i = row_index(S, k);
-        kp.bk_p[i] = d.P(k);
-        kp.bk_q[i] = d.Q(k);
-        kp.bk_id[i] = make_uint2(d.LO(k), d.HI(k));
-        kp.bk_st[i] = d.ST(k);
+    if constexpr (SMEM) {  // rows below the high-water mark: four bulk stores
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // lanes' smem writes -> async proxy
+      __syncwarp();
+      const uint32_t rows = static_cast<uint32_t>((hwm + kWarp - 1) / kWarp);
+      if (lane == 0 && rows) {
+        const size_t g = (env * 2 + S) * SPL * kWarp;
+        const uint32_t* b = d.base_;
+        bulk_store(kp.bk_p + g, b, rows * kWarp * 4);
+        bulk_store(kp.bk_q + g, b + SPL * kWarp, rows * kWarp * 4);
+        bulk_store(kp.bk_id + g, b + 2 * SPL * kWarp, rows * kWarp * 8);
+        bulk_store(kp.bk_st + g, b + 4 * SPL * kWarp, rows * kWarp * 4);
+      }
+    } else {
+      MLOB_ROWS(k) {
+        if (k * kWarp < hwm) {
+          const size_t i = row_index(S, k);
+          kp.bk_p[i] = d.P(k);
+          kp.bk_q[i] = d.Q(k);
+          kp.bk_id[i] = make_uint2(d.LO(k), d.HI(k));
+          kp.bk_st[i] = d.ST(k);
+        }
       }
     }
     return hwm;
@@ -511,9 +545,57 @@ struct WarpEnv {
     ++q_consumed;
     return b ? sm.chunk1 : sm.chunk0;
   }
+  // Shared-memory books: the rows below each side's high-water mark arrive by
+  // bulk copies issued right after the header (they overlap the action
+  // conversion); lanes fill the rows above with empty slots.  Register books
+  // load at book_load_wait().
+  uint32_t book_loads = 0;  // mbarrier [2] phase
+  __device__ __forceinline__ void book_load_issue() {
+    if constexpr (SMEM) {
+      const EnvHdr& h = kp.hdr[env];
+      const int rows0 = (h.hwm[0] + kWarp - 1) / kWarp, rows1 = (h.hwm[1] + kWarp - 1) / kWarp;
+      for (int k = rows0; k < SPL; ++k) bid.put(k, INT_MIN, 0, 0, 0, kEmptySt);
+      for (int k = rows1; k < SPL; ++k) ask.put(k, INT_MAX, 0, 0, 0, kEmptySt);
+      if (lane == 0) {
+        bar_arrive_tx(&sm.bar[2], static_cast<uint32_t>(rows0 + rows1) * kWarp * 20u);
+#pragma unroll
+        for (int S = 0; S < 2; ++S) {
+          const uint32_t rows = static_cast<uint32_t>(S ? rows1 : rows0);
+          if (rows == 0) continue;
+          const size_t g = (env * 2 + S) * SPL * kWarp;
+          uint32_t* b = S ? ask.base_ : bid.base_;
+          bulk_load_tx(b, kp.bk_p + g, rows * kWarp * 4, &sm.bar[2]);
+          bulk_load_tx(b + SPL * kWarp, kp.bk_q + g, rows * kWarp * 4, &sm.bar[2]);
+          bulk_load_tx(b + 2 * SPL * kWarp, kp.bk_id + g, rows * kWarp * 8, &sm.bar[2]);
+          bulk_load_tx(b + 4 * SPL * kWarp, kp.bk_st + g, rows * kWarp * 4, &sm.bar[2]);
+        }
+      }
+    }
+  }
+  __device__ __forceinline__ void book_load_wait() {
+    if constexpr (SMEM) {
+      bar_wait(&sm.bar[2], book_loads & 1);
+      ++book_loads;
+      __syncwarp();
+    } else {
+      load_book();
+    }
+  }
   __device__ __forceinline__ void store_book() {
     hwm0 = store_side<0>();
     hwm1 = store_side<1>();
+    if constexpr (SMEM) {  // the bulk stores must have read the rows before they change
+      if (lane == 0) {
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+      __syncwarp();
+    }
+  }
+  __device__ __forceinline__ void book_store_drain() {  // before the kernel ends
+    if constexpr (SMEM) {
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
   }
   __device__ __forceinline__ void store_state(uint8_t just_reset) {
     const int h0 = hwm0, h1 = hwm1;
