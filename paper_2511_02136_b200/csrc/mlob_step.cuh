@@ -166,6 +166,18 @@ struct SmemSide {
   int32_t* q_;
   uint2* id_;
   uint32_t* st_;
+  uint32_t occ;  // this lane's occupied rows (bit k = row k), kept by every mutator
+  __device__ __forceinline__ void occ_set(int k, bool on) {
+    const uint32_t b = 1u << k;
+    occ = on ? (occ | b) : (occ & ~b);
+  }
+  __device__ __forceinline__ uint32_t free_mask() const {
+    return ~occ & (SPL >= 32 ? 0xffffffffu : ((1u << SPL) - 1u));
+  }
+  __device__ __forceinline__ void recompute_occ() {
+    occ = 0;
+    for (int k = 0; k < SPL; ++k) occ |= (q_[k * 32] > 0 ? 1u : 0u) << k;
+  }
   __device__ __forceinline__ int32_t P(int k) const { return p_[k * 32]; }
   __device__ __forceinline__ int32_t Q(int k) const { return q_[k * 32]; }
   __device__ __forceinline__ uint32_t LO(int k) const { return id_[k * 32].x; }
@@ -177,6 +189,7 @@ struct SmemSide {
     q_[k * 32] = q;
     id_[k * 32] = make_uint2(lo, hi);
     st_[k * 32] = st;
+    occ_set(k, q > 0);
   }
   __device__ __forceinline__ void get_pq(int k, int32_t& p, int32_t& q) const {
     p = p_[k * 32];
@@ -204,6 +217,7 @@ struct SmemSide {
       p_[k * 32] = empty_p;
       q_[k * 32] = 0;
       st_[k * 32] = kEmptySt;
+      occ_set(k, false);
     }
   }
   __device__ __forceinline__ void bind(uint32_t* base, int lane) {  // 5 x SPL*32 words
@@ -577,6 +591,8 @@ struct WarpEnv {
       bar_wait(&sm.bar[2], book_loads & 1);
       ++book_loads;
       __syncwarp();
+      bid.recompute_occ();
+      ask.recompute_occ();
     } else {
       load_book();
     }
@@ -723,7 +739,10 @@ struct WarpEnv {
   __device__ __forceinline__ void free_slot_t(int& pk, int& pl) {
     SideT& d = sd<S>();
     uint32_t fm = 0;
-    MLOB_ROWS(k) fm |= (d.Q(k) == 0 ? 1u : 0u) << k;
+    if constexpr (SMEM)
+      fm = d.free_mask();  // maintained occupancy: no row scan
+    else
+      MLOB_ROWS(k) fm |= (d.Q(k) == 0 ? 1u : 0u) << k;
     const uint32_t key = fm ? (static_cast<uint32_t>(__ffs(fm) - 1) << 5) | static_cast<uint32_t>(lane)
                             : 0xffffffffu;
     const uint32_t g = __reduce_min_sync(FULLMASK, key);
