@@ -167,6 +167,12 @@ struct SmemSide {
   uint2* id_;
   uint32_t* st_;
   uint32_t occ;  // this lane's occupied rows (bit k = row k), kept by every mutator
+  // this lane's worst live price (bids: lowest, asks: highest; identity when
+  // none), widened on inserts; a removal at that price marks it stale
+  int32_t lw;
+  uint32_t lw_stale;
+  int side_;
+  __device__ __forceinline__ int32_t worse(int32_t a, int32_t b) const { return side_ ? max(a, b) : min(a, b); }
   __device__ __forceinline__ void occ_set(int k, bool on) {
     const uint32_t b = 1u << k;
     occ = on ? (occ | b) : (occ & ~b);
@@ -174,9 +180,16 @@ struct SmemSide {
   __device__ __forceinline__ uint32_t free_mask() const {
     return ~occ & (SPL >= 32 ? 0xffffffffu : ((1u << SPL) - 1u));
   }
+  __device__ __forceinline__ void refresh_lw() {
+    lw = side_ ? INT_MIN : INT_MAX;
+    for (int k = 0; k < SPL; ++k)
+      if (q_[k * 32] > 0) lw = worse(lw, p_[k * 32]);
+    lw_stale = 0;
+  }
   __device__ __forceinline__ void recompute_occ() {
     occ = 0;
     for (int k = 0; k < SPL; ++k) occ |= (q_[k * 32] > 0 ? 1u : 0u) << k;
+    refresh_lw();
   }
   __device__ __forceinline__ int32_t P(int k) const { return p_[k * 32]; }
   __device__ __forceinline__ int32_t Q(int k) const { return q_[k * 32]; }
@@ -190,6 +203,7 @@ struct SmemSide {
     id_[k * 32] = make_uint2(lo, hi);
     st_[k * 32] = st;
     occ_set(k, q > 0);
+    if (q > 0) lw = worse(lw, p);
   }
   __device__ __forceinline__ void get_pq(int k, int32_t& p, int32_t& q) const {
     p = p_[k * 32];
@@ -214,13 +228,18 @@ struct SmemSide {
   }
   __device__ __forceinline__ void clear(int k, bool pred, int32_t empty_p) {
     if (pred) {
+      if (p_[k * 32] == lw) lw_stale = 1;
       p_[k * 32] = empty_p;
       q_[k * 32] = 0;
       st_[k * 32] = kEmptySt;
       occ_set(k, false);
     }
   }
-  __device__ __forceinline__ void bind(uint32_t* base, int lane) {  // 5 x SPL*32 words
+  __device__ __forceinline__ void bind(uint32_t* base, int lane, int side) {  // 5 x SPL*32 words
+    side_ = side;
+    lw = side ? INT_MIN : INT_MAX;
+    lw_stale = 1;
+    occ = 0;
     base_ = base;
     p_ = reinterpret_cast<int32_t*>(base) + lane;
     q_ = reinterpret_cast<int32_t*>(base + SPL * 32) + lane;
@@ -438,8 +457,8 @@ struct WarpEnv {
                      uint32_t* book_smem)
       : kp(p), cfg(c), sm(s), lane(ln), env(e) {
     if constexpr (SMEM) {
-      bid.bind(book_smem, ln);
-      ask.bind(book_smem + 5 * SPL * 32, ln);
+      bid.bind(book_smem, ln, 0);
+      ask.bind(book_smem + 5 * SPL * 32, ln, 1);
     }
     bind(e);
     err = 0;
@@ -538,6 +557,10 @@ struct WarpEnv {
     const EnvHdr& h = kp.hdr[env];
     load_side<0>(h.hwm[0]);
     load_side<1>(h.hwm[1]);
+    if constexpr (SMEM) {
+      bid.recompute_occ();
+      ask.recompute_occ();
+    }
   }
   int hwm0, hwm1;
   // chunk stager: copy #q goes to buffer q & 1 and completes phase (q >> 1) & 1
@@ -780,11 +803,14 @@ struct WarpEnv {
   __device__ __forceinline__ bool evict_t(int32_t price) {
     SideT& d = sd<S>();
     int32_t lw = S == 0 ? INT_MAX : INT_MIN;
-    // live <=> price != the empty sentinel (live prices are range-checked to
-    // exclude INT_MIN / INT_MAX), so the shared-memory book reads one word per row
-    MLOB_ROWS(k) {
-      const int32_t pk = d.P(k);
-      if (SMEM ? pk != empty_price<S>() : d.Q(k) > 0) lw = S == 0 ? min(lw, pk) : max(lw, pk);
+    if constexpr (SMEM) {  // the side's cached per-lane worst, rescanned by stale lanes only
+      if (__any_sync(FULLMASK, d.lw_stale)) {
+        if (d.lw_stale) d.refresh_lw();
+        __syncwarp();
+      }
+      lw = d.lw;
+    } else {
+      MLOB_ROWS(k) if (d.Q(k) > 0) lw = S == 0 ? min(lw, d.P(k)) : max(lw, d.P(k));
     }
     const int32_t worst = S == 0 ? __reduce_min_sync(FULLMASK, lw) : __reduce_max_sync(FULLMASK, lw);
     const bool better = S == 0 ? price > worst : price < worst;
@@ -1671,6 +1697,7 @@ struct WarpEnv {
         d.put(k, empty_price<S>(), 0, 0, 0, kEmptySt);
       }
     }
+    if constexpr (SMEM) d.recompute_occ();  // occupancy + cached worst of the new book
   }
 
   __device__ __forceinline__ uint64_t episode_for(uint64_t k) const {  // rollout.hpp:286-288

@@ -63,6 +63,11 @@ def scenario_configs():
          A.agent_spec(A.EXECUTOR, count=4, task_size=300)],
         steps_per_episode=5, messages_per_step=200, start_stride_steps=5, obs_depth=64),
         {"state_sample_every": 1000, "n_messages": 40000}, 5)
+    # shared-memory book (capacity 300 -> 16 rows/lane) that runs full: every
+    # better-priced newcomer evicts (book.hpp:174-181) through the cached worst
+    out["deep_evict"] = (A.env_config([mm, ex], steps_per_episode=16, messages_per_step=100,
+                                      start_stride_steps=32, book_capacity=300),
+                         dict(DEEP_SYNTH, n_messages=40000, state_sample_every=3200, state_depth=200), 16)
     out["deep_book"] = (A.env_config([mm, ex], steps_per_episode=8, messages_per_step=100,
                                      start_stride_steps=64, book_capacity=1000),
                         dict(DEEP_SYNTH, n_messages=80000, state_sample_every=6400), 8)
