@@ -113,15 +113,17 @@ __global__ void __launch_bounds__(kPolicyWarps * 32) policy_kernel(const PolicyA
     pa.env_actions[slot] = best;
     return;
   }
-  double v = nt.b_critic;  // critic head, net.hpp:180-182
+  double v = nt.b_critic_dev ? *nt.b_critic_dev : nt.b_critic;  // critic head, net.hpp:180-182
   for (int j = 0; j < H; ++j) v += nt.w_critic[j] * sn[j];
   pa.values[static_cast<uint64_t>(pa.row) * B + s] = v;
   if (!pa.sample) return;
   pa.resets[static_cast<uint64_t>(pa.row) * B + s] = reset;
   // sample_categorical (ppo.hpp:80-98), u = CounterRng(make_key(seed, ActionSample,
   // tau, update, t, s)).uniform() (rollout.hpp:88-93)
-  uint64_t key = pol_fold(pol_fold(pol_splitmix64(pa.seed), 3), static_cast<uint64_t>(pa.type));
-  key = pol_fold(pol_fold(pol_fold(key, pa.update_index), static_cast<uint64_t>(pa.row)), s);
+  const uint64_t seed = pa.seed_update ? pa.seed_update[0] : pa.seed;
+  const uint64_t update = pa.seed_update ? pa.seed_update[1] : pa.update_index;
+  uint64_t key = pol_fold(pol_fold(pol_splitmix64(seed), 3), static_cast<uint64_t>(pa.type));
+  key = pol_fold(pol_fold(pol_fold(key, update), static_cast<uint64_t>(pa.row)), s);
   const double u = static_cast<double>(pol_splitmix64(key + 0x9E3779B97F4A7C15ull) >> 11) * 0x1.0p-53;
   const double* lg = sl;
   double max_l = lg[0];

@@ -28,6 +28,7 @@ struct DevNet {
   const double* b_actor;
   const double* w_critic;
   double b_critic;
+  const double* b_critic_dev;  // non-null: b_critic read from device memory (kept current by ppo_update)
 };
 
 struct PolicyArgs {
@@ -42,6 +43,7 @@ struct PolicyArgs {
   const uint8_t* env_policy;  // [env * n_specs + type]
   int32_t n_specs, filter;
   uint64_t seed, update_index;
+  const uint64_t* seed_update;  // non-null: {seed, update_index} read from device memory (graph replays)
   // env side
   const double* obs_env;      // the type's observation buffer, [s * D]
   const uint8_t* just_reset;  // [env]; null = no reset (evaluate.hpp:83)

@@ -165,6 +165,12 @@ struct mlob_venv {
   NetState nets[MLOB_MAX_SPECS];
   Batch batch[MLOB_MAX_SPECS];
   bool has_nets = false;
+  // collect_rollout as a CUDA graph: captured once per (T, hidden-buffer
+  // parities, buffer version), replayed with {seed, update} in device memory
+  cudaGraphExec_t roll_graph = nullptr;
+  uint64_t roll_key = ~0ull;
+  uint64_t buf_version = 0;  // bumped whenever a net / batch buffer is reallocated
+  uint64_t* d_seed_update = nullptr;
   std::vector<NetState> eval_nets;  // evaluate_matrix: one per Learned option
   std::vector<uint64_t> starts;
   std::vector<EpState> ep_state;
@@ -226,6 +232,7 @@ struct mlob_venv {
       cudaFree(batch[t].arena);
     }
     for (NetState& n : eval_nets) free_net(n);
+    if (roll_graph) cudaGraphExecDestroy(roll_graph);
     cudaFree(ppo_ws);
     if (blas) cublasDestroy(blas);
     for (void* p : allocs) cudaFree(p);
@@ -1067,6 +1074,7 @@ static void upload_net(mlob_venv* v, const mlob_policy_net& n, mlob_venv::NetSta
   flat.insert(flat.end(), n.w_critic, n.w_critic + H);
   flat.push_back(n.b_critic);
   if (!same_shape) {
+    ++v->buf_version;
     mlob_venv::free_net(ns);
     cuda_check(cudaMalloc(&ns.p, P * 8), "cudaMalloc(params)");
     cuda_check(cudaMalloc(&ns.g, P * 8), "cudaMalloc(grad)");
@@ -1095,6 +1103,7 @@ static void upload_net(mlob_venv* v, const mlob_policy_net& n, mlob_venv::NetSta
   ns.dn.b_actor = base + (b_a - w.data());
   ns.dn.w_critic = base + (w_c - w.data());
   ns.dn.b_critic = n.b_critic;
+  ns.dn.b_critic_dev = ns.p + (P - 1);  // the reference layout ends with b_critic
   cuda_check(cudaStreamSynchronize(v->stream), "sync");  // `w` is a host temporary
 }
 
@@ -1113,6 +1122,7 @@ static void ensure_batch(mlob_venv* v, int t, uint64_t T) {
   mlob_venv::Batch& b = v->batch[t];
   const uint64_t B = v->n_envs * static_cast<uint64_t>(v->cfg.specs[t].count);
   if (b.arena && b.T == T && b.B == B) return;
+  ++v->buf_version;
   cudaFree(b.arena);
   b = mlob_venv::Batch{};
   const uint64_t D = v->nets[t].dn.D, H = v->nets[t].dn.H, TB = T * B;
@@ -1157,6 +1167,46 @@ static PolicyArgs policy_args(mlob_venv* v, int t, const mlob_rollout_config& c,
   return pa;
 }
 
+// The launches of one rollout (rollout.hpp:64-123): per step, one policy
+// launch per type then the env step; then bootstrap values and GAE.
+static void enqueue_rollout(mlob_venv* v, const mlob_rollout_config& cfg, uint64_t update_index, uint64_t T,
+                            const uint64_t* seed_update) {
+  const int NT = v->cfg.n_specs;
+  for (uint64_t step = 0; step < T; ++step) {
+    for (int t = 0; t < NT; ++t) {  // gather + policy_forward + sample + set_action
+      mlob_venv::NetState& ns = v->nets[t];
+      mlob_venv::Batch& b = v->batch[t];
+      PolicyArgs pa = policy_args(v, t, cfg, update_index);
+      pa.seed_update = seed_update;
+      pa.row = static_cast<int32_t>(step);
+      pa.prev_row = static_cast<int32_t>(step) - 1;
+      pa.sample = 1;
+      pa.hidden_in = ns.hidden[ns.cur];
+      pa.hidden_out = ns.hidden[ns.cur ^ 1];
+      pa.h0_out = step == 0 ? b.h0 : nullptr;
+      pa.obs_out = b.obs + step * b.B * static_cast<uint64_t>(ns.dn.D);
+      cuda_check(launch_policy(pa, v->stream), "policy kernel");
+      ns.cur ^= 1;
+    }
+    KParams kp = v->params();  // step_all (rollout.hpp:92)
+    kp.action_mode = kActIds;
+    cuda_check(launch_step(kp, v->dcfg, v->spl, v->stream), "step kernel");
+  }
+  for (int t = 0; t < NT; ++t) {  // bootstrap values (hidden untouched), then GAE
+    mlob_venv::NetState& ns = v->nets[t];
+    mlob_venv::Batch& b = v->batch[t];
+    PolicyArgs pa = policy_args(v, t, cfg, update_index);
+    pa.seed_update = seed_update;
+    pa.row = static_cast<int32_t>(T);
+    pa.prev_row = static_cast<int32_t>(T) - 1;
+    pa.sample = 0;
+    pa.hidden_in = ns.hidden[ns.cur];
+    cuda_check(launch_policy(pa, v->stream), "policy kernel");
+    cuda_check(launch_gae(b.rewards, b.values, b.dones, T, b.B, cfg.discount, cfg.gae_lambda, b.adv, b.ret,
+                          v->stream), "gae kernel");
+  }
+}
+
 mlob_status mlob_venv_collect_rollout(mlob_venv* v, const mlob_rollout_config* cfg, uint64_t update_index) {
   return guarded([&] {
     if (!cfg || cfg->rollout_len < 1) fail(MLOB_E_INVALID_ARGUMENT, "collect_rollout: rollout_len >= 1");
@@ -1167,37 +1217,49 @@ mlob_status mlob_venv_collect_rollout(mlob_venv* v, const mlob_rollout_config* c
     const uint64_t T = static_cast<uint64_t>(cfg->rollout_len);
     const int NT = v->cfg.n_specs;
     for (int t = 0; t < NT; ++t) ensure_batch(v, t, T);
-    for (uint64_t step = 0; step < T; ++step) {
-      for (int t = 0; t < NT; ++t) {  // gather + policy_forward + sample + set_action
-        mlob_venv::NetState& ns = v->nets[t];
-        mlob_venv::Batch& b = v->batch[t];
-        PolicyArgs pa = policy_args(v, t, *cfg, update_index);
-        pa.row = static_cast<int32_t>(step);
-        pa.prev_row = static_cast<int32_t>(step) - 1;
-        pa.sample = 1;
-        pa.hidden_in = ns.hidden[ns.cur];
-        pa.hidden_out = ns.hidden[ns.cur ^ 1];
-        pa.h0_out = step == 0 ? b.h0 : nullptr;
-        pa.obs_out = b.obs + step * b.B * static_cast<uint64_t>(ns.dn.D);
-        cuda_check(launch_policy(pa, v->stream), "policy kernel");
-        ++v->launches;
-        ns.cur ^= 1;
+    const uint64_t launches = T * (NT + 1) + 2 * NT;
+    if (std::getenv("MLOB_NO_GRAPH")) {  // diagnostics: plain launches
+      enqueue_rollout(v, *cfg, update_index, T, nullptr);
+    } else {
+      if (!v->d_seed_update) v->d_seed_update = v->alloc<uint64_t>(2, "seed/update");
+      const uint64_t su[2] = {cfg->seed, update_index};
+      cuda_check(cudaMemcpyAsync(v->d_seed_update, su, sizeof su, cudaMemcpyHostToDevice, v->stream), "H2D");
+      // graph key: T, the hidden-buffer parity of every type, the buffer version,
+      // and the GAE constants baked into the captured launches
+      uint64_t key = T * 1315423911ull ^ v->buf_version * 2654435761ull;
+      for (int t = 0; t < NT; ++t) key ^= static_cast<uint64_t>(v->nets[t].cur) << (40 + t);
+      uint64_t dbits, lbits;
+      std::memcpy(&dbits, &cfg->discount, 8);
+      std::memcpy(&lbits, &cfg->gae_lambda, 8);
+      key ^= host_splitmix(dbits) ^ host_splitmix(lbits + 1);
+      if (!v->roll_graph || v->roll_key != key) {
+        if (v->roll_graph) cudaGraphExecDestroy(v->roll_graph);
+        v->roll_graph = nullptr;
+        int cur[MLOB_MAX_SPECS];
+        for (int t = 0; t < NT; ++t) cur[t] = v->nets[t].cur;
+        cudaGraph_t g = nullptr;
+        cuda_check(cudaStreamSynchronize(v->stream), "sync");
+        cuda_check(cudaStreamBeginCapture(v->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+        try {
+          enqueue_rollout(v, *cfg, update_index, T, v->d_seed_update);
+        } catch (...) {
+          cudaStreamEndCapture(v->stream, &g);
+          if (g) cudaGraphDestroy(g);
+          throw;
+        }
+        cuda_check(cudaStreamEndCapture(v->stream, &g), "end capture");
+        const cudaError_t e = cudaGraphInstantiate(&v->roll_graph, g, 0);
+        cudaGraphDestroy(g);
+        cuda_check(e, "graph instantiate");
+        for (int t = 0; t < NT; ++t) v->nets[t].cur = cur[t];  // replay advances them below
+        v->roll_key = key;
       }
-      do_step(v, kActIds, 0, 0);  // step_all
+      cuda_check(cudaGraphLaunch(v->roll_graph, v->stream), "graph launch");
+      for (int t = 0; t < NT; ++t)
+        if (T & 1) v->nets[t].cur ^= 1;
     }
-    for (int t = 0; t < NT; ++t) {  // bootstrap values (hidden untouched), then GAE
-      mlob_venv::NetState& ns = v->nets[t];
-      mlob_venv::Batch& b = v->batch[t];
-      PolicyArgs pa = policy_args(v, t, *cfg, update_index);
-      pa.row = static_cast<int32_t>(T);
-      pa.prev_row = static_cast<int32_t>(T) - 1;
-      pa.sample = 0;
-      pa.hidden_in = ns.hidden[ns.cur];
-      cuda_check(launch_policy(pa, v->stream), "policy kernel");
-      cuda_check(launch_gae(b.rewards, b.values, b.dones, T, b.B, cfg->discount, cfg->gae_lambda, b.adv, b.ret,
-                            v->stream), "gae kernel");
-      v->launches += 2;
-    }
+    for (uint64_t i = 0; i < T; ++i) advance_step(v);
+    v->launches += launches;
     v->action_mode = kActIds;
   });
 }

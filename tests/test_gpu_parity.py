@@ -487,3 +487,30 @@ def test_ppo_update_matches_reference(ref):
                                            err_msg=f"{upd} {t} {f}")
             np.testing.assert_allclose(g.read_net(t), o.read_net(t), rtol=1e-8, atol=1e-12,
                                        err_msg=f"params {upd} {t}")
+
+
+def test_rollout_graph_replay_matches_plain_launches(monkeypatch):
+    """collect_rollout replayed from its captured CUDA graph (seed / update read
+    from device memory, odd T flipping the hidden-buffer parity, weights
+    re-uploaded and PPO-updated between rollouts) equals plain launches."""
+    from oracle.oracle import Oracle
+    from tests.common import rollout_case
+    orc = Oracle("orc")
+    cfg, synth_kw, nets = rollout_case(orc)
+    envs = []
+    for _ in range(2):
+        v = MarketVecEnv(dev_store(synth_kw), cfg, seed=3, n_envs=7)
+        v.reset_all()
+        v.set_nets(nets)
+        envs.append(v)
+    outs = [[], []]
+    for i, v in enumerate(envs):
+        if i == 1:
+            monkeypatch.setenv("MLOB_NO_GRAPH", "1")
+        for upd, T in ((1, 5), (2, 5), (3, 6), (4, 5)):
+            v.collect_rollout(T, 0.99, 0.95, seed=11, update_index=upd)
+            outs[i] += [v.rollout(t, f).tobytes() for t in range(2) for f in range(11)]
+            if upd == 2:
+                v.ppo_update(0, abi.ppo_config(epochs=1, minibatches=1), seed=5, update_index=upd)
+        monkeypatch.delenv("MLOB_NO_GRAPH", raising=False)
+    assert outs[0] == outs[1]
