@@ -293,6 +293,7 @@ def gpu_arm(args) -> None:
     avg_launch_s = ms / 1e3 / max(1, launches)
     achieved = bmsg * per_launch_msgs / avg_launch_s / 1e9
     traffic = None
+    prof = {}
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             prof = json.load(f)
@@ -311,7 +312,11 @@ def gpu_arm(args) -> None:
            "env_steps_per_s": env_steps,
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                         "frac": achieved / peak, "traffic": traffic,
-                        "bytes_per_msg": bmsg, "peak_kind": peak_kind},
+                        "bytes_per_msg": bmsg, "peak_kind": peak_kind,
+                        # from the committed ncu capture (profiles/ncu_summary.json): the
+                        # resource that actually binds the step
+                        "alu_pipe_pct_of_peak": prof.get("alu_pipe_pct_of_peak"),
+                        "issue_active_pct": prof.get("issue_active_pct")},
            "gpu_launches": launches,
            "clocks": clocks.summary(),
            "episode_stats": {"episodes": float(stats[4].item())},
