@@ -445,21 +445,31 @@ template <int SPL>
 static cudaError_t launch_step_t(const KParams& kp, const DevCfg& cfg, cudaStream_t s) {
   const int kWarpsPerBlock = step_warps(cfg);
   const size_t sm = warp_smem_bytes(cfg) * kWarpsPerBlock;
-  cudaError_t e = cudaFuncSetAttribute(step_kernel<SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(sm));
+  // the dynamic-smem opt-in only grows (a per-process cache per instantiation:
+  // small launches are host-bound, so no attribute call per launch)
+  static size_t sm_set[64] = {};
+  int cur_dev = 0;
+  cudaError_t e = cudaGetDevice(&cur_dev);
   if (e != cudaSuccess) return e;
-  // persistent grid: every SM filled to its occupancy limit, warps loop over envs
-  int dev = 0, n_sm = 0, per_sm = 0;
-  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-  if ((e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<SPL>, kWarpsPerBlock * kWarp,
-                                                         sm)) != cudaSuccess)
-    return e;
+  size_t& done = sm_set[cur_dev & 63];
+  if (sm > done) {
+    e = cudaFuncSetAttribute(step_kernel<SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    if (e != cudaSuccess) return e;
+    done = sm;
+  }
   const uint64_t need = (kp.n_envs + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  const uint64_t cap = static_cast<uint64_t>(n_sm) * (per_sm > 0 ? per_sm : 1);
-  const unsigned blocks =
-      static_cast<unsigned>((MLOB_PERSIST && !phase_sync<SPL>()) ? (need < cap ? need : cap) : need);
-  step_kernel<SPL><<<blocks, kWarpsPerBlock * kWarp, sm, s>>>(kp);
+  uint64_t blocks = need;
+  if (MLOB_PERSIST && !phase_sync<SPL>()) {  // persistent grid: every SM filled to its occupancy limit
+    int dev = 0, n_sm = 0, per_sm = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<SPL>, kWarpsPerBlock * kWarp,
+                                                           sm)) != cudaSuccess)
+      return e;
+    const uint64_t cap = static_cast<uint64_t>(n_sm) * (per_sm > 0 ? per_sm : 1);
+    blocks = need < cap ? need : cap;
+  }
+  step_kernel<SPL><<<static_cast<unsigned>(blocks), kWarpsPerBlock * kWarp, sm, s>>>(kp);
   return cudaGetLastError();
 }
 

@@ -1796,10 +1796,15 @@ mlob_status mlob_venv_step_io(mlob_venv* v, const mlob_step_io* io) {
     }
     k0.action_mode = v->action_mode;
     cudaEvent_t* ev = v->io_events.data();
-    cuda_check(cudaEventRecord(ev[0], v->stream), "event");
-    cuda_check(cudaStreamWaitEvent(v->stream2, ev[0], 0), "wait");
+    // one chunk: nothing to overlap, so everything stays on the handle's stream
+    const bool single = nc == 1;
+    cudaStream_t cs = single ? v->stream : v->copy_stream;
+    if (!single) {
+      cuda_check(cudaEventRecord(ev[0], v->stream), "event");
+      cuda_check(cudaStreamWaitEvent(v->stream2, ev[0], 0), "wait");
+    }
     const auto d2h = [&](void* dst, const void* src, uint64_t bytes) {
-      if (dst && bytes) cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, v->copy_stream), "D2H");
+      if (dst && bytes) cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, cs), "D2H");
     };
     for (uint64_t i = 0; i < nc; ++i) {
       const uint64_t c0 = i * chunk, m = std::min(chunk, n - c0);
@@ -1812,8 +1817,10 @@ mlob_status mlob_venv_step_io(mlob_venv* v, const mlob_step_io* io) {
           cuda_check(launch_expand_resets(v->d_just_reset + c0, m, cnt, v->d_resets[t] + c0 * cnt, s), "resets");
           ++v->launches;
         }
-      cuda_check(cudaEventRecord(ev[1 + i], s), "event");
-      cuda_check(cudaStreamWaitEvent(v->copy_stream, ev[1 + i], 0), "wait");
+      if (!single) {
+        cuda_check(cudaEventRecord(ev[1 + i], s), "event");
+        cuda_check(cudaStreamWaitEvent(v->copy_stream, ev[1 + i], 0), "wait");
+      }
       d2h(io->rewards ? io->rewards + c0 * A : nullptr, v->d_rewards + c0 * A, m * A * 8);
       d2h(io->dones ? io->dones + c0 * A : nullptr, v->d_dones + c0 * A, m * A);
       d2h(io->infos ? io->infos + c0 * A : nullptr, v->d_infos + c0 * A, m * A * sizeof(mlob_agent_info));
@@ -1825,11 +1832,12 @@ mlob_status mlob_venv_step_io(mlob_venv* v, const mlob_step_io* io) {
           d2h(io->resets[t] + c0 * cnt, cnt > 1 ? v->d_resets[t] + c0 * cnt : v->d_just_reset + c0, m * cnt);
       }
     }
-    // join: later work on the handle's stream is ordered after both streams and the copies
-    cuda_check(cudaEventRecord(ev[nc + 1], v->stream2), "event");
-    cuda_check(cudaEventRecord(ev[nc + 2], v->copy_stream), "event");
-    cuda_check(cudaStreamWaitEvent(v->stream, ev[nc + 1], 0), "wait");
-    cuda_check(cudaStreamWaitEvent(v->stream, ev[nc + 2], 0), "wait");
+    if (!single) {  // join: later work on the handle's stream follows both streams and the copies
+      cuda_check(cudaEventRecord(ev[nc + 1], v->stream2), "event");
+      cuda_check(cudaEventRecord(ev[nc + 2], v->copy_stream), "event");
+      cuda_check(cudaStreamWaitEvent(v->stream, ev[nc + 1], 0), "wait");
+      cuda_check(cudaStreamWaitEvent(v->stream, ev[nc + 2], 0), "wait");
+    }
     uint32_t e = 0;
     cuda_check(cudaMemcpyAsync(&e, v->d_error, sizeof e, cudaMemcpyDeviceToHost, v->stream), "error word");
     cuda_check(cudaStreamSynchronize(v->stream), "stream sync");
