@@ -34,30 +34,37 @@ __host__ __device__ inline size_t warp_smem_bytes(const DevCfg& c) {
 }
 
 __device__ WarpSmem carve(char* base, const DevCfg& c) {
-  WarpSmem s;
+  // every warp writes the same offsets; the warp's own writes are visible to
+  // it after the __syncwarp, other warps' writes carry identical values
   const int chunk = c.mps < kChunk ? c.mps : kChunk;
   const int nbuf = c.mps > kChunk ? 2 : 1;
-  char* p = base;
-  s.chunk0 = reinterpret_cast<DevMsg*>(p);
-  s.chunk1 = nbuf == 2 ? s.chunk0 + chunk : s.chunk0;
-  p += static_cast<size_t>(nbuf) * chunk * sizeof(DevMsg);
-  s.bar = reinterpret_cast<uint64_t*>(p);
-  p += 32;
-  s.amsg = reinterpret_cast<DevMsg*>(p);
-  p += static_cast<size_t>(4 * c.n_agents + 4) * sizeof(DevMsg);
-  s.ag = reinterpret_cast<AgentRec*>(p);
-  p += static_cast<size_t>(c.n_agents) * sizeof(AgentRec);
-  s.act = reinterpret_cast<ActiveRec*>(p);
-  p += static_cast<size_t>(c.n_agents) * kMaxActive * sizeof(ActiveRec);
-  s.acc = reinterpret_cast<StepAcc*>(p);
-  p += static_cast<size_t>(c.n_agents) * sizeof(StepAcc);
-  s.fills = reinterpret_cast<FillEnt*>(p);
-  p += kFillLog * sizeof(FillEnt);
-  s.scal = reinterpret_cast<int32_t*>(p);
-  p += 16;
-  s.l2 = reinterpret_cast<L2Lvl*>(p);
-  p += static_cast<size_t>(2 * c.obs_depth) * sizeof(L2Lvl);
-  s.obs = reinterpret_cast<double*>(p);
+  if ((threadIdx.x & 31) == 0) {
+    uint32_t p = 0;
+    SmemOff& o = g_smem_off;
+    o.chunk0 = p;
+    o.chunk1 = nbuf == 2 ? p + static_cast<uint32_t>(chunk * sizeof(DevMsg)) : p;
+    p += static_cast<uint32_t>(nbuf * chunk * sizeof(DevMsg));
+    o.bar = p;
+    p += 32;
+    o.amsg = p;
+    p += static_cast<uint32_t>((4 * c.n_agents + 4) * sizeof(DevMsg));
+    o.ag = p;
+    p += static_cast<uint32_t>(c.n_agents * sizeof(AgentRec));
+    o.act = p;
+    p += static_cast<uint32_t>(c.n_agents * kMaxActive * sizeof(ActiveRec));
+    o.acc = p;
+    p += static_cast<uint32_t>(c.n_agents * sizeof(StepAcc));
+    o.fills = p;
+    p += static_cast<uint32_t>(kFillLog * sizeof(FillEnt));
+    o.scal = p;
+    p += 16;
+    o.l2 = p;
+    p += static_cast<uint32_t>(2 * c.obs_depth * sizeof(L2Lvl));
+    o.obs = p;
+  }
+  __syncwarp();
+  WarpSmem s;
+  s.base = base;
   return s;
 }
 
@@ -183,9 +190,9 @@ __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL
   const int nch = (mps + kChunk - 1) / kChunk;
   const int A = cfg.n_agents;
   if (lane == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.bar[0])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.bar[1])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.bar[2])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.bar()[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.bar()[1])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.bar()[2])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
@@ -244,9 +251,9 @@ __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL
         for (int i = n_amsg - 1; i > 0; --i) {
           const int j = static_cast<int>(r.below(static_cast<uint64_t>(i + 1)));
           if (i != j) {
-            const DevMsg t = sm.amsg[i];
-            sm.amsg[i] = sm.amsg[j];
-            sm.amsg[j] = t;
+            const DevMsg t = sm.amsg()[i];
+            sm.amsg()[i] = sm.amsg()[j];
+            sm.amsg()[j] = t;
           }
         }
       }
@@ -272,7 +279,7 @@ __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL
       // (5) outcomes
       w.mbar = w.mid_count > 0 ? static_cast<double>(w.mid_sum) / (2.0 * static_cast<double>(w.mid_count))
                                : static_cast<double>(w.prev_mid_half) / 2.0;
-      if (sm.scal[1] && lane == 0) atomicAdd(kp.fill_overflow, 1ull);
+      if (sm.scal()[1] && lane == 0) atomicAdd(kp.fill_overflow, 1ull);
       w.rebuild_active();
       PHASE(5);
       ++w.step;

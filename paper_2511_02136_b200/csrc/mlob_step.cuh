@@ -151,6 +151,16 @@ struct RegSide {
         q_[kk] = 0;
         st_[kk] = kEmptySt;
       }
+  }  // compile-time row k, runtime predicate (no select chain over rows)
+  __device__ __forceinline__ void clear_row(int k, bool pred, int32_t empty_p) {
+    if (pred) {
+      p_[k] = empty_p;
+      q_[k] = 0;
+      st_[k] = kEmptySt;
+    }
+  }
+  __device__ __forceinline__ void setq_row(int k, bool pred, int32_t q) {
+    if (pred) q_[k] = q;
   }
 };
 
@@ -291,18 +301,28 @@ struct L2Lvl {
   int64_t qty;
 };
 
+// Per-warp shared-memory regions.  The region offsets are the same for every
+// warp of a block (they depend on the config only), so they live once in a
+// block-shared table and a warp keeps only its base pointer: eleven 64-bit
+// region pointers held in registers across the message loop forced spills
+// at the 80-register cap.
+struct SmemOff {
+  uint32_t chunk0, chunk1, bar, amsg, ag, act, acc, fills, scal, l2, obs, _pad;
+};
+__shared__ __align__(16) SmemOff g_smem_off;  // written by carve() (identical values from every warp)
 struct WarpSmem {
-  DevMsg* chunk0;  // replay chunk buffers (no array: keeps WarpEnv promotable to registers)
-  DevMsg* chunk1;
-  uint64_t* bar;  // mbarriers: [0], [1] replay chunks, [2] shared-memory book load
-  DevMsg* amsg;   // agent messages (<= 4 * A)
-  AgentRec* ag;
-  ActiveRec* act;
-  StepAcc* acc;
-  FillEnt* fills;
-  int32_t* scal;  // [0] fill-log count, [1] fill-log overflow
-  L2Lvl* l2;      // [2][obs_depth]
-  double* obs;    // staging, max_obs_dim
+  char* base;
+  __device__ __forceinline__ DevMsg* chunk0() const { return reinterpret_cast<DevMsg*>(base + g_smem_off.chunk0); }
+  __device__ __forceinline__ DevMsg* chunk1() const { return reinterpret_cast<DevMsg*>(base + g_smem_off.chunk1); }
+  __device__ __forceinline__ uint64_t* bar() const { return reinterpret_cast<uint64_t*>(base + g_smem_off.bar); }
+  __device__ __forceinline__ DevMsg* amsg() const { return reinterpret_cast<DevMsg*>(base + g_smem_off.amsg); }
+  __device__ __forceinline__ AgentRec* ag() const { return reinterpret_cast<AgentRec*>(base + g_smem_off.ag); }
+  __device__ __forceinline__ ActiveRec* act() const { return reinterpret_cast<ActiveRec*>(base + g_smem_off.act); }
+  __device__ __forceinline__ StepAcc* acc() const { return reinterpret_cast<StepAcc*>(base + g_smem_off.acc); }
+  __device__ __forceinline__ FillEnt* fills() const { return reinterpret_cast<FillEnt*>(base + g_smem_off.fills); }
+  __device__ __forceinline__ int32_t* scal() const { return reinterpret_cast<int32_t*>(base + g_smem_off.scal); }
+  __device__ __forceinline__ L2Lvl* l2() const { return reinterpret_cast<L2Lvl*>(base + g_smem_off.l2); }
+  __device__ __forceinline__ double* obs() const { return reinterpret_cast<double*>(base + g_smem_off.obs); }
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -378,8 +398,8 @@ __device__ __forceinline__ void attribute_fill(int n_agents, const DevCfg& cfg, 
     const int a = trader - 1;
     const int side = r == 0 ? 1 - aside : aside;
     const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
-    AgentRec& st = sm.ag[a];
-    StepAcc& ac = sm.acc[a];
+    AgentRec& st = sm.ag()[a];
+    StepAcc& ac = sm.acc()[a];
     const int64_t pq = static_cast<int64_t>(price) * qty;
     if (side == MLOB_BID) {
       st.inventory += qty;
@@ -400,17 +420,20 @@ __device__ __forceinline__ void attribute_fill(int n_agents, const DevCfg& cfg, 
     ac.count += 1;
     ac.sq[side] += qty;
     ac.spq[side] += pq;
-    const int nf = sm.scal[0];
+    const int nf = sm.scal()[0];
     if (nf < kFillLog) {
-      sm.fills[nf] = FillEnt{price, qty, a, side};
-      sm.scal[0] = nf + 1;
+      sm.fills()[nf] = FillEnt{price, qty, a, side};
+      sm.scal()[0] = nf + 1;
     } else {
-      sm.scal[1] = 1;
+      sm.scal()[1] = 1;
     }
   }
 }
 
 // ---------------------------------------------------------------------------
+#ifndef MLOB_ST_MATCH  // register books: address slots by their unique arrival word
+#define MLOB_ST_MATCH 1
+#endif
 #ifndef MLOB_SMEM_BOOK  // 1: shared-memory book for every capacity (experiment)
 #define MLOB_SMEM_BOOK 0
 #endif
@@ -571,16 +594,16 @@ struct WarpEnv {
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       const int b = q_issued & 1;
-      bulk_copy(b ? sm.chunk1 : sm.chunk0, src, static_cast<uint32_t>(n * sizeof(DevMsg)),
-                b ? &sm.bar[1] : &sm.bar[0]);
+      bulk_copy(b ? sm.chunk1() : sm.chunk0(), src, static_cast<uint32_t>(n * sizeof(DevMsg)),
+                b ? &sm.bar()[1] : &sm.bar()[0]);
     }
     ++q_issued;
   }
   __device__ __forceinline__ const DevMsg* staged() {
     const int b = q_consumed & 1;
-    bar_wait(b ? &sm.bar[1] : &sm.bar[0], (q_consumed >> 1) & 1);
+    bar_wait(b ? &sm.bar()[1] : &sm.bar()[0], (q_consumed >> 1) & 1);
     ++q_consumed;
-    return b ? sm.chunk1 : sm.chunk0;
+    return b ? sm.chunk1() : sm.chunk0();
   }
   // Shared-memory books: the rows below each side's high-water mark arrive by
   // bulk copies issued right after the header (they overlap the action
@@ -594,24 +617,24 @@ struct WarpEnv {
       for (int k = rows0; k < SPL; ++k) bid.put(k, INT_MIN, 0, 0, 0, kEmptySt);
       for (int k = rows1; k < SPL; ++k) ask.put(k, INT_MAX, 0, 0, 0, kEmptySt);
       if (lane == 0) {
-        bar_arrive_tx(&sm.bar[2], static_cast<uint32_t>(rows0 + rows1) * kWarp * 20u);
+        bar_arrive_tx(&sm.bar()[2], static_cast<uint32_t>(rows0 + rows1) * kWarp * 20u);
 #pragma unroll
         for (int S = 0; S < 2; ++S) {
           const uint32_t rows = static_cast<uint32_t>(S ? rows1 : rows0);
           if (rows == 0) continue;
           const size_t g = (env * 2 + S) * SPL * kWarp;
           uint32_t* b = S ? ask.base_ : bid.base_;
-          bulk_load_tx(b, kp.bk_p + g, rows * kWarp * 4, &sm.bar[2]);
-          bulk_load_tx(b + SPL * kWarp, kp.bk_q + g, rows * kWarp * 4, &sm.bar[2]);
-          bulk_load_tx(b + 2 * SPL * kWarp, kp.bk_id + g, rows * kWarp * 8, &sm.bar[2]);
-          bulk_load_tx(b + 4 * SPL * kWarp, kp.bk_st + g, rows * kWarp * 4, &sm.bar[2]);
+          bulk_load_tx(b, kp.bk_p + g, rows * kWarp * 4, &sm.bar()[2]);
+          bulk_load_tx(b + SPL * kWarp, kp.bk_q + g, rows * kWarp * 4, &sm.bar()[2]);
+          bulk_load_tx(b + 2 * SPL * kWarp, kp.bk_id + g, rows * kWarp * 8, &sm.bar()[2]);
+          bulk_load_tx(b + 4 * SPL * kWarp, kp.bk_st + g, rows * kWarp * 4, &sm.bar()[2]);
         }
       }
     }
   }
   __device__ __forceinline__ void book_load_wait() {
     if constexpr (SMEM) {
-      bar_wait(&sm.bar[2], book_loads & 1);
+      bar_wait(&sm.bar()[2], book_loads & 1);
       ++book_loads;
       __syncwarp();
       bid.recompute_occ();
@@ -668,12 +691,12 @@ struct WarpEnv {
     }
     const int A = cfg.n_agents;
     const int words = A * static_cast<int>(sizeof(AgentRec) / 8);
-    const uint64_t* src = reinterpret_cast<const uint64_t*>(sm.ag);
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(sm.ag());
     uint64_t* dst = reinterpret_cast<uint64_t*>(kp.agents + env * A);
     for (int i = lane; i < words; i += kWarp) dst[i] = src[i];
     for (int a = 0; a < A; ++a) {
-      const int n = sm.ag[a].n_active;
-      if (lane < n) kp.active[(env * A + a) * kMaxActive + lane] = sm.act[a * kMaxActive + lane];
+      const int n = sm.ag()[a].n_active;
+      if (lane < n) kp.active[(env * A + a) * kMaxActive + lane] = sm.act()[a * kMaxActive + lane];
     }
   }
   __device__ __forceinline__ void report_errors() {
@@ -683,12 +706,12 @@ struct WarpEnv {
     const int A = cfg.n_agents;
     const int words = A * static_cast<int>(sizeof(AgentRec) / 8);
     const uint64_t* src = reinterpret_cast<const uint64_t*>(kp.agents + env * A);
-    uint64_t* dst = reinterpret_cast<uint64_t*>(sm.ag);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(sm.ag());
     for (int i = lane; i < words; i += kWarp) dst[i] = src[i];
     __syncwarp();
     for (int a = 0; a < A; ++a) {
-      const int n = sm.ag[a].n_active;
-      if (lane < n) sm.act[a * kMaxActive + lane] = kp.active[(env * A + a) * kMaxActive + lane];
+      const int n = sm.ag()[a].n_active;
+      if (lane < n) sm.act()[a * kMaxActive + lane] = kp.active[(env * A + a) * kMaxActive + lane];
     }
     __syncwarp();
   }
@@ -848,6 +871,68 @@ struct WarpEnv {
     return __ffs(__ballot_sync(FULLMASK, any && ms == gs)) - 1;
   }
 
+  // ---- register books: slots addressed by content, not by (row, lane) ----
+  // The arrival word `st` is unique within a book (one sequence counter for
+  // both sides, book.hpp:183), so the oldest order at a price is named by its
+  // st: a lane-local min, one redux.min, then the winner's fields gathered by
+  // a one-hot redux.or and the slot updated where ST == st.  No row index,
+  // owner ballot or shuffle sits on the fill chain.
+  template <int S>
+  __device__ __forceinline__ uint32_t oldest_st_t(int32_t price) {
+    SideT& d = sd<S>();
+    uint32_t m = kEmptySt;
+    MLOB_ROWS(k) m = min(m, d.P(k) == price ? d.ST(k) : kEmptySt);
+    return __reduce_min_sync(FULLMASK, m);
+  }
+  template <int S>
+  __device__ __forceinline__ int32_t q_of_st_t(uint32_t st, bool ids, uint32_t& lo, uint32_t& hi) {
+    SideT& d = sd<S>();
+    uint32_t qv = 0, lv = 0, hv = 0;
+    MLOB_ROWS(k) {
+      const bool h = d.ST(k) == st;
+      qv |= h ? static_cast<uint32_t>(d.Q(k)) : 0u;
+      lv |= h ? d.LO(k) : 0u;
+      hv |= h ? d.HI(k) : 0u;
+    }
+    if (ids) {
+      lo = __reduce_or_sync(FULLMASK, lv);
+      hi = __reduce_or_sync(FULLMASK, hv);
+    }
+    return static_cast<int32_t>(__reduce_or_sync(FULLMASK, qv));
+  }
+  template <int S>
+  __device__ __forceinline__ void clear_st_t(uint32_t st) {
+    SideT& d = sd<S>();
+    MLOB_ROWS(k) d.clear_row(k, d.ST(k) == st, empty_price<S>());
+  }
+  template <int S>
+  __device__ __forceinline__ void setq_st_t(uint32_t st, int32_t q) {
+    SideT& d = sd<S>();
+    MLOB_ROWS(k) d.setq_row(k, d.ST(k) == st, q);
+  }
+  // id lookup: live matches counted warp-wide; for a unique match its price,
+  // quantity and st are gathered one-hot (duplicates take the slow path)
+  template <int S>
+  __device__ __forceinline__ uint32_t id_gather_t(uint32_t lo, uint32_t hi, int32_t& p, int32_t& q,
+                                                  uint32_t& st) {
+    SideT& d = sd<S>();
+    uint32_t n = 0, pv = 0, qv = 0, sv = 0;
+    MLOB_ROWS(k) {
+      const bool c = d.Q(k) > 0 && d.LO(k) == lo && d.HI(k) == hi;
+      n += c ? 1u : 0u;
+      pv |= c ? static_cast<uint32_t>(d.P(k)) : 0u;
+      qv |= c ? static_cast<uint32_t>(d.Q(k)) : 0u;
+      sv |= c ? d.ST(k) : 0u;
+    }
+    const uint32_t tot = __reduce_add_sync(FULLMASK, n);
+    if (tot == 1) {
+      p = static_cast<int32_t>(__reduce_or_sync(FULLMASK, pv));
+      q = static_cast<int32_t>(__reduce_or_sync(FULLMASK, qv));
+      st = __reduce_or_sync(FULLMASK, sv);
+    }
+    return tot;
+  }
+
   // ---- message handlers (runtime side) -------------------------------------
   __device__ __forceinline__ void record_trade(int32_t price, int32_t qty, const DevMsg& m,
                                                uint32_t lo, uint32_t hi, uint32_t st, int aside) {
@@ -882,6 +967,29 @@ struct WarpEnv {
       const int lo_ = o ? live1 : live0;
       const int32_t bp = o ? best1 : best0;
       if (lo_ == 0 || (s == 0 ? bp > m.price : bp < m.price)) break;
+      if constexpr (!SMEM && MLOB_ST_MATCH) {
+        const uint32_t gst = o ? oldest_st_t<1>(bp) : oldest_st_t<0>(bp);
+        uint32_t idlo = 0, idhi = 0;
+        const int32_t q = o ? q_of_st_t<1>(gst, pass_ids, idlo, idhi) : q_of_st_t<0>(gst, pass_ids, idlo, idhi);
+        const int32_t fill = min(rem, q);
+        rem -= fill;
+        if (fill == q) {
+          moved = true;
+          if (o) {
+            clear_st_t<1>(gst);
+            if (--live1 > 0) best1 = side_best_t<1>();
+          } else {
+            clear_st_t<0>(gst);
+            if (--live0 > 0) best0 = side_best_t<0>();
+          }
+        } else if (o) {
+          setq_st_t<1>(gst, q - fill);
+        } else {
+          setq_st_t<0>(gst, q - fill);
+        }
+        record_trade(bp, fill, m, idlo, idhi, gst, s);
+        continue;
+      }
       uint32_t lm;
       int lk;
       if (o)
@@ -953,6 +1061,31 @@ struct WarpEnv {
   __device__ __forceinline__ bool by_id(const DevMsg& m, bool remove) {
     const int s = m.side;
     const uint32_t lo = static_cast<uint32_t>(m.order_id), hi = static_cast<uint32_t>(m.order_id >> 32);
+    if constexpr (!SMEM && MLOB_ST_MATCH) {
+      int32_t p = 0, q = 0;
+      uint32_t st = 0;
+      const uint32_t tot = s ? id_gather_t<1>(lo, hi, p, q, st) : id_gather_t<0>(lo, hi, p, q, st);
+      if (tot == 0) return false;
+      if (tot == 1) {
+        const int32_t nq = remove ? 0 : q - min(q, m.qty);
+        if (nq == 0) {
+          if (s) {
+            clear_st_t<1>(st);
+            if (--live1 > 0 && p == best1) best1 = side_best_t<1>();
+          } else {
+            clear_st_t<0>(st);
+            if (--live0 > 0 && p == best0) best0 = side_best_t<0>();
+          }
+          return true;
+        }
+        if (s)
+          setq_st_t<1>(st, nq);
+        else
+          setq_st_t<0>(st, nq);
+        return false;
+      }
+      // duplicate live ids: the generic path below
+    }
     int nm, lk;
     if (s)
       scan_id_t<1>(lo, hi, nm, lk);
@@ -1014,7 +1147,7 @@ struct WarpEnv {
       const DevMsg* buf;
       int n;
       if (seg < 0) {
-        buf = sm.amsg;
+        buf = sm.amsg();
         n = n_amsg;
       } else {
         buf = staged();
@@ -1030,7 +1163,7 @@ struct WarpEnv {
     const int total = n_amsg + mps;
     msgs += static_cast<uint64_t>(total);
     mid_count = total;
-    if (total > 0) last_time = mps > 0 ? slice[mps - 1].time : lds_msg(sm.amsg + n_amsg - 1).time;
+    if (total > 0) last_time = mps > 0 ? slice[mps - 1].time : lds_msg(sm.amsg() + n_amsg - 1).time;
     __syncwarp();  // lane 0's agent updates become visible to the warp
   }
 
@@ -1079,7 +1212,7 @@ struct WarpEnv {
 
   __device__ __forceinline__ void decode(int a, int id, Quotes& q) {
     const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
-    const AgentRec& st = sm.ag[a];
+    const AgentRec& st = sm.ag()[a];
     int64_t bb, ba;
     effective_tops(sp, bb, ba);
     q.n = 0;
@@ -1144,7 +1277,7 @@ struct WarpEnv {
   // avst_policy (avst.hpp:19-32).
   __device__ __forceinline__ void scripted(int a, const DevPolicy& pol, Quotes& q) {
     const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
-    const AgentRec& st = sm.ag[a];
+    const AgentRec& st = sm.ag()[a];
     if (pol.kind == MLOB_POLICY_TWAP) {
       const int64_t S = cfg.steps_per_episode, T = sp.task_size, s = step;
       const int64_t sched = ((s + 1) * T) / S - (s * T) / S;
@@ -1172,7 +1305,7 @@ struct WarpEnv {
       m.side = static_cast<uint8_t>(side);
       m._pad = 0;
       m.trader = trader;
-      sm.amsg[n_amsg] = m;
+      sm.amsg()[n_amsg] = m;
     }
     ++n_amsg;
   }
@@ -1181,7 +1314,7 @@ struct WarpEnv {
   // quotes not already resting at the same (side, price).
   __device__ __forceinline__ void convert_action(int a, int64_t step_time, int& n_amsg) {
     const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
-    AgentRec& st = sm.ag[a];
+    AgentRec& st = sm.ag()[a];
     Quotes q;
     q.n = 0;
     q.s0 = q.s1 = 0;
@@ -1236,7 +1369,7 @@ struct WarpEnv {
     bool kept0 = false, kept1 = false;
     const int na = st.n_active;
     for (int i = 0; i < na; ++i) {
-      const ActiveRec ar = sm.act[a * kMaxActive + i];
+      const ActiveRec ar = sm.act()[a * kMaxActive + i];
       const int side = static_cast<int>(ar.qty_side >> 31);
       const bool r0 = q.n >= 1 && q.s0 == side && q.p0 == ar.price;
       const bool r1 = q.n >= 2 && q.s1 == side && q.p1 == ar.price;
@@ -1295,7 +1428,7 @@ struct WarpEnv {
   // out to the agents.
   __device__ __forceinline__ void rebuild_active() {
     const int A = cfg.n_agents;
-    ActTmp* tmp = reinterpret_cast<ActTmp*>(sm.amsg);  // agent messages are consumed
+    ActTmp* tmp = reinterpret_cast<ActTmp*>(sm.amsg());  // agent messages are consumed
     const int cap = 4 * A + 4;                          // DevMsg slots = ActTmp slots
     int base = 0;
     base = compact_side<0>(tmp, base, cap);
@@ -1303,7 +1436,7 @@ struct WarpEnv {
     base = compact_side<1>(tmp, base, cap);
     __syncwarp();
     if (lane == 0) {
-      for (int a = 0; a < A; ++a) sm.ag[a].n_active = 0;
+      for (int a = 0; a < A; ++a) sm.ag()[a].n_active = 0;
       const int total = base < cap ? base : cap;
       if (base > cap) err |= kErrActiveOverflow;
       // insertion sort each side into storage order: bids (price asc, seq desc),
@@ -1330,15 +1463,15 @@ struct WarpEnv {
           err |= kErrBadTrader;
           continue;
         }
-        const int n = sm.ag[a].n_active;
+        const int n = sm.ag()[a].n_active;
         if (n >= kMaxActive) {
           err |= kErrActiveOverflow;
           continue;
         }
-        sm.act[a * kMaxActive + n] =
+        sm.act()[a * kMaxActive + n] =
             ActiveRec{(static_cast<uint64_t>(x.hi) << 32) | x.lo, x.price,
                       static_cast<uint32_t>(x.qty) | (static_cast<uint32_t>(i >= nbid) << 31)};
-        sm.ag[a].n_active = n + 1;
+        sm.ag()[a].n_active = n + 1;
       }
     }
     __syncwarp();
@@ -1367,8 +1500,8 @@ struct WarpEnv {
   // env.hpp:445-464 (also accumulates slippage_total); lane 0 writes.
   __device__ __forceinline__ void fill_info(int a) {
     const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
-    AgentRec& st = sm.ag[a];
-    const StepAcc& ac = sm.acc[a];
+    AgentRec& st = sm.ag()[a];
+    const StepAcc& ac = sm.acc()[a];
     mlob_agent_info info;
     info.inventory = st.inventory;
     info.cash = st.cash;
@@ -1392,8 +1525,8 @@ struct WarpEnv {
   // env.hpp:409-433 + rewards.hpp
   __device__ __forceinline__ double compute_reward(int a) {
     const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
-    const AgentRec& st = sm.ag[a];
-    const StepAcc& ac = sm.acc[a];
+    const AgentRec& st = sm.ag()[a];
+    const StepAcc& ac = sm.acc()[a];
     double r = 0.0;
     if (sp.reward == MLOB_REWARD_EXEC) {
       r = -ac.slip;
@@ -1401,15 +1534,15 @@ struct WarpEnv {
         r -= sp.unfilled_penalty_coef * static_cast<double>(st.task_remaining) * st.p_init;
     } else {
       double pb = 0.0, ps = 0.0;
-      const int nf = sm.scal[0];
-      if (!sm.scal[1]) {
+      const int nf = sm.scal()[0];
+      if (!sm.scal()[1]) {
         for (int i = 0; i < nf; ++i) {
-          const FillEnt f = sm.fills[i];
+          const FillEnt f = sm.fills()[i];
           if (f.agent == a && f.side == MLOB_BID)
             pb += (mbar - static_cast<double>(f.price)) * static_cast<double>(f.qty);
         }
         for (int i = 0; i < nf; ++i) {
-          const FillEnt f = sm.fills[i];
+          const FillEnt f = sm.fills()[i];
           if (f.agent == a && f.side == MLOB_ASK)
             ps += (static_cast<double>(f.price) - mbar) * static_cast<double>(f.qty);
         }
@@ -1449,7 +1582,7 @@ struct WarpEnv {
   // 0 then written by lanes (coalesced).
   __device__ __forceinline__ void build_observation(int a, const L2Lvl* l2b, int nb, const L2Lvl* l2a, int na) {
     const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
-    const AgentRec& st = sm.ag[a];
+    const AgentRec& st = sm.ag()[a];
     const int dim = sp.obs_dim;
     if (lane == 0) {
       const int64_t bb = live0 > 0 ? best0 : -1;
@@ -1460,14 +1593,14 @@ struct WarpEnv {
       const double spread = (bb < 0 || ba < 0) ? 0.0 : fmin_ref(32.0, static_cast<double>(ba - bb));
       int64_t own_bid = -1, own_ask = -1;
       for (int i = 0; i < st.n_active; ++i) {
-        const ActiveRec ar = sm.act[a * kMaxActive + i];
+        const ActiveRec ar = sm.act()[a * kMaxActive + i];
         if ((ar.qty_side >> 31) == 0)
           own_bid = own_bid < 0 ? ar.price : max(own_bid, static_cast<int64_t>(ar.price));
         else
           own_ask = own_ask < 0 ? ar.price : min(own_ask, static_cast<int64_t>(ar.price));
       }
       const double dmid = static_cast<double>(mid_half - prev_mid_half) / 2.0;
-      double* out = sm.obs;
+      double* out = sm.obs();
       if (sp.type == MLOB_EXECUTOR) {
         const int dir = st.task_dir == MLOB_TASK_BUY ? 1 : -1;
         out[0] = static_cast<double>(st.task_remaining) /
@@ -1513,7 +1646,7 @@ struct WarpEnv {
     const int t = cfg.flat_spec[a];
     const int kk = a - cfg.specs[t].flat_offset;
     double* dst = kp.obs[t] + (env * static_cast<uint64_t>(cfg.specs[t].count) + kk) * dim;
-    for (int j = lane; j < dim; j += kWarp) dst[j] = sm.obs[j];
+    for (int j = lane; j < dim; j += kWarp) dst[j] = sm.obs()[j];
     __syncwarp();
   }
 
@@ -1524,13 +1657,13 @@ struct WarpEnv {
   // through local memory in v1).
   __device__ __forceinline__ void snapshot() {
     if (!cfg.full_l2 && summarize_l2<0>() && summarize_l2<1>()) return;
-    nb_l2 = l2_levels<0>(sm.l2);
-    na_l2 = l2_levels<1>(sm.l2 + cfg.obs_depth);
+    nb_l2 = l2_levels<0>(sm.l2());
+    na_l2 = l2_levels<1>(sm.l2() + cfg.obs_depth);
     sumq0 = sumq1 = topq0 = topq1 = 0;
-    for (int i = 0; i < nb_l2; ++i) sumq0 += sm.l2[i].qty;
-    for (int i = 0; i < na_l2; ++i) sumq1 += sm.l2[cfg.obs_depth + i].qty;
-    topq0 = nb_l2 > 0 ? sm.l2[0].qty : 0;
-    topq1 = na_l2 > 0 ? sm.l2[cfg.obs_depth].qty : 0;
+    for (int i = 0; i < nb_l2; ++i) sumq0 += sm.l2()[i].qty;
+    for (int i = 0; i < na_l2; ++i) sumq1 += sm.l2()[cfg.obs_depth + i].qty;
+    topq0 = nb_l2 > 0 ? sm.l2()[0].qty : 0;
+    topq1 = na_l2 > 0 ? sm.l2()[cfg.obs_depth].qty : 0;
   }
 
   // Warp-sum of a per-lane value < 2^36 (16-bit split keeps redux.sync exact).
@@ -1588,8 +1721,8 @@ struct WarpEnv {
   }
 
   __device__ __forceinline__ void outcomes(bool write_rewards) {
-    const L2Lvl* l2b = sm.l2;
-    const L2Lvl* l2a = sm.l2 + cfg.obs_depth;
+    const L2Lvl* l2b = sm.l2();
+    const L2Lvl* l2a = sm.l2() + cfg.obs_depth;
     const int nb = nb_l2, na = na_l2;
     for (int a = 0; a < cfg.n_agents; ++a) {
       if (write_rewards) {
@@ -1606,10 +1739,10 @@ struct WarpEnv {
 
   __device__ __forceinline__ void clear_step_acc() {
     const int A = cfg.n_agents;
-    for (int i = lane; i < A; i += kWarp) sm.acc[i] = StepAcc{0.0, 0, {0, 0}, {0, 0}, 0, 0};
+    for (int i = lane; i < A; i += kWarp) sm.acc()[i] = StepAcc{0.0, 0, {0, 0}, {0, 0}, 0, 0};
     if (lane == 0) {
-      sm.scal[0] = 0;
-      sm.scal[1] = 0;
+      sm.scal()[0] = 0;
+      sm.scal()[1] = 0;
     }
     __syncwarp();
   }
@@ -1657,7 +1790,7 @@ struct WarpEnv {
       st.nonce = 0;
       st.n_active = 0;
       st.p_init = static_cast<double>(mid_half) / 2.0;
-      st.task_dir = sm.ag[a].task_dir;
+      st.task_dir = sm.ag()[a].task_dir;
       if (sp.type == MLOB_EXECUTOR) {
         uint64_t h = splitmix64(seed);
         h = key_fold(h, genv);
@@ -1672,7 +1805,7 @@ struct WarpEnv {
         st.task_remaining = 0;
       }
       __syncwarp();
-      if (lane == 0) sm.ag[a] = st;
+      if (lane == 0) sm.ag()[a] = st;
     }
     __syncwarp();
     clear_step_acc();
