@@ -348,6 +348,39 @@ __device__ __forceinline__ DevMsg lds_msg(const DevMsg* p) {
   return m;
 }
 
+// A staged message in the loop: the hot fields (price, qty, kind, side,
+// trader: one 16-byte ld.shared) live in registers; the order id and time are
+// re-read from shared memory where they are used (rest, id lookup, trade
+// record), which keeps four registers free across the fill loop.
+struct MsgRef {
+  uint32_t a;  // shared-window address of the record
+  int32_t price, qty;
+  uint8_t kind, side;
+  int32_t trader;
+  __device__ __forceinline__ uint64_t order_id() const {
+    uint32_t lo, hi;
+    asm("ld.shared.v2.u32 {%0,%1}, [%2+8];" : "=r"(lo), "=r"(hi) : "r"(a));
+    return (static_cast<uint64_t>(hi) << 32) | lo;
+  }
+  __device__ __forceinline__ int64_t time() const {
+    uint32_t lo, hi;
+    asm("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(a));
+    return static_cast<int64_t>((static_cast<uint64_t>(hi) << 32) | lo);
+  }
+};
+__device__ __forceinline__ MsgRef lds_hot(const DevMsg* p) {
+  MsgRef m;
+  m.a = smem_u32(p);
+  uint32_t x, y, z, w;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4+16];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(m.a));
+  m.price = static_cast<int32_t>(x);
+  m.qty = static_cast<int32_t>(y);
+  m.kind = static_cast<uint8_t>(z & 0xffu);
+  m.side = static_cast<uint8_t>((z >> 8) & 0xffu);
+  m.trader = static_cast<int32_t>(w);
+  return m;
+}
+
 __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   const uint32_t b = smem_u32(bar);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
@@ -468,9 +501,13 @@ struct WarpEnv {
   int64_t mid_sum, mid_count;
   uint32_t n_trades;
   uint32_t err;
-  int capacity;        // cached kernel params (avoid generic loads of param space)
-  bool rec_trades;
-  int n_agents;
+  // config words cached in registers (measured: reading them from the staged
+  // shared-memory copy at each use is 4% slower)
+  int capacity_, n_agents_;
+  bool rec_trades_;
+  __device__ __forceinline__ int capacity() const { return capacity_; }
+  __device__ __forceinline__ bool rec_trades() const { return rec_trades_; }
+  __device__ __forceinline__ int n_agents() const { return n_agents_; }
   int nb_l2, na_l2;    // L2 levels staged in smem by snapshot()
   int64_t topq0, topq1;  // level-0 aggregated qty per side
   int64_t sumq0, sumq1;  // Σ qty over the top-D levels per side
@@ -485,9 +522,10 @@ struct WarpEnv {
     }
     bind(e);
     err = 0;
-    capacity = c.capacity;
-    rec_trades = (p.flags & MLOB_VENV_RECORD_TRADES) != 0;
-    n_agents = c.n_agents;
+    if (ln == 0) sm.scal()[2] = 0;  // in-loop error flag (report_errors)
+    capacity_ = c.capacity;
+    rec_trades_ = (p.flags & MLOB_VENV_RECORD_TRADES) != 0;
+    n_agents_ = c.n_agents;
   }
 
   __device__ __forceinline__ void bind(uint64_t e) {
@@ -700,6 +738,7 @@ struct WarpEnv {
     }
   }
   __device__ __forceinline__ void report_errors() {
+    err |= static_cast<uint32_t>(sm.scal()[2]);
     if (err && lane == 0) atomicOr(kp.error, err);
   }
   __device__ __forceinline__ void load_agents() {
@@ -934,15 +973,15 @@ struct WarpEnv {
   }
 
   // ---- message handlers (runtime side) -------------------------------------
-  __device__ __forceinline__ void record_trade(int32_t price, int32_t qty, const DevMsg& m,
+  __device__ __forceinline__ void record_trade(int32_t price, int32_t qty, const MsgRef& m,
                                                uint32_t lo, uint32_t hi, uint32_t st, int aside) {
-    if (rec_trades && lane == 0 && n_trades < kp.trade_cap) {
+    if (rec_trades() && lane == 0 && n_trades < kp.trade_cap) {
       mlob_trade t;
       t.price = price;
       t.quantity = qty;
-      t.time = m.time;
+      t.time = m.time();
       t.passive_order_id = (static_cast<uint64_t>(hi) << 32) | lo;
-      t.aggressor_order_id = m.order_id;
+      t.aggressor_order_id = m.order_id();
       t.passive_trader_id = static_cast<int32_t>(st & 0xffu);
       t.aggressor_trader_id = m.trader;
       t.aggressor_side = static_cast<uint8_t>(aside);
@@ -953,16 +992,16 @@ struct WarpEnv {
     ++n_trades;
     const uint32_t pt = st & 0xffu;
     if ((pt | static_cast<uint32_t>(m.trader)) && lane == 0)  // an agent is involved
-      attribute_fill(n_agents, cfg, sm, price, qty, static_cast<int>(pt), m.trader, aside);
+      attribute_fill(n_agents(), cfg, sm, price, qty, static_cast<int>(pt), m.trader, aside);
   }
 
   bool moved;  // a top (best price or side emptiness) changed: refresh the mid
 
   // book.hpp:150-187 (process_new_limit + rest_order)
-  __device__ __forceinline__ void new_limit(const DevMsg& m) {
+  __device__ __forceinline__ void new_limit(const MsgRef& m) {
     const int s = m.side, o = s ^ 1;
     int32_t rem = m.qty;
-    const bool pass_ids = rec_trades;
+    const bool pass_ids = rec_trades();
     while (rem > 0) {
       const int lo_ = o ? live1 : live0;
       const int32_t bp = o ? best1 : best0;
@@ -1024,7 +1063,7 @@ struct WarpEnv {
     }
     if (rem <= 0) return;
     // rest_order
-    if ((s ? live1 : live0) == capacity) {
+    if ((s ? live1 : live0) == capacity()) {
       const bool ev = s ? evict_t<1>(m.price) : evict_t<0>(m.price);
       if (!ev) return;  // newcomer dropped: no sequence number consumed
       moved = true;
@@ -1034,14 +1073,14 @@ struct WarpEnv {
         --live0;
     }
     const uint32_t seq = next_seq++;
-    if (seq >= kMaxSeq) err |= kErrSeqRange;
+    if (seq >= kMaxSeq) sm.scal()[2] = kErrSeqRange;  // rare: kept out of the loop's registers
     int pk, pl;
     if (s)
       free_slot_t<1>(pk, pl);
     else
       free_slot_t<0>(pk, pl);
     const uint32_t st = (seq << 8) | static_cast<uint32_t>(m.trader & 0xff);
-    const uint32_t ilo = static_cast<uint32_t>(m.order_id), ihi = static_cast<uint32_t>(m.order_id >> 32);
+    const uint32_t ilo = static_cast<uint32_t>(m.order_id()), ihi = static_cast<uint32_t>(m.order_id() >> 32);
     if (s) {
       ask.set_u(pk, lane == pl, m.price, rem, ilo, ihi, st);
       if (++live1 == 1 || m.price < best1) {
@@ -1058,9 +1097,9 @@ struct WarpEnv {
   }
 
   // book.hpp:189-207 (reduce_order / remove_order); absent ids are no-ops.
-  __device__ __forceinline__ bool by_id(const DevMsg& m, bool remove) {
+  __device__ __forceinline__ bool by_id(const MsgRef& m, bool remove) {
     const int s = m.side;
-    const uint32_t lo = static_cast<uint32_t>(m.order_id), hi = static_cast<uint32_t>(m.order_id >> 32);
+    const uint32_t lo = static_cast<uint32_t>(m.order_id()), hi = static_cast<uint32_t>(m.order_id() >> 32);
     if constexpr (!SMEM && MLOB_ST_MATCH) {
       int32_t p = 0, q = 0;
       uint32_t st = 0;
@@ -1117,14 +1156,23 @@ struct WarpEnv {
 
   // env.hpp:230: the mid follows the tops; it is refreshed only on the paths
   // that can move a top (any NewLimit, removals), not per message.
+  // mid_sum (Σ of the mid after every message) is accumulated lazily: the
+  // messages since the last mid change are counted and folded in when the mid
+  // changes or the loop ends, so the per-message work is one 32-bit add.
+  int mid_run;
   __device__ __forceinline__ void refresh_mid() {
     const int64_t b0 = best0, b1 = best1;
-    mid_half = live0 > 0 ? (live1 > 0 ? b0 + b1 : 2 * b0) : (live1 > 0 ? 2 * b1 : mid_half);
+    const int64_t nm = live0 > 0 ? (live1 > 0 ? b0 + b1 : 2 * b0) : (live1 > 0 ? 2 * b1 : mid_half);
+    if (nm != mid_half) {
+      mid_sum += mid_half * mid_run;
+      mid_run = 0;
+      mid_half = nm;
+    }
   }
 
   // book.hpp:65-86 + env.hpp:223-235 (mid_count / last_time / messages are
   // derived once after the loop: they only depend on the message count).
-  __device__ __forceinline__ void run_message(const DevMsg& m) {
+  __device__ __forceinline__ void run_message(const MsgRef& m) {
     if (m.kind == MLOB_NEW_LIMIT) {
       if (m.qty > 0) {
         moved = false;
@@ -1134,7 +1182,7 @@ struct WarpEnv {
     } else if (m.kind <= MLOB_EXECUTE_VISIBLE) {
       if (by_id(m, m.kind == MLOB_DELETE)) refresh_mid();
     }
-    mid_sum += mid_half;
+    ++mid_run;
   }
 
   // Agent messages, then the replay slice staged in smem chunks (env.hpp:236-237).
@@ -1143,6 +1191,7 @@ struct WarpEnv {
   __device__ __forceinline__ void process_messages(int n_amsg, const DevMsg* slice) {
     const int mps = cfg.mps;
     const int nch = (mps + kChunk - 1) / kChunk;
+    mid_run = 0;
     for (int seg = -1; seg < nch; ++seg) {
       const DevMsg* buf;
       int n;
@@ -1154,12 +1203,13 @@ struct WarpEnv {
         n = min(kChunk, mps - seg * kChunk);
       }
 #if MLOB_LDS_ASM
-      for (int i = 0; i < n; ++i) run_message(lds_msg(buf + i));
+      for (int i = 0; i < n; ++i) run_message(lds_hot(buf + i));
 #else
       for (int i = 0; i < n; ++i) run_message(buf[i]);
 #endif
       if (seg >= 0 && seg + 2 < nch) stage(slice + (seg + 2) * kChunk, min(kChunk, mps - (seg + 2) * kChunk));
     }
+    mid_sum += mid_half * mid_run;
     const int total = n_amsg + mps;
     msgs += static_cast<uint64_t>(total);
     mid_count = total;
