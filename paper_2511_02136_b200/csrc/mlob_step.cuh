@@ -151,7 +151,40 @@ struct RegSide {
         q_[kk] = 0;
         st_[kk] = kEmptySt;
       }
-  }  // compile-time row k, runtime predicate (no select chain over rows)
+  }  // compile-time row K, runtime predicate.  The asm text differs per row
+  // (the "row K" comment), so LLVM cannot merge the per-row branches of
+  // insert_t into one runtime-indexed write (that demotes the book to local
+  // memory).
+#define MLOB_PUT_IF(K)                                                                          \
+  asm volatile("{\n.reg .pred pp; // row " #K "\nsetp.ne.b32 pp, %5, 0;\n@pp mov.b32 %0, %6;\n"    \
+               "@pp mov.b32 %1, %7;\n@pp mov.b32 %2, %8;\n@pp mov.b32 %3, %9;\n@pp mov.b32 %4, %10;\n}" \
+               : "+r"(p_[K]), "+r"(q_[K]), "+r"(lo_[K]), "+r"(hi_[K]), "+r"(st_[K])                 \
+               : "r"(static_cast<uint32_t>(pred)), "r"(p), "r"(q), "r"(lo), "r"(hi), "r"(st))
+  template <int K>
+  __device__ __forceinline__ void put_if(bool pred, int32_t p, int32_t q, uint32_t lo, uint32_t hi, uint32_t st) {
+    static_assert(K < SPL && K < 8, "row");
+    if constexpr (K == 0) MLOB_PUT_IF(0);
+    else if constexpr (K == 1) MLOB_PUT_IF(1);
+    else if constexpr (K == 2) MLOB_PUT_IF(2);
+    else if constexpr (K == 3) MLOB_PUT_IF(3);
+    else if constexpr (K == 4) MLOB_PUT_IF(4);
+    else if constexpr (K == 5) MLOB_PUT_IF(5);
+    else if constexpr (K == 6) MLOB_PUT_IF(6);
+    else MLOB_PUT_IF(7);
+  }
+#undef MLOB_PUT_IF
+  // first row K.. with a free lane (ballots b), warp-uniform branches
+  template <int K>
+  __device__ __forceinline__ void insert_rows(const uint32_t* b, int lane, int32_t p, int32_t q, uint32_t lo,
+                                              uint32_t hi, uint32_t st) {
+    if constexpr (K < SPL) {
+      if (b[K])
+        put_if<K>(lane == __ffs(b[K]) - 1, p, q, lo, hi, st);
+      else
+        insert_rows<K + 1>(b, lane, p, q, lo, hi, st);
+    }
+  }
+  // compile-time row k, runtime predicate (no select chain over rows)
   __device__ __forceinline__ void clear_row(int k, bool pred, int32_t empty_p) {
     if (pred) {
       p_[k] = empty_p;
@@ -466,6 +499,9 @@ __device__ __forceinline__ void attribute_fill(int n_agents, const DevCfg& cfg, 
 // ---------------------------------------------------------------------------
 #ifndef MLOB_ST_MATCH  // register books: address slots by their unique arrival word
 #define MLOB_ST_MATCH 1
+#endif
+#ifndef MLOB_BALLOT_INSERT  // register books: per-row ballots + uniform branch for inserts
+#define MLOB_BALLOT_INSERT 1
 #endif
 #ifndef MLOB_SMEM_BOOK  // 1: shared-memory book for every capacity (experiment)
 #define MLOB_SMEM_BOOK 0
@@ -949,6 +985,18 @@ struct WarpEnv {
     SideT& d = sd<S>();
     MLOB_ROWS(k) d.setq_row(k, d.ST(k) == st, q);
   }
+  // insert at the lowest free position (row-major), book.hpp:183-186 (any
+  // free slot would do: priority is carried by st): one ballot per row, the
+  // first row with a free lane taken by a warp-uniform branch, so only that
+  // row's five registers are written (a runtime row index compiles to
+  // selects over every row)
+  template <int S>
+  __device__ __forceinline__ void insert_t(int32_t p, int32_t q, uint32_t lo, uint32_t hi, uint32_t st) {
+    SideT& d = sd<S>();
+    uint32_t b[SPL];
+    MLOB_ROWS(k) b[k] = __ballot_sync(FULLMASK, d.Q(k) == 0);
+    d.template insert_rows<0>(b, lane, p, q, lo, hi, st);
+  }
   // id lookup: live matches counted warp-wide; for a unique match its price,
   // quantity and st are gathered one-hot (duplicates take the slow path)
   template <int S>
@@ -1074,21 +1122,30 @@ struct WarpEnv {
     }
     const uint32_t seq = next_seq++;
     if (seq >= kMaxSeq) sm.scal()[2] = kErrSeqRange;  // rare: kept out of the loop's registers
-    int pk, pl;
-    if (s)
-      free_slot_t<1>(pk, pl);
-    else
-      free_slot_t<0>(pk, pl);
     const uint32_t st = (seq << 8) | static_cast<uint32_t>(m.trader & 0xff);
     const uint32_t ilo = static_cast<uint32_t>(m.order_id()), ihi = static_cast<uint32_t>(m.order_id() >> 32);
+    if constexpr (!SMEM && MLOB_BALLOT_INSERT) {
+      if (s)
+        insert_t<1>(m.price, rem, ilo, ihi, st);
+      else
+        insert_t<0>(m.price, rem, ilo, ihi, st);
+    } else {
+      int pk, pl;
+      if (s)
+        free_slot_t<1>(pk, pl);
+      else
+        free_slot_t<0>(pk, pl);
+      if (s)
+        ask.set_u(pk, lane == pl, m.price, rem, ilo, ihi, st);
+      else
+        bid.set_u(pk, lane == pl, m.price, rem, ilo, ihi, st);
+    }
     if (s) {
-      ask.set_u(pk, lane == pl, m.price, rem, ilo, ihi, st);
       if (++live1 == 1 || m.price < best1) {
         best1 = m.price;
         moved = true;
       }
     } else {
-      bid.set_u(pk, lane == pl, m.price, rem, ilo, ihi, st);
       if (++live0 == 1 || m.price > best0) {
         best0 = m.price;
         moved = true;
