@@ -185,11 +185,13 @@ struct RegSide {
     }
   }
   // compile-time row k, runtime predicate (no select chain over rows)
+  // (st is left stale: every st query names a live order, st values are
+  // never reused within an episode, and empty slots are excluded by their
+  // sentinel price / zero quantity everywhere else)
   __device__ __forceinline__ void clear_row(int k, bool pred, int32_t empty_p) {
     if (pred) {
       p_[k] = empty_p;
       q_[k] = 0;
-      st_[k] = kEmptySt;
     }
   }
   __device__ __forceinline__ void setq_row(int k, bool pred, int32_t q) {
