@@ -390,7 +390,7 @@ __device__ __forceinline__ DevMsg lds_msg(const DevMsg* p) {
 struct MsgRef {
   uint32_t a;  // shared-window address of the record
   int32_t price, qty;
-  uint8_t kind, side;
+  int32_t kind, side;  // widened once at the load (no per-use byte masks)
   int32_t trader;
   __device__ __forceinline__ uint64_t order_id() const {
     uint32_t lo, hi;
@@ -410,8 +410,8 @@ __device__ __forceinline__ MsgRef lds_hot(const DevMsg* p) {
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4+16];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(m.a));
   m.price = static_cast<int32_t>(x);
   m.qty = static_cast<int32_t>(y);
-  m.kind = static_cast<uint8_t>(z & 0xffu);
-  m.side = static_cast<uint8_t>((z >> 8) & 0xffu);
+  m.kind = static_cast<int32_t>(z & 0xffu);
+  m.side = static_cast<int32_t>((z >> 8) & 0xffu);
   m.trader = static_cast<int32_t>(w);
   return m;
 }
@@ -1052,10 +1052,13 @@ struct WarpEnv {
     const int s = m.side, o = s ^ 1;
     int32_t rem = m.qty;
     const bool pass_ids = rec_trades();
+    // crossing test with the sign folded in: ~x reverses the int32 order, so
+    // for a sell (s = 1, flip = -1) (bp ^ flip) <= (price ^ flip) is bp >= price
+    const int32_t flip = -s, kprice = m.price ^ flip;
     while (rem > 0) {
       const int lo_ = o ? live1 : live0;
       const int32_t bp = o ? best1 : best0;
-      if (lo_ == 0 || (s == 0 ? bp > m.price : bp < m.price)) break;
+      if (lo_ == 0 || (bp ^ flip) > kprice) break;
       if constexpr (!SMEM && MLOB_ST_MATCH) {
         const uint32_t gst = o ? oldest_st_t<1>(bp) : oldest_st_t<0>(bp);
         uint32_t idlo = 0, idhi = 0;
