@@ -560,7 +560,6 @@ struct WarpEnv {
     }
     bind(e);
     err = 0;
-    if (ln == 0) sm.scal()[2] = 0;  // in-loop error flag (report_errors)
     capacity_ = c.capacity;
     rec_trades_ = (p.flags & MLOB_VENV_RECORD_TRADES) != 0;
     n_agents_ = c.n_agents;
@@ -776,7 +775,6 @@ struct WarpEnv {
     }
   }
   __device__ __forceinline__ void report_errors() {
-    err |= static_cast<uint32_t>(sm.scal()[2]);
     if (err && lane == 0) atomicOr(kp.error, err);
   }
   __device__ __forceinline__ void load_agents() {
@@ -1125,8 +1123,7 @@ struct WarpEnv {
       else
         --live0;
     }
-    const uint32_t seq = next_seq++;
-    if (seq >= kMaxSeq) sm.scal()[2] = kErrSeqRange;  // rare: kept out of the loop's registers
+    const uint32_t seq = next_seq++;  // range checked once after the loop (process_messages)
     const uint32_t st = (seq << 8) | static_cast<uint32_t>(m.trader & 0xff);
     const uint32_t ilo = static_cast<uint32_t>(m.order_id()), ihi = static_cast<uint32_t>(m.order_id() >> 32);
     if constexpr (!SMEM && MLOB_BALLOT_INSERT) {
@@ -1272,6 +1269,8 @@ struct WarpEnv {
       if (seg >= 0 && seg + 2 < nch) stage(slice + (seg + 2) * kChunk, min(kChunk, mps - (seg + 2) * kChunk));
     }
     mid_sum += mid_half * mid_run;
+    // next_seq only grows: some arrival sequence reached kMaxSeq iff it ends above it
+    if (next_seq > kMaxSeq) err |= kErrSeqRange;
     const int total = n_amsg + mps;
     msgs += static_cast<uint64_t>(total);
     mid_count = total;
@@ -1424,6 +1423,7 @@ struct WarpEnv {
 
   // env.hpp:285-370: quotes -> Delete for stale active orders, NewLimit for
   // quotes not already resting at the same (side, price).
+  Rng bench_rng;  // kActBench: keyed at agent 0, one draw per agent in order
   __device__ __forceinline__ void convert_action(int a, int64_t step_time, int& n_amsg) {
     const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
     AgentRec& st = sm.ag()[a];
@@ -1456,10 +1456,10 @@ struct WarpEnv {
     } else {
       int id;
       if (kp.action_mode == kActBench) {  // bench.hpp:57-60: one rng, one draw per agent in order
-        Rng r{key_fold(key_fold(key_fold(splitmix64(kp.bench_seed), kRngBenchAction), genv),
-                       kp.global_step)};
-        for (int b = 0; b < a; ++b) r.next();
-        id = static_cast<int>(r.below(static_cast<uint64_t>(sp.arity)));
+        if (a == 0)
+          bench_rng.s = key_fold(key_fold(key_fold(splitmix64(kp.bench_seed), kRngBenchAction), genv),
+                                 kp.global_step);
+        id = static_cast<int>(bench_rng.below(static_cast<uint64_t>(sp.arity)));
       } else if (pol && pol->kind == MLOB_POLICY_LEARNED) {  // argmax id from the policy kernel
         id = kp.action_ids[env * cfg.n_agents + a];
       } else if (pol) {  // PolicyKind::Random, evaluate.hpp:74-79
