@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL
   // so the next env's data can be prefetched; kp.ticket is zeroed per launch.
   const uint64_t first = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + warp;
   // phase-sync builds keep idle warps alive for the block barriers
-  const bool idle = first >= kp.n_envs;
+  bool idle = first >= kp.n_envs;
   if (idle && !phase_sync<SPL>()) return;
   const auto ticket = [&]() -> uint64_t {
     unsigned long long t = 0;
@@ -202,8 +202,18 @@ __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL
   };
   if (!idle && mps > 0) w.stage(slice_of(first), min(kChunk, mps));
 
-  uint64_t nenv = (MLOB_PERSIST && !phase_sync<SPL>()) ? ticket() : kp.n_envs;
-  for (uint64_t env = first; env < kp.n_envs || (idle && env == first);) {
+  // MLOB_ROUNDS (phase-sync blocks): a grid of one block per SM walks the
+  // envs in rounds (env = first + r * stride) with a block barrier at each
+  // round start, so every round begins with all warps in phase 1 (like a
+  // fresh block) while the next round's first replay chunk and header / book
+  // rows are prefetched during this one; idle warps keep joining the barriers.
+  constexpr bool rounds = MLOB_ROUNDS && phase_sync<SPL>();
+  const uint64_t n_rounds = rounds ? (kp.n_envs + stride - 1) / stride : 1;
+  uint64_t nenv = (MLOB_PERSIST && !phase_sync<SPL>()) ? ticket() : rounds ? first + stride : kp.n_envs;
+  for (uint64_t env = first, round = 0; round < n_rounds && (env < kp.n_envs || phase_sync<SPL>()); ++round) {
+    if constexpr (rounds) {
+      if (round > 0) __syncthreads();
+    }
     const DevMsg* slice = nullptr;
     const bool has_next = nenv < kp.n_envs;
     const DevMsg* next_slice = nullptr;
@@ -322,9 +332,16 @@ __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL
       w.store_state(just_reset);
       PHASE(9);
     }
-    if (idle) break;
-    env = nenv;
-    if (has_next) nenv = ticket();
+    if constexpr (rounds) {
+      env = nenv;
+      nenv = env + stride;
+      idle = env >= kp.n_envs;
+    } else {
+      if (idle) break;
+      env = nenv;
+      if (has_next) nenv = ticket();
+      if (MLOB_PERSIST && !phase_sync<SPL>()) --round;  // ticketed: runs until the envs run out
+    }
   }
   w.book_store_drain();
   w.report_errors();
@@ -466,7 +483,8 @@ static cudaError_t launch_step_t(const KParams& kp, const DevCfg& cfg, cudaStrea
   }
   const uint64_t need = (kp.n_envs + kWarpsPerBlock - 1) / kWarpsPerBlock;
   uint64_t blocks = need;
-  if (MLOB_PERSIST && !phase_sync<SPL>()) {  // persistent grid: every SM filled to its occupancy limit
+  if ((MLOB_PERSIST && !phase_sync<SPL>()) || (MLOB_ROUNDS && phase_sync<SPL>())) {
+    // persistent grid: every SM filled to its occupancy limit
     int dev = 0, n_sm = 0, per_sm = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;

@@ -32,11 +32,14 @@
 #ifndef MLOB_LDS_ASM
 #define MLOB_LDS_ASM 1
 #endif
+#ifndef MLOB_ROUNDS  // phase-sync step kernel: one block per SM looping over env rounds
+#define MLOB_ROUNDS 1
+#endif
 #ifndef MLOB_PERSIST  // persistent warps + ticketed envs: measured slower (r1 notes)
 #define MLOB_PERSIST 0
 #endif
-#ifndef MLOB_PREFETCH
-#define MLOB_PREFETCH 1
+#ifndef MLOB_PREFETCH  // L2 prefetch of the next env's header / agents / book rows (measured -1% with rounds)
+#define MLOB_PREFETCH 0
 #endif
 
 namespace mlob {
