@@ -510,6 +510,15 @@ def random_stream(o: Oracle, seed: int, **kw) -> np.ndarray:
     return out
 
 
+def dup_id_stream(o: Oracle, seed: int, n_ids: int = 5, **kw) -> np.ndarray:
+    """A random_stream whose order ids are folded onto n_ids values, so resting
+    orders share ids and cancels / deletes / executes hit duplicate live ids
+    (the first-match-in-storage-order rule of book.hpp:191-206)."""
+    msgs = random_stream(o, seed, **kw).copy()
+    msgs["order_id"] = msgs["order_id"] % n_ids + 1
+    return msgs
+
+
 def fnv1a(data: bytes, h: int = 1469598103934665603) -> int:
     """FNV-1a 64 (SURVEY §8c digest recipe)."""
     for b in data:

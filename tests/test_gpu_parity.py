@@ -187,6 +187,32 @@ def test_random_streams_zero_agents(orc):
             compare_env_state(b.view(i), r)
 
 
+@pytest.mark.parametrize("capacity", [64, 100, 256, 600])
+def test_duplicate_live_ids_zero_agents(orc, capacity):
+    """Replay streams whose resting orders share ids (oracle.dup_id_stream): the
+    device's duplicate-id path (first match in storage order, book.hpp:191-206)
+    for register books (SPL 2 / 4 / 8) and a shared-memory book (SPL 32),
+    every step vs the oracle (books in storage order, trades, mids)."""
+    from oracle.oracle import dup_id_stream
+    streams = [dup_id_stream(orc, seed, n_messages=4000) for seed in range(6)]
+    msgs = np.concatenate(streams)
+    states = [(i * 4000, [], []) for i in range(6)]
+    dev = DeviceStore(HostStore.from_messages(msgs, states), 0)
+    ost = orc.store_from(msgs, states)
+    cfg = abi.env_config([], steps_per_episode=40, messages_per_step=100, start_stride_steps=40,
+                         book_capacity=capacity)
+    b = MarketEnvBatch(dev, cfg, n_envs=6, seed=0)
+    b.reset(list(range(6)))
+    refs = [OEnv(orc, ost, cfg, 0, i) for i in range(6)]
+    for i, r in enumerate(refs):
+        r.reset(i)
+    for t in range(40):
+        b.step_ids(np.zeros((6, 0), dtype=np.int32))
+        for i, r in enumerate(refs):
+            r.step_ids([])
+            compare_env_state(b.view(i), r)
+
+
 def test_errors_match_reference_exceptions():
     cfg = abi.env_config([abi.agent_spec(abi.MARKET_MAKER)], steps_per_episode=4,
                          messages_per_step=10, start_stride_steps=4)

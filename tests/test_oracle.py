@@ -174,6 +174,21 @@ def test_random_streams_match_naive_book(orc, ref):  # test_lob.cpp:258-281
         ref.naive_free(naive)
 
 
+@pytest.mark.parametrize("capacity", [8, 64, 1 << 15])
+def test_duplicate_live_ids_match_reference(orc, ref, capacity):
+    """Resting orders sharing ids: reduce / remove take the first match in the
+    reference's storage order (book.hpp:191-206); with evictions at small
+    capacities.  C restatement vs the compiled reference, message by message."""
+    from oracle.oracle import dup_id_stream
+    for seed in range(6):
+        msgs = dup_id_stream(orc, seed, n_messages=3000)
+        b, r = OBook(orc, capacity), OBook(ref, capacity)
+        for m in msgs:
+            assert b.process(m).tobytes() == r.process(m).tobytes()
+        assert b.orders(0).tobytes() == r.orders(0).tobytes()
+        assert b.orders(1).tobytes() == r.orders(1).tobytes()
+
+
 # ---- synthetic store -----------------------------------------------------------
 
 @pytest.mark.parametrize("kw,seed", [({}, 0), ({"state_sample_every": 100}, 11),
