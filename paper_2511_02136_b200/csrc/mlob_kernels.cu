@@ -467,34 +467,52 @@ static unsigned grid_for(uint64_t n) {
 
 template <int SPL>
 static cudaError_t launch_step_t(const KParams& kp, const DevCfg& cfg, cudaStream_t s) {
-  const int kWarpsPerBlock = step_warps(cfg);
-  const size_t sm = warp_smem_bytes(cfg) * kWarpsPerBlock;
+  int warps = step_warps(cfg);
+  const size_t full_sm = warp_smem_bytes(cfg) * warps;
   // the dynamic-smem opt-in only grows (a per-process cache per instantiation:
   // small launches are host-bound, so no attribute call per launch)
   static size_t sm_set[64] = {};
+  static int n_sm_of[64] = {}, per_sm_of[64] = {};
   int cur_dev = 0;
   cudaError_t e = cudaGetDevice(&cur_dev);
   if (e != cudaSuccess) return e;
   size_t& done = sm_set[cur_dev & 63];
-  if (sm > done) {
-    e = cudaFuncSetAttribute(step_kernel<SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+  if (full_sm > done) {
+    e = cudaFuncSetAttribute(step_kernel<SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(full_sm));
     if (e != cudaSuccess) return e;
-    done = sm;
+    done = full_sm;
+    per_sm_of[cur_dev & 63] = 0;  // re-query the occupancy for the new block size
   }
-  const uint64_t need = (kp.n_envs + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  uint64_t blocks = need;
+  uint64_t blocks = (kp.n_envs + warps - 1) / warps;
   if ((MLOB_PERSIST && !phase_sync<SPL>()) || (MLOB_ROUNDS && phase_sync<SPL>())) {
-    // persistent grid: every SM filled to its occupancy limit
-    int dev = 0, n_sm = 0, per_sm = 0;
-    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-    if ((e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<SPL>, kWarpsPerBlock * kWarp,
-                                                           sm)) != cudaSuccess)
+    // persistent grid: every SM filled to its occupancy limit (cached per device)
+    int& n_sm = n_sm_of[cur_dev & 63];
+    int& per_sm = per_sm_of[cur_dev & 63];
+    if (n_sm == 0 &&
+        (e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, cur_dev)) != cudaSuccess)
       return e;
-    const uint64_t cap = static_cast<uint64_t>(n_sm) * (per_sm > 0 ? per_sm : 1);
+    if (per_sm == 0) {
+      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<SPL>, warps * kWarp,
+                                                             full_sm)) != cudaSuccess)
+        return e;
+      if (per_sm < 1) per_sm = 1;
+    }
+    const uint64_t cap = static_cast<uint64_t>(n_sm) * static_cast<uint64_t>(per_sm);
+    if (MLOB_ROUNDS && phase_sync<SPL>()) {
+      // balanced rounds: the fewest rounds at full width, then the narrowest
+      // block that still covers the envs in that many rounds (4,096 envs:
+      // 2 rounds of 14 warps on every SM instead of 24 + a 3.7 %-full round)
+      const uint64_t per_round = cap * static_cast<uint64_t>(warps);
+      const uint64_t rounds = (kp.n_envs + per_round - 1) / per_round;
+      const uint64_t w = (kp.n_envs + cap * rounds - 1) / (cap * rounds);
+      warps = static_cast<int>(w < static_cast<uint64_t>(warps) ? (w > 0 ? w : 1) : warps);
+    }
+    const uint64_t need = (kp.n_envs + warps - 1) / warps;
     blocks = need < cap ? need : cap;
   }
-  step_kernel<SPL><<<static_cast<unsigned>(blocks), kWarpsPerBlock * kWarp, sm, s>>>(kp);
+  const size_t sm = warp_smem_bytes(cfg) * warps;
+  step_kernel<SPL><<<static_cast<unsigned>(blocks), warps * kWarp, sm, s>>>(kp);
   return cudaGetLastError();
 }
 
