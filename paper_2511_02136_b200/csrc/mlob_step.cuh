@@ -967,10 +967,10 @@ struct WarpEnv {
     SideT& d = sd<S>();
     uint32_t qv = 0, lv = 0, hv = 0;
     MLOB_ROWS(k) {
-      const bool h = d.ST(k) == st;
-      qv |= h ? static_cast<uint32_t>(d.Q(k)) : 0u;
-      lv |= h ? d.LO(k) : 0u;
-      hv |= h ? d.HI(k) : 0u;
+      const bool h = d.ST(k) == st;  // one-hot: a select chain, no OR
+      qv = h ? static_cast<uint32_t>(d.Q(k)) : qv;
+      lv = h ? d.LO(k) : lv;
+      hv = h ? d.HI(k) : hv;
     }
     if (ids) {
       lo = __reduce_or_sync(FULLMASK, lv);
@@ -1010,9 +1010,11 @@ struct WarpEnv {
     MLOB_ROWS(k) {
       const bool c = d.Q(k) > 0 && d.LO(k) == lo && d.HI(k) == hi;
       n += c ? 1u : 0u;
-      pv |= c ? static_cast<uint32_t>(d.P(k)) : 0u;
-      qv |= c ? static_cast<uint32_t>(d.Q(k)) : 0u;
-      sv |= c ? d.ST(k) : 0u;
+      // select chains: the gathered values are used only when the match is
+      // unique warp-wide (then one lane has exactly one matching row)
+      pv = c ? static_cast<uint32_t>(d.P(k)) : pv;
+      qv = c ? static_cast<uint32_t>(d.Q(k)) : qv;
+      sv = c ? d.ST(k) : sv;
     }
     const uint32_t tot = __reduce_add_sync(FULLMASK, n);
     if (tot == 1) {
