@@ -25,7 +25,7 @@ __host__ __device__ inline size_t warp_smem_bytes(const DevCfg& c) {
   b += static_cast<size_t>(c.n_agents) * kMaxActive * sizeof(ActiveRec);
   b += static_cast<size_t>(c.n_agents) * sizeof(StepAcc);
   b += kFillLog * sizeof(FillEnt);
-  b += 16;  // scalars
+  b += 32;  // scalars (WarpSmem::scal: fill-log count / overflow, mid anchor / segment base, Σmid)
   b += static_cast<size_t>(2 * c.obs_depth) * sizeof(L2Lvl);
   b += static_cast<size_t>(c.max_obs_dim + 1) * sizeof(double);
   b = (b + 15) / 16 * 16;
@@ -57,7 +57,7 @@ __device__ WarpSmem carve(char* base, const DevCfg& c) {
     o.fills = p;
     p += static_cast<uint32_t>(kFillLog * sizeof(FillEnt));
     o.scal = p;
-    p += 16;
+    p += 32;
     o.l2 = p;
     p += static_cast<uint32_t>(2 * c.obs_depth * sizeof(L2Lvl));
     o.obs = p;

@@ -29,9 +29,6 @@
 
 #include "mlob_dev.h"
 
-#ifndef MLOB_LDS_ASM
-#define MLOB_LDS_ASM 1
-#endif
 #ifndef MLOB_ROUNDS  // phase-sync step kernel: one block per SM looping over env rounds
 #define MLOB_ROUNDS 1
 #endif
@@ -1220,33 +1217,40 @@ struct WarpEnv {
 
   // env.hpp:230: the mid follows the tops; it is refreshed only on the paths
   // that can move a top (any NewLimit, removals), not per message.
-  // mid_sum (Σ of the mid after every message) is accumulated lazily: the
-  // messages since the last mid change are counted and folded in when the mid
-  // changes or the loop ends, so the per-message work is one 32-bit add.
-  int mid_run;
-  __device__ __forceinline__ void refresh_mid() {
+  // mid_sum (Σ of the mid after every message) is accumulated lazily: at a
+  // mid change after message j (index within the step) the messages
+  // mid_anchor..j-1 carried the old mid; the remainder is folded in after
+  // the loop.  No per-message counter (a counter register was spilled: two
+  // local loads and a store per message).
+  // The fold state lives in shared memory (scal[2] anchor, scal[3] segment
+  // base, scal[4..5] Σmid): it is touched only at mid changes, so it holds no
+  // register across the loop.
+  __device__ __forceinline__ void refresh_mid(int i) {
     const int64_t b0 = best0, b1 = best1;
     const int64_t nm = live0 > 0 ? (live1 > 0 ? b0 + b1 : 2 * b0) : (live1 > 0 ? 2 * b1 : mid_half);
     if (nm != mid_half) {
-      mid_sum += mid_half * mid_run;
-      mid_run = 0;
+      int32_t* sc = sm.scal();
+      const int j = sc[3] + i;
+      int64_t& ms = *reinterpret_cast<int64_t*>(sc + 4);
+      ms += mid_half * (j - sc[2]);
+      sc[2] = j;
       mid_half = nm;
     }
   }
 
   // book.hpp:65-86 + env.hpp:223-235 (mid_count / last_time / messages are
   // derived once after the loop: they only depend on the message count).
-  __device__ __forceinline__ void run_message(const MsgRef& m) {
+  // i: the message's index within its segment (see refresh_mid)
+  __device__ __forceinline__ void run_message(const MsgRef& m, int i) {
     if (m.kind == MLOB_NEW_LIMIT) {
       if (m.qty > 0) {
         moved = false;
         new_limit(m);
-        if (moved) refresh_mid();
+        if (moved) refresh_mid(i);
       }
     } else if (m.kind <= MLOB_EXECUTE_VISIBLE) {
-      if (by_id(m, m.kind == MLOB_DELETE)) refresh_mid();
+      if (by_id(m, m.kind == MLOB_DELETE)) refresh_mid(i);
     }
-    ++mid_run;
   }
 
   // Agent messages, then the replay slice staged in smem chunks (env.hpp:236-237).
@@ -1255,7 +1259,12 @@ struct WarpEnv {
   __device__ __forceinline__ void process_messages(int n_amsg, const DevMsg* slice) {
     const int mps = cfg.mps;
     const int nch = (mps + kChunk - 1) / kChunk;
-    mid_run = 0;
+    {
+      int32_t* sc = sm.scal();
+      sc[2] = 0;
+      sc[3] = 0;
+      *reinterpret_cast<int64_t*>(sc + 4) = 0;
+    }
     for (int seg = -1; seg < nch; ++seg) {
       const DevMsg* buf;
       int n;
@@ -1265,15 +1274,13 @@ struct WarpEnv {
       } else {
         buf = staged();
         n = min(kChunk, mps - seg * kChunk);
+        sm.scal()[3] = n_amsg + seg * kChunk;
       }
-#if MLOB_LDS_ASM
-      for (int i = 0; i < n; ++i) run_message(lds_hot(buf + i));
-#else
-      for (int i = 0; i < n; ++i) run_message(buf[i]);
-#endif
+      for (int i = 0; i < n; ++i) run_message(lds_hot(buf + i), i);
       if (seg >= 0 && seg + 2 < nch) stage(slice + (seg + 2) * kChunk, min(kChunk, mps - (seg + 2) * kChunk));
     }
-    mid_sum += mid_half * mid_run;
+    __syncwarp();
+    mid_sum = *reinterpret_cast<const int64_t*>(sm.scal() + 4) + mid_half * (n_amsg + mps - sm.scal()[2]);
     // next_seq only grows: some arrival sequence reached kMaxSeq iff it ends above it
     if (next_seq > kMaxSeq) err |= kErrSeqRange;
     const int total = n_amsg + mps;
