@@ -104,7 +104,8 @@ __host__ __device__ constexpr bool phase_sync() {
 }
 template <int SPL>
 __host__ __device__ constexpr int warps_per_block() {
-  return (phase_sync<SPL>() && SPL <= 8) ? MLOB_SYNC_WARPS : 4;  // deep books: smem-bound 4-warp blocks
+  // deep books: as many warps as the shared memory holds (5 at C = 1000), <= 8
+  return (phase_sync<SPL>() && SPL <= 8) ? MLOB_SYNC_WARPS : (SPL > 8 ? 8 : 4);
 }
 template <int SPL>
 __host__ __device__ constexpr int min_blocks() {
@@ -112,7 +113,7 @@ __host__ __device__ constexpr int min_blocks() {
   return (phase_sync<SPL>() && SPL <= 8) ? (65536 / (MLOB_SYNC_REGS * 32 * MLOB_SYNC_WARPS) > 0
                                   ? 65536 / (MLOB_SYNC_REGS * 32 * MLOB_SYNC_WARPS)
                                   : 1)
-                           : 4;
+                           : (SPL > 8 ? 1 : 4);
 }
 constexpr int kWarpsPerBlock = 4;  // reset kernel
 
@@ -156,6 +157,14 @@ __device__ __forceinline__ void stage_params(StagedParams& sp, const KParams& kp
   __syncthreads();
 }
 static_assert(sizeof(KParams) % 16 == 0, "KParams must be int4-copyable");
+// Deep-book step blocks stage the parameters at the front of the dynamic
+// shared memory with only the config's n_specs agent specs (a static
+// StagedParams reserves all kMaxSpecs = 5.2 KB): that is what lets a fifth
+// 45 KB warp fit in the 227 KB block at C = 1000.
+__host__ __device__ inline size_t staged_dyn_bytes(int n_specs) {
+  const size_t b = offsetof(StagedParams, cfg) + offsetof(DevCfg, specs) + static_cast<size_t>(n_specs) * sizeof(DevSpec);
+  return (b + 127) / 128 * 128;
+}
 
 template <int SPL>
 __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL>())
@@ -163,8 +172,17 @@ __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL
   // warps per block: warps_per_block<SPL>() unless the config's shared memory
   // per warp needs a smaller block (step_warps)
   const int kWarpsPerBlock = static_cast<int>(blockDim.x) / kWarp;
-  extern __shared__ __align__(128) char smem[];
-  __shared__ __align__(16) StagedParams sp_;
+  extern __shared__ __align__(128) char dsmem[];
+  StagedParams* spp;
+  char* smem = dsmem;  // the warps' regions
+  if constexpr (SPL <= 8) {
+    __shared__ __align__(16) StagedParams sp_static;
+    spp = &sp_static;
+  } else {
+    spp = reinterpret_cast<StagedParams*>(dsmem);
+    smem = dsmem + staged_dyn_bytes(kparam.cfg->n_specs);
+  }
+  StagedParams& sp_ = *spp;
   stage_params(sp_, kparam);
   const KParams& kp = sp_.kp;
   if (kp.gate && *kp.gate) return;  // the batch's actions were rejected: no env steps
@@ -449,15 +467,25 @@ __global__ void clear_finished_kernel(EnvHdr* hdr, uint64_t n) {
 // shared-memory books, fewer when the config's per-warp shared memory
 // (obs depth, agents) would not fit the 227 KB block limit
 constexpr size_t kBlockSmemLimit = 227 * 1024 - sizeof(StagedParams) - 1024;
+static bool deep_book(const DevCfg& c) { return spl_of(c.capacity) > 8; }
+static size_t step_staged_bytes(const DevCfg& c) {  // dynamic-smem prefix (deep books)
+  return deep_book(c) ? staged_dyn_bytes(c.n_specs) : 0;
+}
 static int step_warps(const DevCfg& c) {
-  const int want = spl_of(c.capacity) <= 8 && MLOB_PHASE_SYNC ? MLOB_SYNC_WARPS : 4;
+  const bool deep = deep_book(c);
+  const int want = deep ? 8 : (MLOB_PHASE_SYNC ? MLOB_SYNC_WARPS : 4);
   const size_t per = warp_smem_bytes(c);
-  const int fit = static_cast<int>(kBlockSmemLimit / (per > 0 ? per : 1));
+  // deep: 227 KB less the static g_smem_off table, the staged prefix and a margin
+  const size_t limit = deep ? 227 * 1024 - sizeof(SmemOff) - step_staged_bytes(c) - 256 : kBlockSmemLimit;
+  const int fit = static_cast<int>(limit / (per > 0 ? per : 1));
   return fit < 1 ? 1 : (fit < want ? fit : want);
 }
 
 size_t step_smem_bytes(const DevCfg& c) {  // dynamic smem of the step kernel's block
-  return warp_smem_bytes(c) * step_warps(c);
+  return step_staged_bytes(c) + warp_smem_bytes(c) * step_warps(c);
+}
+size_t step_min_smem_bytes(const DevCfg& c) {  // ... of a one-warp block (the feasibility bound)
+  return step_staged_bytes(c) + warp_smem_bytes(c);
 }
 
 static unsigned grid_for(uint64_t n) {
@@ -468,7 +496,8 @@ static unsigned grid_for(uint64_t n) {
 template <int SPL>
 static cudaError_t launch_step_t(const KParams& kp, const DevCfg& cfg, cudaStream_t s) {
   int warps = step_warps(cfg);
-  const size_t full_sm = warp_smem_bytes(cfg) * warps;
+  const size_t staged = step_staged_bytes(cfg);
+  const size_t full_sm = staged + warp_smem_bytes(cfg) * warps;
   // the dynamic-smem opt-in only grows (a per-process cache per instantiation:
   // small launches are host-bound, so no attribute call per launch)
   static size_t sm_set[64] = {};
@@ -511,7 +540,7 @@ static cudaError_t launch_step_t(const KParams& kp, const DevCfg& cfg, cudaStrea
     const uint64_t need = (kp.n_envs + warps - 1) / warps;
     blocks = need < cap ? need : cap;
   }
-  const size_t sm = warp_smem_bytes(cfg) * warps;
+  const size_t sm = staged + warp_smem_bytes(cfg) * warps;
   step_kernel<SPL><<<static_cast<unsigned>(blocks), warps * kWarp, sm, s>>>(kp);
   return cudaGetLastError();
 }

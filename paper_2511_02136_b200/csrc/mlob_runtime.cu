@@ -22,7 +22,7 @@
 #include <sstream>
 
 namespace mlob {
-size_t step_smem_bytes(const DevCfg& c);
+size_t step_min_smem_bytes(const DevCfg& c);
 int slots_per_lane(int capacity);
 cudaError_t launch_step(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s);
 cudaError_t launch_reset(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s);
@@ -836,7 +836,7 @@ mlob_status mlob_venv_create(const mlob_venv_desc* desc, mlob_venv** out) {
       v->d_env_index = v->alloc<uint64_t>(n, "env_index");
       cuda_check(cudaMemcpy(v->d_env_index, v->genv.data(), n * 8, cudaMemcpyHostToDevice), "H2D");
     }
-    if (step_smem_bytes(v->dcfg) > 226 * 1024)
+    if (step_min_smem_bytes(v->dcfg) > 226 * 1024)
       fail(MLOB_E_INVALID_ARGUMENT, "configuration needs more shared memory per env than an SM has");
     cuda_check(cudaDeviceSynchronize(), "create");
     *out = v.release();
