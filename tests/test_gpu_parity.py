@@ -292,6 +292,32 @@ def test_two_shards_equal_one_batch():
     assert float(tot[:, 4].sum()) > 0
 
 
+@pytest.mark.parametrize("n", [7105, 3553])
+def test_rounds_cover_every_env(n):
+    """The step kernel's rounds (one block per SM walking env rounds, the
+    launcher's balanced block width, a partial last round) step every env
+    exactly once: a batch of n envs equals the same envs run as 8 small shards
+    (one round each), env for env."""
+    from paper_2511_02136_b200.sharding import sharded_vec_env
+    cfg = abi.env_config([abi.agent_spec(abi.MARKET_MAKER), abi.agent_spec(abi.EXECUTOR)],
+                         steps_per_episode=6, messages_per_step=40, start_stride_steps=1)
+    dev = dev_store({"state_sample_every": 40, "n_messages": 80000})
+    full = MarketVecEnv(dev, cfg, seed=9, n_envs=n)
+    shards = [sharded_vec_env(dev, cfg, n, r, 8, seed=9) for r in range(8)]
+    for v in [full] + shards:
+        v.reset_all()
+    for t in range(14):  # crosses two auto-resets
+        for v in [full] + shards:
+            v.step_random(5, t)
+    assert full.messages_processed() == sum(s.messages_processed() for s in shards)
+    for ty in range(cfg.n_specs):
+        a = full.gather(ty)
+        b = [s.gather(ty) for s in shards]
+        assert a[0].tobytes() == np.concatenate([x[0] for x in b]).tobytes()
+        assert a[1].tobytes() == np.concatenate([x[1] for x in b]).tobytes()
+    assert full.rewards().tobytes() == np.concatenate([s.rewards() for s in shards]).tobytes()
+
+
 @pytest.mark.parametrize("chunks", ["1", "3"])
 def test_step_io_matches_separate_calls(monkeypatch, chunks):
     """mlob_venv_step_io (chunked step on two streams + overlapped copies) gives
