@@ -1660,14 +1660,13 @@ struct WarpEnv {
       double pb = 0.0, ps = 0.0;
       const int nf = sm.scal()[0];
       if (!sm.scal()[1]) {
+        // one pass: each side's sum still accumulates in fill order
         for (int i = 0; i < nf; ++i) {
           const FillEnt f = sm.fills()[i];
-          if (f.agent == a && f.side == MLOB_BID)
+          if (f.agent != a) continue;
+          if (f.side == MLOB_BID)
             pb += (mbar - static_cast<double>(f.price)) * static_cast<double>(f.qty);
-        }
-        for (int i = 0; i < nf; ++i) {
-          const FillEnt f = sm.fills()[i];
-          if (f.agent == a && f.side == MLOB_ASK)
+          else
             ps += (static_cast<double>(f.price) - mbar) * static_cast<double>(f.qty);
         }
       } else {
