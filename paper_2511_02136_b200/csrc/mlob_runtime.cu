@@ -956,7 +956,6 @@ static void do_step(mlob_venv* v, int mode, uint64_t bench_seed, uint64_t global
   kp.action_mode = mode;
   kp.bench_seed = bench_seed;
   kp.global_step = global_step;
-  cuda_check(cudaMemsetAsync(v->d_ticket, 0, sizeof(unsigned long long), v->stream), "ticket reset");
   cuda_check(launch_step(kp, v->dcfg, v->spl, v->stream), "step kernel");
   ++v->launches;
   advance_step(v);

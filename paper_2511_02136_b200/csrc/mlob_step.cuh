@@ -35,6 +35,9 @@
 #ifndef MLOB_PERSIST  // persistent warps + ticketed envs: measured slower (r1 notes)
 #define MLOB_PERSIST 0
 #endif
+#if MLOB_PERSIST
+#error "ticketed mode needs KParams::ticket zeroed before every step launch (mlob_runtime.cu)"
+#endif
 #ifndef MLOB_PREFETCH  // L2 prefetch of the next env's header / agents / book rows (measured -1% with rounds)
 #define MLOB_PREFETCH 0
 #endif
