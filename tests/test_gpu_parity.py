@@ -566,3 +566,36 @@ def test_rollout_graph_replay_matches_plain_launches(monkeypatch):
                 v.ppo_update(0, abi.ppo_config(epochs=1, minibatches=1), seed=5, update_index=upd)
         monkeypatch.delenv("MLOB_NO_GRAPH", raising=False)
     assert outs[0] == outs[1]
+
+
+@pytest.mark.parametrize("workload", ["C", "D", "E"])
+def test_bench_workload_sampled_envs_match_oracle(orc, workload):
+    """Full bench sizes (config C: 65,536 envs; config D's shape: 262,144
+    deep-book envs, untrimmed store; config E: 2^20 envs): the whole batch steps through the bench
+    harness (device-drawn actions, bench.hpp:53-70) across an episode
+    boundary; sampled envs — block-round edges, the middle, the last, random
+    picks — are replayed one by one in the oracle and compared bit-exactly."""
+    import bench
+    n, cfg, synth, _ = bench.workload(workload)
+    dev = DeviceStore(HostStore.synth(synth, 0), 0)
+    ost = orc.synth(synth, 0)
+    g = MarketVecEnv(dev, cfg, seed=0, n_envs=n)
+    g.reset_all()
+    T = cfg.steps_per_episode + 6
+    for s in range(T):
+        g.step_random(0, s)
+    arities = [abi.action_arity(cfg.specs[t]) for t in abi.flat_specs(cfg)]
+    rng = np.random.default_rng(7)
+    sample = sorted({0, 1, 31, 3551, 3552, n // 2, n - 2, n - 1,
+                     *rng.integers(0, n, size=4).tolist()})
+    for e in sample:
+        o = OEnv(orc, ost, cfg, 0, e)
+        n_ep = o.n_episodes
+        o.reset(e % n_ep)
+        cursor = 1
+        for s in range(T):
+            o.step_ids(kat.bench_actions(0, e, s, arities))
+            if o.scalars().terminal:
+                o.reset((e + cursor * n) % n_ep)
+                cursor += 1
+        compare_env_state(g.view(e), o, trades=False)  # the bench runs without the trade log
