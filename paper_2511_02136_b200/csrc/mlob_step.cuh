@@ -230,6 +230,9 @@ struct SmemSide {
   }
   __device__ __forceinline__ void refresh_lw() {
     lw = side_ ? INT_MIN : INT_MAX;
+#if MLOB_LW_UNROLL
+#pragma unroll
+#endif
     for (int k = 0; k < SPL; ++k)
       if (q_[k * 32] > 0) lw = worse(lw, p_[k * 32]);
     lw_stale = 0;
@@ -515,14 +518,29 @@ __device__ __forceinline__ void attribute_fill(int n_agents, const DevCfg& cfg, 
 #define MLOB_ROWS(k)                                        \
   _Pragma("unroll 1") for (int k##_g = 0; k##_g < SPL; k##_g += kUnr) \
   _Pragma("unroll") for (int k = k##_g; k < k##_g + kUnr; ++k)
+// the shared-memory book's candidate-filter scans (id, oldest at a price,
+// best price) with their own unroll width
+#define MLOB_SCAN_ROWS(k)                                      \
+  _Pragma("unroll 1") for (int k##_g = 0; k##_g < SPL; k##_g += kScanUnr) \
+  _Pragma("unroll") for (int k = k##_g; k < k##_g + kScanUnr; ++k)
+#ifndef MLOB_SCAN_UNR  // candidate-filter scans fully unrolled: 32 loads in flight
+#define MLOB_SCAN_UNR 32
+#endif
 template <int SPL, bool SMEM = (SPL > 8) || MLOB_SMEM_BOOK>
 struct WarpEnv {
   using SideT = typename std::conditional<SMEM, SmemSide<SPL>, RegSide<SPL>>::type;
   // rows per unrolled group: all rows for register books (a full unroll keeps
-  // them in registers), groups of 4 for shared-memory books (code size).  An
+  // them in registers); for shared-memory books the candidate-filter scans
+  // (id, oldest at a price, best price) unroll fully — 32 independent
+  // ld.shared in flight, D +17 % over groups of 4 — and every other row loop
+  // runs in groups of 2 (code size: 16 or a full unroll everywhere is slower).  An
   // explicit `#pragma unroll N` on the row loops changes the register-book
   // code (measured -11% on config C), hence the two-level loop below.
-  static constexpr int kUnr = (SMEM && SPL >= 4) ? 4 : SPL;
+#ifndef MLOB_SMEM_UNR  // shared-memory books: rows per unrolled group (measured: 2)
+#define MLOB_SMEM_UNR 2
+#endif
+  static constexpr int kUnr = (SMEM && SPL >= MLOB_SMEM_UNR) ? MLOB_SMEM_UNR : SPL;
+  static constexpr int kScanUnr = (SMEM && SPL >= MLOB_SCAN_UNR) ? MLOB_SCAN_UNR : SPL;
   SideT bid, ask;
   const KParams& kp;
   const DevCfg& cfg;
@@ -799,7 +817,7 @@ struct WarpEnv {
   __device__ __forceinline__ int32_t side_best_t() {
     SideT& d = sd<S>();
     int32_t b = empty_price<S>();
-    MLOB_ROWS(k) b = better_of<S>(b, d.P(k));
+    MLOB_SCAN_ROWS(k) b = better_of<S>(b, d.P(k));
     return redux_best<S>(b);
   }
   // lane-local oldest slot (min st) at `price`
@@ -812,7 +830,7 @@ struct WarpEnv {
       // shared-memory book: one load per row for the price, the arrival word
       // only for the (few) rows at that price
       uint32_t cand = 0;
-      MLOB_ROWS(k) cand |= (d.P(k) == price ? 1u : 0u) << k;
+      MLOB_SCAN_ROWS(k) cand |= (d.P(k) == price ? 1u : 0u) << k;
       while (cand) {
         const int k = __ffs(cand) - 1;
         cand &= cand - 1;
@@ -840,7 +858,7 @@ struct WarpEnv {
       // shared-memory book: filter rows on the low id word (one load per row),
       // then check the high word and liveness of the candidates only
       uint32_t cand = 0;
-      MLOB_ROWS(k) cand |= (d.LO(k) == lo ? 1u : 0u) << k;
+      MLOB_SCAN_ROWS(k) cand |= (d.LO(k) == lo ? 1u : 0u) << k;
       while (cand) {
         const int k = __ffs(cand) - 1;
         cand &= cand - 1;
