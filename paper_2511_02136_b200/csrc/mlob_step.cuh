@@ -228,19 +228,47 @@ struct SmemSide {
   __device__ __forceinline__ uint32_t free_mask() const {
     return ~occ & (SPL >= 32 ? 0xffffffffu : ((1u << SPL) - 1u));
   }
+#ifndef MLOB_LW_UNROLL
+#define MLOB_LW_UNROLL 1
+#endif
+#ifndef MLOB_ACT_ROWS  // shared-memory books: active-order rebuild visits only agent rows
+#define MLOB_ACT_ROWS 1
+#endif
+#ifndef MLOB_LW_OCC  // worst-price rescans read only the price row, gated by the occupancy mask
+#define MLOB_LW_OCC 1
+#endif
   __device__ __forceinline__ void refresh_lw() {
     lw = side_ ? INT_MIN : INT_MAX;
 #if MLOB_LW_UNROLL
 #pragma unroll
 #endif
-    for (int k = 0; k < SPL; ++k)
+    for (int k = 0; k < SPL; ++k) {
+#if MLOB_LW_OCC
+      const int32_t p = p_[k * 32];
+      lw = (occ >> k) & 1u ? worse(lw, p) : lw;
+#else
       if (q_[k * 32] > 0) lw = worse(lw, p_[k * 32]);
+#endif
+    }
     lw_stale = 0;
   }
   __device__ __forceinline__ void recompute_occ() {
     occ = 0;
+#if MLOB_LW_OCC  // one pass: occupancy and worst price together
+    lw = side_ ? INT_MIN : INT_MAX;
+#if MLOB_LW_UNROLL
+#pragma unroll
+#endif
+    for (int k = 0; k < SPL; ++k) {
+      const int32_t q = q_[k * 32], p = p_[k * 32];
+      occ |= (q > 0 ? 1u : 0u) << k;
+      lw = q > 0 ? worse(lw, p) : lw;
+    }
+    lw_stale = 0;
+#else
     for (int k = 0; k < SPL; ++k) occ |= (q_[k * 32] > 0 ? 1u : 0u) << k;
     refresh_lw();
+#endif
   }
   __device__ __forceinline__ int32_t P(int k) const { return p_[k * 32]; }
   __device__ __forceinline__ int32_t Q(int k) const { return q_[k * 32]; }
@@ -1624,6 +1652,26 @@ struct WarpEnv {
   template <int S>
   __device__ __forceinline__ int compact_side(ActTmp* tmp, int base, int cap) {
     SideT& d = sd<S>();
+#if MLOB_ACT_ROWS
+    if constexpr (SMEM) {
+      // shared-memory book: one pass over the arrival words (gated by the
+      // occupancy mask) finds this lane's agent rows; only rows holding an
+      // agent order in some lane take the ballot (same row-major order)
+      uint32_t agm = 0;
+      MLOB_SCAN_ROWS(k) agm |= (((d.occ >> k) & 1u) && (d.ST(k) & 0xffu) != 0 ? 1u : 0u) << k;
+      uint32_t rows = __reduce_or_sync(FULLMASK, agm);
+      while (rows) {
+        const int k = __ffs(rows) - 1;
+        rows &= rows - 1;
+        const bool is_ag = (agm >> k) & 1u;
+        const uint32_t b = __ballot_sync(FULLMASK, is_ag);
+        const int pos = base + __popc(b & ((1u << lane) - 1u));
+        if (is_ag && pos < cap) tmp[pos] = ActTmp{d.P(k), d.ST(k), d.LO(k), d.HI(k), d.Q(k), 0};
+        base += __popc(b);
+      }
+      return base;
+    }
+#endif
     MLOB_ROWS(k) {
       const bool is_ag = d.Q(k) > 0 && (d.ST(k) & 0xffu) != 0;
       const uint32_t b = __ballot_sync(FULLMASK, is_ag);
