@@ -228,6 +228,9 @@ struct SmemSide {
   __device__ __forceinline__ uint32_t free_mask() const {
     return ~occ & (SPL >= 32 ? 0xffffffffu : ((1u << SPL) - 1u));
   }
+#ifndef MLOB_HWM_OCC  // shared-memory books: high-water mark from the occupancy masks
+#define MLOB_HWM_OCC 1
+#endif
 #ifndef MLOB_LW_UNROLL
 #define MLOB_LW_UNROLL 1
 #endif
@@ -649,9 +652,17 @@ struct WarpEnv {
   __device__ __forceinline__ int store_side() {
     SideT& d = sd<S>();
     int hwm = 0;
-    MLOB_ROWS(k) {
-      const uint32_t b = __ballot_sync(FULLMASK, d.Q(k) > 0);
-      if (b) hwm = k * kWarp + 32 - __clz(b);
+    if constexpr (SMEM && MLOB_HWM_OCC) {  // from the occupancy masks: one redux + one ballot
+      const uint32_t rows = __reduce_or_sync(FULLMASK, d.occ);
+      if (rows) {
+        const int k = 31 - __clz(rows);
+        hwm = k * kWarp + 32 - __clz(__ballot_sync(FULLMASK, (d.occ >> k) & 1u));
+      }
+    } else {
+      MLOB_ROWS(k) {
+        const uint32_t b = __ballot_sync(FULLMASK, d.Q(k) > 0);
+        if (b) hwm = k * kWarp + 32 - __clz(b);
+      }
     }
     if constexpr (SMEM) {  // rows below the high-water mark: four bulk stores
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // lanes' smem writes -> async proxy
