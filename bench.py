@@ -297,6 +297,8 @@ def gpu_arm(args) -> None:
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             prof = json.load(f)
+        if args.workload == "D":  # the deep-book kernel's own capture
+            prof = prof["deep_book_D"]
         traffic = prof["dram_bytes_per_msg"] * per_launch_msgs
     except Exception:
         pass
