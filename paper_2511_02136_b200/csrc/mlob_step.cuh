@@ -240,15 +240,29 @@ struct SmemSide {
 #ifndef MLOB_LW_OCC  // worst-price rescans read only the price row, gated by the occupancy mask
 #define MLOB_LW_OCC 1
 #endif
+#ifndef MLOB_LW_CNT  // experiment: count the lane's orders at its worst price (measured -30 % on D)
+#define MLOB_LW_CNT 0
+#endif
+  int lw_n;  // this lane's live orders at price lw (meaningful while !lw_stale)
+  __device__ __forceinline__ void lw_take(bool live, int32_t p) {
+    const bool w = live && (side_ ? p > lw : p < lw);  // strictly worse than lw
+    lw_n = w ? 1 : lw_n + ((live && p == lw) ? 1 : 0);
+    lw = w ? p : lw;
+  }
   __device__ __forceinline__ void refresh_lw() {
     lw = side_ ? INT_MIN : INT_MAX;
+    lw_n = 0;
 #if MLOB_LW_UNROLL
 #pragma unroll
 #endif
     for (int k = 0; k < SPL; ++k) {
 #if MLOB_LW_OCC
       const int32_t p = p_[k * 32];
+#if MLOB_LW_CNT
+      lw_take((occ >> k) & 1u, p);
+#else
       lw = (occ >> k) & 1u ? worse(lw, p) : lw;
+#endif
 #else
       if (q_[k * 32] > 0) lw = worse(lw, p_[k * 32]);
 #endif
@@ -259,13 +273,18 @@ struct SmemSide {
     occ = 0;
 #if MLOB_LW_OCC  // one pass: occupancy and worst price together
     lw = side_ ? INT_MIN : INT_MAX;
+    lw_n = 0;
 #if MLOB_LW_UNROLL
 #pragma unroll
 #endif
     for (int k = 0; k < SPL; ++k) {
       const int32_t q = q_[k * 32], p = p_[k * 32];
       occ |= (q > 0 ? 1u : 0u) << k;
+#if MLOB_LW_CNT
+      lw_take(q > 0, p);
+#else
       lw = q > 0 ? worse(lw, p) : lw;
+#endif
     }
     lw_stale = 0;
 #else
@@ -285,7 +304,11 @@ struct SmemSide {
     id_[k * 32] = make_uint2(lo, hi);
     st_[k * 32] = st;
     occ_set(k, q > 0);
+#if MLOB_LW_CNT
+    lw_take(q > 0, p);
+#else
     if (q > 0) lw = worse(lw, p);
+#endif
   }
   __device__ __forceinline__ void get_pq(int k, int32_t& p, int32_t& q) const {
     p = p_[k * 32];
@@ -310,7 +333,11 @@ struct SmemSide {
   }
   __device__ __forceinline__ void clear(int k, bool pred, int32_t empty_p) {
     if (pred) {
+#if MLOB_LW_CNT
+      if (p_[k * 32] == lw && --lw_n <= 0) lw_stale = 1;
+#else
       if (p_[k * 32] == lw) lw_stale = 1;
+#endif
       p_[k * 32] = empty_p;
       q_[k * 32] = 0;
       st_[k * 32] = kEmptySt;
@@ -320,6 +347,7 @@ struct SmemSide {
   __device__ __forceinline__ void bind(uint32_t* base, int lane, int side) {  // 5 x SPL*32 words
     side_ = side;
     lw = side ? INT_MIN : INT_MAX;
+    lw_n = 0;
     lw_stale = 1;
     occ = 0;
     base_ = base;
