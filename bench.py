@@ -241,7 +241,7 @@ def gpu_arm(args) -> None:
     env_steps = n_total * args.steps / (ms_max / 1e3)
 
     # K4 + NCCL: episode statistics reduced across ranks (the only collective)
-    stats = torch.zeros(5 * cfg.n_specs, dtype=torch.float64, device="cuda")
+    stats = torch.zeros(abi.STAT_WORDS * cfg.n_specs, dtype=torch.float64, device="cuda")
     venv.episode_stats_device(stats.data_ptr())
     venv.synchronize()
     allreduce(stats)

@@ -593,11 +593,27 @@ mlob_status mlob_venv_env_obs(mlob_venv* v, uint64_t env, double* out, uint64_t 
 
 /* MarketVecEnv::episode_stats / clear_episode_stats (rollout.hpp:255-278).
  * episode_stats sums this handle's envs in env order (bit-identical to the
- * reference); episode_stats_device reduces on the GPU (K4) into `out_device`
- * (5 doubles per type: pv, slip, completion, inv², episodes) for NCCL. */
+ * reference); episode_stats_device reduces on the GPU (K4) into `out_device`,
+ * MLOB_STAT_WORDS doubles per type (layout below), ready for an all-reduce.
+ * PV, slippage and inventory² are multiples of 0.5 and the remaining-quantity
+ * sum is an integer, so their sums are exact in any order; the exact
+ * completion sum is episodes·count − Σremaining / task_size (executors). */
+#define MLOB_STAT_WORDS 6
+enum { MLOB_STAT_PV = 0, MLOB_STAT_SLIPPAGE = 1, MLOB_STAT_COMPLETION = 2, MLOB_STAT_INVENTORY_SQ = 3,
+       MLOB_STAT_EPISODES = 4, MLOB_STAT_REMAINING = 5 };
 mlob_status mlob_venv_episode_stats(mlob_venv* v, int type, mlob_episode_stats* out);
 mlob_status mlob_venv_episode_stats_device(mlob_venv* v, double* out_device);
 mlob_status mlob_venv_clear_episode_stats(mlob_venv* v);
+/* The episode statistics of every type summed over all ranks of a NCCL
+ * communicator — the one collective of the path: K4 on this
+ * GPU, one ncclAllReduce(sum) of MLOB_STAT_WORDS doubles per type on the
+ * handle's stream, then per-type stats (completion formed exactly as above).
+ * Replaces MarketVecEnv::episode_stats (rollout.hpp:255-270) as the trainer
+ * consumes it per update (train.hpp:200-219) when the envs are sharded over
+ * GPUs.  nccl_comm: an ncclComm_t (one rank per GPU) or NULL for this handle
+ * alone; ncclAllReduce is resolved at run time from the process's
+ * libnccl.so.2 (MLOB_E_RUNTIME if absent).  out: [n_types]. */
+mlob_status mlob_venv_allreduce_episode_stats(mlob_venv* v, void* nccl_comm, mlob_episode_stats* out);
 
 /* Parity readers in reference record formats. */
 mlob_status mlob_venv_read_scalars(mlob_venv* v, uint64_t env, mlob_env_scalars* out);

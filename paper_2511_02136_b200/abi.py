@@ -30,6 +30,7 @@ MAX_GAMMA = 16
 MAX_ACTIVE = 8
 MAX_SPECS = 8
 MAX_AGENTS = 32
+STAT_WORDS = 6  # MLOB_STAT_WORDS: pv, slippage, completion, inventory², episodes, Σ remaining
 
 VENV_AUTO_RESET = 1 << 0
 VENV_RECORD_TRADES = 1 << 1

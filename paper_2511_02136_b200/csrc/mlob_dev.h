@@ -42,6 +42,36 @@ struct EpState {
   uint32_t _pad;
 };
 
+// One agent-side fill of the step, in fill order (env.hpp:381-396: the
+// passive agent's entry first, then the aggressor's).  The outcome kernel
+// replays the log for the agent accounting, the slippage sums and the MM
+// rewards (rewards.hpp:22-36), so every sum keeps the reference's order.
+struct FillEnt {
+  int32_t price;
+  int32_t qty;
+  int32_t agent;
+  int32_t side;
+};
+constexpr int kStatWords = 6;            // K4 doubles per agent type (stats_kernel)
+constexpr int kFillInline = 16;          // per-env inline fill-log entries
+constexpr int kFillChunk = 32;           // overflow chunk: entry 0 links the next chunk
+constexpr uint32_t kNoChunk = 0xffffffffu;
+
+// One aggregated L2 level (book.hpp:209-220).
+struct L2Lvl {
+  int32_t price;
+  int32_t _pad;
+  int64_t qty;
+};
+// Step summary of the book for the observations (observations.hpp:42-148):
+// level counts within obs_depth, top-of-book and top-D quantities per side.
+struct L2Sum {
+  int32_t nb, na;
+  int64_t sumq0, sumq1, topq0, topq1;
+  int64_t _pad;
+};
+static_assert(sizeof(L2Sum) == 48, "L2Sum must be 48 bytes");
+
 struct DevLevel {
   int32_t price;
   int32_t qty;
@@ -86,7 +116,10 @@ struct EnvHdr {
   int32_t best[2];
   uint32_t n_trades;
   uint8_t terminal, just_reset, _pad8[2];
-  uint64_t _pad64[2];
+  // split-step hand-offs: agent messages of this step (act_kernel ->
+  // book_kernel), agent fills logged (book_kernel -> outcome_kernel) and the
+  // first overflow chunk of the fill log (kNoChunk: none)
+  uint32_t n_amsg, n_fills, fill_head, _pad32;
 };
 static_assert(sizeof(EnvHdr) == 128, "EnvHdr must be 128 bytes");
 
@@ -124,6 +157,8 @@ enum DevError : uint32_t {
   kErrSeqRange = 1u << 4,       // arrival_seq beyond 2^24
   kErrBadAction = 1u << 5,      // device-resident action id out of range (actions.hpp:69-70)
   kErrBadTrader = 1u << 6,      // replay trader_id names a non-existent agent
+  kErrFillPool = 1u << 7,       // agent-fill overflow pool exhausted in one step
+  kErrAmsgCap = 1u << 8,        // more agent messages in one step than the hand-off buffer holds
 };
 
 struct __align__(16) KParams {
@@ -157,6 +192,7 @@ struct __align__(16) KParams {
   double* t_slip;
   double* t_comp;
   double* t_inv;
+  int64_t* t_rem;          // Σ task_remaining of finished executor episodes [env * A + a]
   mlob_trade* trades;      // [env * trade_cap + i]
   uint32_t trade_cap;
   uint32_t fill_overflows_unused;
@@ -177,6 +213,15 @@ struct __align__(16) KParams {
   const DevPolicy* policies;
   const uint8_t* env_policy;
   const uint64_t* env_cell;
+  // split step hand-offs (per env, offset with the launch's env range)
+  DevMsg* amsg;              // [env * amsg_cap + i] agent messages in processing order
+  FillEnt* fills;            // [env * kFillInline + i] inline agent-fill log
+  L2Sum* l2sum;              // [env]
+  L2Lvl* l2lv;               // [env * 2 * obs_depth] MMFull levels (null unless some agent uses them)
+  FillEnt* fill_pool;        // overflow chunks of this launch's env range
+  uint32_t* fill_pool_ctr;   // chunks taken (zeroed by the launch's act_kernel)
+  uint32_t fill_pool_chunks;
+  uint32_t amsg_cap;
 };
 
 }  // namespace mlob

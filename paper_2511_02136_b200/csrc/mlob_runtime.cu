@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <dlfcn.h>
 #include <memory>
 #include <string>
 #include <vector>
@@ -23,6 +24,8 @@
 
 namespace mlob {
 size_t step_min_smem_bytes(const DevCfg& c);
+uint32_t step_amsg_cap(const DevCfg& c);
+int step_launches();
 int slots_per_lane(int capacity);
 cudaError_t launch_step(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s);
 cudaError_t launch_reset(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s);
@@ -108,6 +111,8 @@ struct mlob_store {
     return it - st_index.begin();
   }
 };
+
+constexpr uint64_t kMaxIoChunks = 16;  // step_io env chunks (each owns a share of the fill pool)
 
 struct mlob_venv {
   const mlob_store* store = nullptr;
@@ -202,16 +207,28 @@ struct mlob_venv {
   uint8_t* d_just_reset = nullptr;
   double* d_t[4] = {};
   mlob_trade* d_trades = nullptr;
-  unsigned long long* d_fill_overflow = nullptr;
+  // split-step hand-offs (mlob_kernels.cu): agent messages, fill log + overflow pool, L2 summary
+  DevMsg* d_amsg = nullptr;
+  uint32_t amsg_cap = 0;
+  FillEnt* d_fills = nullptr;
+  FillEnt* d_fill_pool = nullptr;
+  uint32_t* d_fill_pool_ctr = nullptr;  // one counter per step_io chunk
+  uint64_t fill_pool_chunks = 0;
+  L2Sum* d_l2sum = nullptr;
+  L2Lvl* d_l2lv = nullptr;
+  int64_t* d_t_rem = nullptr;
   uint64_t* d_env_seed = nullptr;
   uint64_t* d_env_index = nullptr;
   uint64_t* d_reset_eps = nullptr;
   uint32_t* d_error = nullptr;
   unsigned long long* d_scratch = nullptr;
-  unsigned long long* d_ticket = nullptr;
-  long long* d_timing = nullptr;
   DevCfg* d_cfg = nullptr;
 
+  double* d_stats = nullptr;  // K4 output for mlob_venv_allreduce_episode_stats
+  double* alloc_scratch_stats() {
+    if (!d_stats) d_stats = alloc<double>(static_cast<size_t>(MLOB_MAX_SPECS) * kStatWords, "stats");
+    return d_stats;
+  }
   template <class T>
   T* alloc(size_t n, const char* what) {
     T* p = dalloc<T>(n, what);
@@ -269,9 +286,15 @@ struct mlob_venv {
     k.t_inv = d_t[3];
     k.trades = d_trades;
     k.trade_cap = trade_cap;
-    k.fill_overflow = d_fill_overflow;
-    k.ticket = d_ticket;
-    k.timing = d_timing;
+    k.t_rem = d_t_rem;
+    k.amsg = d_amsg;
+    k.amsg_cap = amsg_cap;
+    k.fills = d_fills;
+    k.l2sum = d_l2sum;
+    k.l2lv = d_l2lv;
+    k.fill_pool = d_fill_pool;
+    k.fill_pool_ctr = d_fill_pool_ctr;
+    k.fill_pool_chunks = static_cast<uint32_t>(fill_pool_chunks);
     k.env_seed = d_env_seed;
     k.env_index = d_env_index;
     k.seed = seed;
@@ -308,6 +331,8 @@ struct mlob_venv {
     if (e & kErrSeqRange) fail(MLOB_E_RUNTIME, "arrival sequence beyond 2^24 in one episode");
     if (e & kErrActiveOverflow) fail(MLOB_E_RUNTIME, "more than MLOB_MAX_ACTIVE resting orders for one agent");
     if (e & kErrBadTrader) fail(MLOB_E_RUNTIME, "replay trader_id names a non-existent agent");
+    if (e & kErrFillPool) fail(MLOB_E_RUNTIME, "agent-fill log overflow pool exhausted in one step");
+    if (e & kErrAmsgCap) fail(MLOB_E_RUNTIME, "more agent messages in one step than the hand-off buffer holds");
     fail(MLOB_E_RUNTIME, "device error");
   }
 
@@ -822,10 +847,19 @@ mlob_status mlob_venv_create(const mlob_venv_desc* desc, mlob_venv** out) {
     v->d_just_reset = v->alloc<uint8_t>(n, "just_reset");
     for (int i = 0; i < 4; ++i) v->d_t[i] = v->alloc<double>(n * std::max(A, 1), "stats");
     if (v->trade_cap) v->d_trades = v->alloc<mlob_trade>(n * v->trade_cap, "trades");
-    v->d_fill_overflow = v->alloc<unsigned long long>(1, "fill_overflow");
+    v->d_t_rem = v->alloc<int64_t>(n * std::max(A, 1), "stats");
     v->d_scratch = v->alloc<unsigned long long>(8, "scratch");
-    v->d_ticket = v->alloc<unsigned long long>(1, "ticket");
-    if (std::getenv("MLOB_TIMING")) v->d_timing = v->alloc<long long>(n * 16, "timing");
+    v->amsg_cap = step_amsg_cap(v->dcfg);
+    v->d_amsg = v->alloc<DevMsg>(n * v->amsg_cap, "agent messages");
+    v->d_fills = v->alloc<FillEnt>(n * kFillInline, "fill log");
+    // overflow pool: enough chunks for every env of the step to log 32 more
+    // agent fills than the inline part holds (beyond: MLOB_E_RUNTIME), split
+    // evenly over the step_io chunks, >= 64 chunks each
+    v->fill_pool_chunks = std::max<uint64_t>(n / 8, 64 * kMaxIoChunks);
+    v->d_fill_pool = v->alloc<FillEnt>(v->fill_pool_chunks * kFillChunk, "fill pool");
+    v->d_fill_pool_ctr = v->alloc<uint32_t>(kMaxIoChunks, "fill pool counters");
+    v->d_l2sum = v->alloc<L2Sum>(n, "l2 summary");
+    if (v->dcfg.full_l2) v->d_l2lv = v->alloc<L2Lvl>(n * 2 * c.obs_depth, "l2 levels");
     v->d_reset_eps = v->alloc<uint64_t>(n, "reset_eps");
     v->d_error = v->alloc<uint32_t>(1, "error");
     if (desc->env_seeds) {
@@ -956,8 +990,8 @@ static void do_step(mlob_venv* v, int mode, uint64_t bench_seed, uint64_t global
   kp.action_mode = mode;
   kp.bench_seed = bench_seed;
   kp.global_step = global_step;
-  cuda_check(launch_step(kp, v->dcfg, v->spl, v->stream), "step kernel");
-  ++v->launches;
+  cuda_check(launch_step(kp, v->dcfg, v->spl, v->stream), "step kernels");
+  v->launches += step_launches();
   advance_step(v);
 }
 
@@ -1216,7 +1250,7 @@ mlob_status mlob_venv_collect_rollout(mlob_venv* v, const mlob_rollout_config* c
     const uint64_t T = static_cast<uint64_t>(cfg->rollout_len);
     const int NT = v->cfg.n_specs;
     for (int t = 0; t < NT; ++t) ensure_batch(v, t, T);
-    const uint64_t launches = T * (NT + 1) + 2 * NT;
+    const uint64_t launches = T * (NT + step_launches()) + 2 * NT;
     if (std::getenv("MLOB_NO_GRAPH")) {  // diagnostics: plain launches
       enqueue_rollout(v, *cfg, update_index, T, nullptr);
     } else {
@@ -1718,8 +1752,19 @@ mlob_status mlob_evaluate_matrix(const mlob_store* store, const mlob_env_config*
 
 // KParams of the env range [c0, c0 + n): every per-env array offset by c0,
 // the global env identity (RNG keys, episode pool) kept
-static KParams chunk_params(const mlob_venv* v, const KParams& k0, uint64_t c0, uint64_t n) {
+static KParams chunk_params(const mlob_venv* v, const KParams& k0, uint64_t c0, uint64_t n, uint64_t idx,
+                            uint64_t nchunks) {
   KParams k = k0;
+  // hand-off buffers and this chunk's share of the fill-overflow pool
+  k.amsg += c0 * v->amsg_cap;
+  k.fills += c0 * kFillInline;
+  k.l2sum += c0;
+  if (k.l2lv) k.l2lv += c0 * 2 * v->cfg.obs_depth;
+  k.t_rem += c0 * static_cast<uint64_t>(v->A);
+  const uint64_t per = v->fill_pool_chunks / nchunks;
+  k.fill_pool += idx * per * kFillChunk;
+  k.fill_pool_chunks = static_cast<uint32_t>(per);
+  k.fill_pool_ctr += idx;
   const uint64_t A = static_cast<uint64_t>(v->A);
   const size_t bs = static_cast<size_t>(2 * v->spl * kWarp) * c0;
   k.bk_p += bs;
@@ -1742,7 +1787,6 @@ static KParams chunk_params(const mlob_venv* v, const KParams& k0, uint64_t c0, 
   k.t_comp += c0 * A;
   k.t_inv += c0 * A;
   if (k.trades) k.trades += c0 * v->trade_cap;
-  if (k.timing) k.timing += c0 * 16;
   if (k.env_seed) k.env_seed += c0;
   if (k.env_index) k.env_index += c0;
   k.env_index_base += c0;
@@ -1752,7 +1796,7 @@ static KParams chunk_params(const mlob_venv* v, const KParams& k0, uint64_t c0, 
 
 static uint64_t io_chunk_envs(uint64_t n) {
   if (const char* e = std::getenv("MLOB_IO_CHUNKS")) {  // diagnostics: fixed chunk count
-    const uint64_t c = std::strtoull(e, nullptr, 10);
+    const uint64_t c = std::min<uint64_t>(std::strtoull(e, nullptr, 10), kMaxIoChunks);
     if (c > 0) return (n + c - 1) / c;
   }
   // ≤ 8 chunks of ≥ 16k envs: each chunk is several rounds of the step kernel,
@@ -1809,8 +1853,8 @@ mlob_status mlob_venv_step_io(mlob_venv* v, const mlob_step_io* io) {
     for (uint64_t i = 0; i < nc; ++i) {
       const uint64_t c0 = i * chunk, m = std::min(chunk, n - c0);
       cudaStream_t s = (i & 1) ? v->stream2 : v->stream;
-      cuda_check(launch_step(chunk_params(v, k0, c0, m), v->dcfg, v->spl, s), "step kernel");
-      ++v->launches;
+      cuda_check(launch_step(chunk_params(v, k0, c0, m, i, nc), v->dcfg, v->spl, s), "step kernels");
+      v->launches += step_launches();
       for (int t = 0; t < v->cfg.n_specs; ++t)
         if (io->resets[t] && v->cfg.specs[t].count > 1) {
           const int cnt = v->cfg.specs[t].count;
@@ -1905,12 +1949,58 @@ mlob_status mlob_venv_episode_stats_device(mlob_venv* v, double* out_device) {
   });
 }
 
+// ncclAllReduce from the process's NCCL (the caller's communicator must come
+// from the same library): an already-loaded libnccl.so.2 first, else load it.
+using NcclAllReduceFn = int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+static NcclAllReduceFn nccl_allreduce() {
+  static NcclAllReduceFn fn = [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    return h ? reinterpret_cast<NcclAllReduceFn>(dlsym(h, "ncclAllReduce")) : nullptr;
+  }();
+  return fn;
+}
+constexpr int kNcclFloat64 = 8, kNcclSum = 0;  // nccl.h ncclDataType_t / ncclRedOp_t
+
+mlob_status mlob_venv_allreduce_episode_stats(mlob_venv* v, void* nccl_comm, mlob_episode_stats* out) {
+  return guarded([&] {
+    v->set_device();
+    const int NT = v->cfg.n_specs;
+    double* d = v->alloc_scratch_stats();
+    cuda_check(launch_stats(v->params(), v->dcfg, d, v->stream), "stats kernel");
+    ++v->launches;
+    if (nccl_comm) {
+      const NcclAllReduceFn f = nccl_allreduce();
+      if (!f) fail(MLOB_E_RUNTIME, "ncclAllReduce not found (libnccl.so.2 not loadable)");
+      const int r = f(d, d, static_cast<size_t>(NT) * kStatWords, kNcclFloat64, kNcclSum, nccl_comm, v->stream);
+      if (r != 0) fail(MLOB_E_RUNTIME, "ncclAllReduce failed with ncclResult_t " + std::to_string(r));
+    }
+    std::vector<double> h(static_cast<size_t>(NT) * kStatWords);
+    d2h(v, h.data(), d, h.size());
+    for (int t = 0; t < NT; ++t) {
+      const double* w = h.data() + t * kStatWords;
+      mlob_episode_stats& o = out[t];
+      std::memset(&o, 0, sizeof o);
+      o.pv_sum = w[MLOB_STAT_PV];
+      o.slippage_sum = w[MLOB_STAT_SLIPPAGE];
+      o.inventory_sq_sum = w[MLOB_STAT_INVENTORY_SQ];
+      o.episodes = static_cast<int64_t>(w[MLOB_STAT_EPISODES]);
+      const mlob_agent_spec& sp = v->cfg.specs[t];
+      o.completion_sum = sp.type == MLOB_EXECUTOR
+                             ? w[MLOB_STAT_EPISODES] * sp.count -
+                                   w[MLOB_STAT_REMAINING] / static_cast<double>(sp.params.task_size)
+                             : 0.0;
+    }
+  });
+}
+
 mlob_status mlob_venv_clear_episode_stats(mlob_venv* v) {
   return guarded([&] {
     v->set_device();
     const uint64_t na = v->n_envs * v->A;
     for (int i = 0; i < 4; ++i)
       cuda_check(cudaMemsetAsync(v->d_t[i], 0, std::max<uint64_t>(na, 1) * 8, v->stream), "memset");
+    cuda_check(cudaMemsetAsync(v->d_t_rem, 0, std::max<uint64_t>(na, 1) * 8, v->stream), "memset");
     cuda_check(launch_clear_finished(v->d_hdr, v->n_envs, v->stream), "clear kernel");
     ++v->launches;
   });
@@ -2020,13 +2110,6 @@ mlob_status mlob_venv_read_trades(mlob_venv* v, uint64_t env, mlob_trade* out, u
                                std::to_string(v->trade_cap));
     const uint64_t n = std::min<uint64_t>(h.n_trades, cap);
     if (n) d2h(v, out, v->d_trades + env * v->trade_cap, n);
-  });
-}
-
-mlob_status mlob_venv_read_timing(mlob_venv* v, long long* out) {
-  return guarded([&] {
-    if (!v->d_timing) fail(MLOB_E_LOGIC, "timing buffer not allocated (set MLOB_TIMING)");
-    d2h(v, out, v->d_timing, v->n_envs * 16);
   });
 }
 

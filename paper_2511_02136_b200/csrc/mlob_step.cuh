@@ -371,21 +371,6 @@ __device__ __forceinline__ int32_t redux_best(int32_t v) {
   return S == 0 ? __reduce_max_sync(FULLMASK, v) : __reduce_min_sync(FULLMASK, v);
 }
 
-// Per-agent per-step accumulators (fills of this step, env.hpp:222, 381-396).
-struct StepAcc {
-  double slip;     // slippage(fills, p_init, dir) accumulated in fill order
-  int64_t filled;  // Σ qty
-  int64_t sq[2];   // Σ qty by side (MM reward fallback beyond kFillLog fills)
-  int64_t spq[2];  // Σ price*qty by side
-  int32_t count;
-  int32_t _pad;
-};
-struct FillEnt {  // exact per-env fill log for the MM rewards (rewards.hpp:22-36)
-  int32_t price;
-  int32_t qty;
-  int32_t agent;
-  int32_t side;
-};
 struct ActTmp {  // one agent-owned resting order, rebuild_active scratch (fits a DevMsg slot)
   int32_t price;
   uint32_t st;
@@ -395,34 +380,25 @@ struct ActTmp {  // one agent-owned resting order, rebuild_active scratch (fits 
 };
 static_assert(sizeof(ActTmp) <= sizeof(DevMsg), "ActTmp reuses the agent-message smem");
 
-struct L2Lvl {
-  int32_t price;
-  int32_t _pad;
-  int64_t qty;
-};
-
 // Per-warp shared-memory regions.  The region offsets are the same for every
 // warp of a block (they depend on the config only), so they live once in a
 // block-shared table and a warp keeps only its base pointer: eleven 64-bit
 // region pointers held in registers across the message loop forced spills
 // at the 80-register cap.
 struct SmemOff {
-  uint32_t chunk0, chunk1, bar, amsg, ag, act, acc, fills, scal, l2, obs, _pad;
+  uint32_t chunk0, chunk1, bar, amsg, act, nact, scal, l2;
 };
-__shared__ __align__(16) SmemOff g_smem_off;  // written by carve() (identical values from every warp)
+__shared__ __align__(16) SmemOff g_smem_off;  // written once per block by carve_block()
 struct WarpSmem {
   char* base;
   __device__ __forceinline__ DevMsg* chunk0() const { return reinterpret_cast<DevMsg*>(base + g_smem_off.chunk0); }
   __device__ __forceinline__ DevMsg* chunk1() const { return reinterpret_cast<DevMsg*>(base + g_smem_off.chunk1); }
   __device__ __forceinline__ uint64_t* bar() const { return reinterpret_cast<uint64_t*>(base + g_smem_off.bar); }
   __device__ __forceinline__ DevMsg* amsg() const { return reinterpret_cast<DevMsg*>(base + g_smem_off.amsg); }
-  __device__ __forceinline__ AgentRec* ag() const { return reinterpret_cast<AgentRec*>(base + g_smem_off.ag); }
   __device__ __forceinline__ ActiveRec* act() const { return reinterpret_cast<ActiveRec*>(base + g_smem_off.act); }
-  __device__ __forceinline__ StepAcc* acc() const { return reinterpret_cast<StepAcc*>(base + g_smem_off.acc); }
-  __device__ __forceinline__ FillEnt* fills() const { return reinterpret_cast<FillEnt*>(base + g_smem_off.fills); }
+  __device__ __forceinline__ int32_t* nact() const { return reinterpret_cast<int32_t*>(base + g_smem_off.nact); }
   __device__ __forceinline__ int32_t* scal() const { return reinterpret_cast<int32_t*>(base + g_smem_off.scal); }
   __device__ __forceinline__ L2Lvl* l2() const { return reinterpret_cast<L2Lvl*>(base + g_smem_off.l2); }
-  __device__ __forceinline__ double* obs() const { return reinterpret_cast<double*>(base + g_smem_off.obs); }
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -459,12 +435,12 @@ struct MsgRef {
   int32_t trader;
   __device__ __forceinline__ uint64_t order_id() const {
     uint32_t lo, hi;
-    asm("ld.shared.v2.u32 {%0,%1}, [%2+8];" : "=r"(lo), "=r"(hi) : "r"(a));
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2+8];" : "=r"(lo), "=r"(hi) : "r"(a) : "memory");
     return (static_cast<uint64_t>(hi) << 32) | lo;
   }
   __device__ __forceinline__ int64_t time() const {
     uint32_t lo, hi;
-    asm("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(a));
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(a) : "memory");
     return static_cast<int64_t>((static_cast<uint64_t>(hi) << 32) | lo);
   }
 };
@@ -518,51 +494,6 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// env.hpp:372-396 (attribute_trade -> apply_fill for the passive, then the
-// aggressor agent); executed by lane 0 only, in fill order.  Agent state is
-// not read inside the message loop, so the other lanes see it after the
-// loop's closing __syncwarp.
-__device__ __forceinline__ void attribute_fill(int n_agents, const DevCfg& cfg, WarpSmem sm,
-                                               int32_t price, int32_t qty, int ptrader, int atrader,
-                                               int aside) {
-  for (int r = 0; r < 2; ++r) {
-    const int trader = r == 0 ? ptrader : atrader;
-    if (trader <= 0 || trader > n_agents) continue;
-    const int a = trader - 1;
-    const int side = r == 0 ? 1 - aside : aside;
-    const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
-    AgentRec& st = sm.ag()[a];
-    StepAcc& ac = sm.acc()[a];
-    const int64_t pq = static_cast<int64_t>(price) * qty;
-    if (side == MLOB_BID) {
-      st.inventory += qty;
-      st.cash -= pq;
-    } else {
-      st.inventory -= qty;
-      st.cash += pq;
-    }
-    st.filled_total += qty;
-    if (sp.type == MLOB_EXECUTOR) {
-      const bool task_side = (st.task_dir == MLOB_TASK_BUY) == (side == MLOB_BID);
-      if (task_side) st.task_remaining = max(static_cast<int64_t>(0), st.task_remaining - qty);
-    }
-    // slippage term, rewards.hpp:69-75: (sign * q) * (price - p_init)
-    const double sign = st.task_dir == MLOB_TASK_BUY ? 1.0 : -1.0;
-    ac.slip += sign * static_cast<double>(qty) * (static_cast<double>(price) - st.p_init);
-    ac.filled += qty;
-    ac.count += 1;
-    ac.sq[side] += qty;
-    ac.spq[side] += pq;
-    const int nf = sm.scal()[0];
-    if (nf < kFillLog) {
-      sm.fills()[nf] = FillEnt{price, qty, a, side};
-      sm.scal()[0] = nf + 1;
-    } else {
-      sm.scal()[1] = 1;
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 #ifndef MLOB_ST_MATCH  // register books: address slots by their unique arrival word
 #define MLOB_ST_MATCH 1
@@ -605,19 +536,20 @@ struct WarpEnv {
   const DevCfg& cfg;
   WarpSmem sm;
   int lane;
-  uint64_t env, genv, seed;
+  uint64_t env;
   // uniform state (identical in every lane)
   int live0, live1;
   int32_t best0, best1;
   uint32_t next_seq;
   int64_t mid_half, prev_mid_half, last_bid, last_ask, last_time;
   double mbar;
-  uint64_t episode, msgs, cursor;
-  int64_t ep_finished;
+  uint64_t episode, msgs;
   int step;
   bool terminal;
   int64_t mid_sum, mid_count;
   uint32_t n_trades;
+  uint32_t n_fills, fill_head, fill_cur;  // agent-fill log (inline, then overflow chunks)
+  uint32_t n_amsg;
   uint32_t err;
   // config words cached in registers (measured: reading them from the staged
   // shared-memory copy at each use is 4% slower)
@@ -626,7 +558,7 @@ struct WarpEnv {
   __device__ __forceinline__ int capacity() const { return capacity_; }
   __device__ __forceinline__ bool rec_trades() const { return rec_trades_; }
   __device__ __forceinline__ int n_agents() const { return n_agents_; }
-  int nb_l2, na_l2;    // L2 levels staged in smem by snapshot()
+  int nb_l2, na_l2;      // top-D level counts (snapshot)
   int64_t topq0, topq1;  // level-0 aggregated qty per side
   int64_t sumq0, sumq1;  // Σ qty over the top-D levels per side
 
@@ -638,18 +570,13 @@ struct WarpEnv {
       bid.bind(book_smem, ln, 0);
       ask.bind(book_smem + 5 * SPL * 32, ln, 1);
     }
-    bind(e);
     err = 0;
     capacity_ = c.capacity;
     rec_trades_ = (p.flags & MLOB_VENV_RECORD_TRADES) != 0;
     n_agents_ = c.n_agents;
   }
 
-  __device__ __forceinline__ void bind(uint64_t e) {
-    env = e;
-    genv = kp.env_index ? kp.env_index[e] : kp.env_index_base + e;
-    seed = kp.env_seed ? kp.env_seed[e] : kp.seed;
-  }
+  __device__ __forceinline__ void bind(uint64_t e) { env = e; }
 
   template <int S>
   __device__ __forceinline__ SideT& sd() {
@@ -721,23 +648,18 @@ struct WarpEnv {
   __device__ __forceinline__ void load_hdr() {
     const EnvHdr& h = kp.hdr[env];
     mid_half = h.mid_half;
-    prev_mid_half = h.prev_mid_half;
-    mbar = h.mbar;
     last_bid = h.last_bid;
     last_ask = h.last_ask;
     last_time = h.last_time;
     episode = h.episode;
     msgs = h.msgs_processed;
-    cursor = h.cursor;
-    ep_finished = h.episodes_finished;
     next_seq = h.next_seq;
     step = h.step;
     live0 = h.live[0];
     live1 = h.live[1];
     best0 = h.best[0];
     best1 = h.best[1];
-    terminal = h.terminal != 0;
-    n_trades = h.n_trades;
+    n_amsg = h.n_amsg;
   }
   __device__ __forceinline__ void load_book() {
     const EnvHdr& h = kp.hdr[env];
@@ -822,20 +744,19 @@ struct WarpEnv {
       if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
   }
-  __device__ __forceinline__ void store_state(uint8_t just_reset) {
+  // The header fields the book kernel advances (the outcome kernel owns
+  // the rest: episode bookkeeping, auto-reset).
+  __device__ __forceinline__ void store_hdr() {
     const int h0 = hwm0, h1 = hwm1;
     if (lane == 0) {
-      EnvHdr h;
+      EnvHdr& h = kp.hdr[env];
       h.mid_half = mid_half;
       h.prev_mid_half = prev_mid_half;
       h.mbar = mbar;
       h.last_bid = last_bid;
       h.last_ask = last_ask;
       h.last_time = last_time;
-      h.episode = episode;
       h.msgs_processed = msgs;
-      h.cursor = cursor;
-      h.episodes_finished = ep_finished;
       h.next_seq = next_seq;
       h.step = step;
       h.live[0] = static_cast<uint16_t>(live0);
@@ -846,36 +767,18 @@ struct WarpEnv {
       h.best[1] = best1;
       h.n_trades = n_trades;
       h.terminal = terminal ? 1 : 0;
-      h.just_reset = just_reset;
-      h._pad8[0] = h._pad8[1] = 0;
-      h._pad64[0] = h._pad64[1] = 0;
-      kp.hdr[env] = h;
-      kp.just_reset[env] = just_reset;
-    }
-    const int A = cfg.n_agents;
-    const int words = A * static_cast<int>(sizeof(AgentRec) / 8);
-    const uint64_t* src = reinterpret_cast<const uint64_t*>(sm.ag());
-    uint64_t* dst = reinterpret_cast<uint64_t*>(kp.agents + env * A);
-    for (int i = lane; i < words; i += kWarp) dst[i] = src[i];
-    for (int a = 0; a < A; ++a) {
-      const int n = sm.ag()[a].n_active;
-      if (lane < n) kp.active[(env * A + a) * kMaxActive + lane] = sm.act()[a * kMaxActive + lane];
+      h.n_fills = n_fills;
+      h.fill_head = fill_head;
     }
   }
   __device__ __forceinline__ void report_errors() {
     if (err && lane == 0) atomicOr(kp.error, err);
   }
-  __device__ __forceinline__ void load_agents() {
-    const int A = cfg.n_agents;
-    const int words = A * static_cast<int>(sizeof(AgentRec) / 8);
-    const uint64_t* src = reinterpret_cast<const uint64_t*>(kp.agents + env * A);
-    uint64_t* dst = reinterpret_cast<uint64_t*>(sm.ag());
-    for (int i = lane; i < words; i += kWarp) dst[i] = src[i];
-    __syncwarp();
-    for (int a = 0; a < A; ++a) {
-      const int n = sm.ag()[a].n_active;
-      if (lane < n) sm.act()[a * kMaxActive + lane] = kp.active[(env * A + a) * kMaxActive + lane];
-    }
+  // this step's agent messages (act_kernel's hand-off) into shared memory
+  __device__ __forceinline__ void load_agent_msgs() {
+    const uint4* src = reinterpret_cast<const uint4*>(kp.amsg + env * kp.amsg_cap);
+    uint4* dst = reinterpret_cast<uint4*>(sm.amsg());
+    for (uint32_t i = lane; i < 2 * n_amsg; i += kWarp) dst[i] = src[i];
     __syncwarp();
   }
 
@@ -1129,8 +1032,41 @@ struct WarpEnv {
     }
     ++n_trades;
     const uint32_t pt = st & 0xffu;
-    if ((pt | static_cast<uint32_t>(m.trader)) && lane == 0)  // an agent is involved
-      attribute_fill(n_agents(), cfg, sm, price, qty, static_cast<int>(pt), m.trader, aside);
+    if (pt | static_cast<uint32_t>(m.trader)) {  // an agent may be involved: env.hpp:372-379 order
+      log_fill(price, qty, static_cast<int>(pt), 1 - aside);
+      log_fill(price, qty, m.trader, aside);
+    }
+  }
+
+  // Appends one agent-side fill to the env's log (inline entries, then
+  // overflow chunks taken from the launch's pool).  Called by every lane with
+  // the same arguments; lane 0 writes.
+  __device__ __forceinline__ void log_fill(int32_t price, int32_t qty, int trader, int side) {
+    if (trader <= 0 || trader > n_agents()) return;
+    const uint32_t i = n_fills;
+    FillEnt* dst;
+    if (i < static_cast<uint32_t>(kFillInline)) {
+      dst = kp.fills + env * kFillInline + i;
+    } else {
+      const uint32_t k = i - kFillInline, off = k % (kFillChunk - 1) + 1;
+      if (off == 1) {  // a new overflow chunk, linked from the previous one
+        uint32_t c = 0;
+        if (lane == 0) c = atomicAdd(kp.fill_pool_ctr, 1u);
+        c = __shfl_sync(FULLMASK, c, 0);
+        if (c >= kp.fill_pool_chunks) {
+          err |= kErrFillPool;
+          return;
+        }
+        if (k == 0)
+          fill_head = c;
+        else if (lane == 0)
+          kp.fill_pool[static_cast<size_t>(fill_cur) * kFillChunk].price = static_cast<int32_t>(c);
+        fill_cur = c;
+      }
+      dst = kp.fill_pool + static_cast<size_t>(fill_cur) * kFillChunk + off;
+    }
+    if (lane == 0) *dst = FillEnt{price, qty, trader - 1, side};
+    n_fills = i + 1;
   }
 
   bool moved;  // a top (best price or side emptiness) changed: refresh the mid
@@ -1378,231 +1314,6 @@ struct WarpEnv {
     __syncwarp();  // lane 0's agent updates become visible to the warp
   }
 
-  // ---- agents (agents/actions.hpp, env.hpp:266-370) ----------------------
-  __device__ __forceinline__ void effective_tops(const DevSpec& p, int64_t& bid_, int64_t& ask_) const {
-    const int64_t mid_floor = mid_half >= 0 ? mid_half / 2 : (mid_half - 1) / 2;
-    const int64_t mid_ceil = (mid_half + 1) / 2;
-    bid_ = live0 > 0 ? static_cast<int64_t>(best0) : mid_floor - p.default_half_spread;
-    ask_ = live1 > 0 ? static_cast<int64_t>(best1) : mid_ceil + p.default_half_spread;
-    if (bid_ < 1) bid_ = 1;
-    if (ask_ <= bid_) ask_ = bid_ + 1;
-  }
-
-  struct Quotes {  // agents::QuoteList (actions.hpp:24-40), no dynamic indexing
-    int n;
-    int s0, s1;
-    int64_t p0, p1, q0, q1;
-    __device__ void push(int s, int64_t p, int64_t q) {
-      if (n == 0) {
-        s0 = s;
-        p0 = p;
-        q0 = q;
-      } else {
-        s1 = s;
-        p1 = p;
-        q1 = q;
-      }
-      ++n;
-    }
-    __device__ void finish_two_sided() {  // actions.hpp:47-56
-      if (n >= 1 && p0 < 1) p0 = 1;
-      if (n >= 2 && p1 < 1) p1 = 1;
-      if (n == 2) {
-        const bool a0 = s0 == MLOB_ASK;  // ask = items[0] if it is an ask, else items[1]
-        const int64_t bp = s0 == MLOB_BID ? p0 : p1;
-        const int64_t ap = a0 ? p0 : p1;
-        if (bp >= ap) {
-          if (a0)
-            p0 = bp + 1;
-          else
-            p1 = bp + 1;
-        }
-      }
-    }
-  };
-
-  __device__ __forceinline__ void decode(int a, int id, Quotes& q) {
-    const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
-    const AgentRec& st = sm.ag()[a];
-    int64_t bb, ba;
-    effective_tops(sp, bb, ba);
-    q.n = 0;
-    if (sp.type == MLOB_EXECUTOR) {  // env.hpp:302-311, actions.hpp:193-224
-      int64_t eb = bb, ea = ba;
-      if (st.task_dir == MLOB_TASK_BUY && live1 == 0) ea = max(static_cast<int64_t>(2), last_ask + 1);
-      if (st.task_dir == MLOB_TASK_SELL && live0 == 0) eb = max(static_cast<int64_t>(1), last_bid - 1);
-      const int pi = id % 4, mi = id / 4;
-      const int64_t spread = ea - eb;
-      int64_t price;
-      if (st.task_dir == MLOB_TASK_BUY)
-        price = pi == 0 ? ea : pi == 1 ? eb : pi == 2 ? eb - 1 : eb + spread / 2;
-      else
-        price = pi == 0 ? eb : pi == 1 ? ea : pi == 2 ? ea + 1 : ea - spread / 2;
-      int64_t qty = sp.order_size * (mi == 0 ? 1 : mi == 1 ? 2 : 5);
-      if (qty > st.task_remaining) qty = st.task_remaining;
-      if (qty > 0) q.push(st.task_dir == MLOB_TASK_BUY ? MLOB_BID : MLOB_ASK, price < 1 ? 1 : price, qty);
-    } else if (sp.type == MLOB_DIRECTIONAL) {  // actions.hpp:227-235
-      if (id == 1) q.push(MLOB_BID, bb < 1 ? 1 : bb, sp.order_size);
-      if (id == 2) q.push(MLOB_ASK, ba < 1 ? 1 : ba, sp.order_size);
-    } else if (sp.mm_space == MLOB_FIXED_QUANT) {  // actions.hpp:66-108
-      const int64_t br = sp.fixed_quant_from_mid ? (bb + ba) / 2 : bb;
-      const int64_t ar = sp.fixed_quant_from_mid ? (bb + ba + 1) / 2 : ba;
-      const int64_t sz = sp.order_size;
-      if (id != 0) {
-        const int64_t pb = id == 1 ? br - 2 : id == 2 ? br - 4 : id == 3 ? bb + 1 : id == 4 ? br - 2
-                         : id == 5 ? bb : id == 6 ? bb - 5 : bb + 1;
-        const int64_t pa = id == 1 ? ar + 2 : id == 2 ? ar + 4 : id == 3 ? ba - 1 : id == 4 ? ba
-                         : id == 5 ? ar + 2 : id == 6 ? ba - 1 : ba + 5;
-        q.push(MLOB_BID, pb, sz);
-        q.push(MLOB_ASK, pa, sz);
-      }
-      q.finish_two_sided();
-    } else if (sp.mm_space == MLOB_SPREAD_SKEW) {  // actions.hpp:128-140
-      const int64_t hs = sp.ss_half[id], sk = sp.ss_skew[id];
-      const int64_t bh = mid_half - 2 * hs + 2 * sk;
-      const int64_t ah = mid_half + 2 * hs + 2 * sk;
-      q.push(MLOB_BID, bh >= 0 ? bh / 2 : (bh - 1) / 2, sp.order_size);
-      q.push(MLOB_ASK, (ah + 1) / 2, sp.order_size);
-      q.finish_two_sided();
-    } else {  // AvSt, actions.hpp:151-178
-      avst(sp.gamma[id], sp.sigma, sp.horizon, sp.avst_term[id], st.inventory, sp.order_size, q);
-    }
-  }
-
-  // decode_avst (actions.hpp:164-178) over avst_quotes (actions.hpp:151-162);
-  // avst_term = (2/gamma) log1p(gamma/kappa), evaluated on the host
-  __device__ __forceinline__ void avst(double gamma, double sigma, double horizon, double avst_term,
-                                       int64_t inventory, int64_t order_size, Quotes& q) const {
-    const double rem = horizon - static_cast<double>(step);
-    const double ttg = 0.0 < rem ? rem : 0.0;
-    const double mid_ticks = static_cast<double>(mid_half) / 2.0;
-    const double reservation = mid_ticks - static_cast<double>(inventory) * gamma * sigma * sigma * ttg;
-    const double half_spread = 0.5 * (gamma * sigma * sigma * ttg + avst_term);
-    q.push(MLOB_BID, static_cast<int64_t>(floor(reservation - half_spread)), order_size);
-    q.push(MLOB_ASK, static_cast<int64_t>(ceil(reservation + half_spread)), order_size);
-    q.finish_two_sided();
-  }
-
-  // Scripted direct actions (evaluate.hpp:63-73): NoOp, twap_policy
-  // (twap.hpp:37-58, plan = make_twap_plan over steps_per_episode, twap.hpp:21-33),
-  // avst_policy (avst.hpp:19-32).
-  __device__ __forceinline__ void scripted(int a, const DevPolicy& pol, Quotes& q) {
-    const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
-    const AgentRec& st = sm.ag()[a];
-    if (pol.kind == MLOB_POLICY_TWAP) {
-      const int64_t S = cfg.steps_per_episode, T = sp.task_size, s = step;
-      const int64_t sched = ((s + 1) * T) / S - (s * T) / S;
-      const int64_t qty = s + 1 == S ? st.task_remaining : min(sched, st.task_remaining);
-      if (qty <= 0) return;
-      int64_t bb, ba;
-      effective_tops(sp, bb, ba);
-      const bool buy = st.task_dir == MLOB_TASK_BUY;
-      const int64_t price = pol.twap_mode == MLOB_TWAP_AGGRESSIVE ? (buy ? ba : bb) : (buy ? bb : ba);
-      q.push(buy ? MLOB_BID : MLOB_ASK, price, qty);
-    } else if (pol.kind == MLOB_POLICY_AVST) {
-      avst(pol.gamma, pol.sigma, pol.horizon, pol.avst_term, st.inventory, sp.order_size, q);
-    }
-  }
-
-  __device__ __forceinline__ void push_amsg(int& n_amsg, int64_t time, uint64_t id, int64_t price,
-                                            int64_t qty, int kind, int side, int trader) {
-    if (lane == 0) {
-      DevMsg m;
-      m.time = time;
-      m.order_id = id;
-      m.price = static_cast<int32_t>(price);
-      m.qty = static_cast<int32_t>(qty);
-      m.kind = static_cast<uint8_t>(kind);
-      m.side = static_cast<uint8_t>(side);
-      m._pad = 0;
-      m.trader = trader;
-      sm.amsg()[n_amsg] = m;
-    }
-    ++n_amsg;
-  }
-
-  // env.hpp:285-370: quotes -> Delete for stale active orders, NewLimit for
-  // quotes not already resting at the same (side, price).
-  Rng bench_rng;  // kActBench: keyed at agent 0, one draw per agent in order
-  __device__ __forceinline__ void convert_action(int a, int64_t step_time, int& n_amsg) {
-    const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
-    AgentRec& st = sm.ag()[a];
-    Quotes q;
-    q.n = 0;
-    q.s0 = q.s1 = 0;
-    q.p0 = q.p1 = q.q0 = q.q1 = 0;
-    const DevPolicy* pol =
-        kp.action_mode == kActScripted ? &kp.policies[kp.env_policy[env * cfg.n_specs + cfg.flat_spec[a]]] : nullptr;
-    const bool direct = pol ? pol->kind != MLOB_POLICY_RANDOM && pol->kind != MLOB_POLICY_LEARNED
-                            : kp.action_mode == kActDirect && kp.action_direct[env * cfg.n_agents + a].direct;
-    if (direct) {  // env.hpp:290-298
-      if (pol) {
-        scripted(a, *pol, q);
-      } else {
-        const mlob_agent_action& da = kp.action_direct[env * cfg.n_agents + a];
-        q.n = da.n_quotes;
-        q.s0 = da.quotes[0].side;
-        q.p0 = da.quotes[0].price;
-        q.q0 = da.quotes[0].quantity;
-        q.s1 = da.quotes[1].side;
-        q.p1 = da.quotes[1].price;
-        q.q1 = da.quotes[1].quantity;
-      }
-      if (sp.type == MLOB_EXECUTOR) {
-        if (q.n >= 1 && q.q0 > st.task_remaining) q.q0 = st.task_remaining;
-        if (q.n >= 2 && q.q1 > st.task_remaining) q.q1 = st.task_remaining;
-        if (q.n == 1 && q.q0 <= 0) q.n = 0;
-      }
-    } else {
-      int id;
-      if (kp.action_mode == kActBench) {  // bench.hpp:57-60: one rng, one draw per agent in order
-        if (a == 0)
-          bench_rng.s = key_fold(key_fold(key_fold(splitmix64(kp.bench_seed), kRngBenchAction), genv),
-                                 kp.global_step);
-        id = static_cast<int>(bench_rng.below(static_cast<uint64_t>(sp.arity)));
-      } else if (pol && pol->kind == MLOB_POLICY_LEARNED) {  // argmax id from the policy kernel
-        id = kp.action_ids[env * cfg.n_agents + a];
-      } else if (pol) {  // PolicyKind::Random, evaluate.hpp:74-79
-        uint64_t h = key_fold(key_fold(splitmix64(seed), kRngEpisodeDraw), kp.env_cell ? kp.env_cell[env] : 0);
-        h = key_fold(key_fold(key_fold(h, episode), static_cast<uint64_t>(step)), static_cast<uint64_t>(a));
-        Rng r{h};
-        id = static_cast<int>(r.below(static_cast<uint64_t>(sp.arity)));
-      } else if (kp.action_mode == kActDirect) {
-        id = kp.action_direct[env * cfg.n_agents + a].id;
-      } else {
-        id = kp.action_ids[env * cfg.n_agents + a];
-      }
-      if (id < 0 || id >= sp.arity) {
-        err |= kErrBadAction;
-        id = 0;
-      }
-      decode(a, id, q);
-    }
-    bool kept0 = false, kept1 = false;
-    const int na = st.n_active;
-    for (int i = 0; i < na; ++i) {
-      const ActiveRec ar = sm.act()[a * kMaxActive + i];
-      const int side = static_cast<int>(ar.qty_side >> 31);
-      const bool r0 = q.n >= 1 && q.s0 == side && q.p0 == ar.price;
-      const bool r1 = q.n >= 2 && q.s1 == side && q.p1 == ar.price;
-      kept0 |= r0;
-      kept1 |= r1;
-      if (r0 || r1) continue;
-      push_amsg(n_amsg, step_time, ar.order_id, 0, 0, MLOB_DELETE, side, a + 1);
-    }
-    uint64_t nonce = st.nonce;
-    const uint64_t id_base = cfg.agent_id_base + static_cast<uint64_t>(a) * cfg.agent_id_range;
-    for (int j = 0; j < q.n; ++j) {
-      if (j == 0 ? kept0 : kept1) continue;
-      const int64_t pr = j == 0 ? q.p0 : q.p1, qt = j == 0 ? q.q0 : q.q1;
-      if (pr > INT_MAX - 1 || pr < INT_MIN + 1 || qt > INT_MAX || qt < INT_MIN) err |= kErrPriceRange;
-      push_amsg(n_amsg, step_time, id_base + nonce, pr, qt, MLOB_NEW_LIMIT, j == 0 ? q.s0 : q.s1, a + 1);
-      ++nonce;
-    }
-    __syncwarp();
-    if (lane == 0) st.nonce = nonce;
-  }
-
   // ---- step outcomes -------------------------------------------------------
   // Top-D aggregated levels per side, best-first (book.hpp:109-120, 209-220).
   template <int S>
@@ -1641,14 +1352,14 @@ struct WarpEnv {
   __device__ __forceinline__ void rebuild_active() {
     const int A = cfg.n_agents;
     ActTmp* tmp = reinterpret_cast<ActTmp*>(sm.amsg());  // agent messages are consumed
-    const int cap = 4 * A + 4;                          // DevMsg slots = ActTmp slots
+    const int cap = static_cast<int>(kp.amsg_cap);      // DevMsg slots = ActTmp slots
     int base = 0;
     base = compact_side<0>(tmp, base, cap);
     const int nbid = base;
     base = compact_side<1>(tmp, base, cap);
     __syncwarp();
     if (lane == 0) {
-      for (int a = 0; a < A; ++a) sm.ag()[a].n_active = 0;
+      for (int a = 0; a < A; ++a) sm.nact()[a] = 0;
       const int total = base < cap ? base : cap;
       if (base > cap) err |= kErrActiveOverflow;
       // insertion sort each side into storage order: bids (price asc, seq desc),
@@ -1675,7 +1386,7 @@ struct WarpEnv {
           err |= kErrBadTrader;
           continue;
         }
-        const int n = sm.ag()[a].n_active;
+        const int n = sm.nact()[a];
         if (n >= kMaxActive) {
           err |= kErrActiveOverflow;
           continue;
@@ -1683,10 +1394,14 @@ struct WarpEnv {
         sm.act()[a * kMaxActive + n] =
             ActiveRec{(static_cast<uint64_t>(x.hi) << 32) | x.lo, x.price,
                       static_cast<uint32_t>(x.qty) | (static_cast<uint32_t>(i >= nbid) << 31)};
-        sm.ag()[a].n_active = n + 1;
+        sm.nact()[a] = n + 1;
       }
     }
     __syncwarp();
+    // hand-off to the outcome kernel and the next step's act_kernel
+    for (int a = lane; a < A; a += kWarp) kp.agents[env * A + a].n_active = sm.nact()[a];
+    for (int i = lane; i < A * kMaxActive; i += kWarp)
+      if (i % kMaxActive < sm.nact()[i / kMaxActive]) kp.active[env * A * kMaxActive + i] = sm.act()[i];
   }
   template <int S>
   __device__ __forceinline__ int compact_side(ActTmp* tmp, int base, int cap) {
@@ -1722,179 +1437,28 @@ struct WarpEnv {
     return base;
   }
 
-  // env.hpp:435-443
-  __device__ __forceinline__ double reference_price(const DevSpec& sp, const AgentRec& st) const {
-    if (sp.ref_price == MLOB_REF_MID || st.inventory == 0) return static_cast<double>(mid_half) / 2.0;
-    if (st.inventory > 0) return static_cast<double>(live0 > 0 ? static_cast<int64_t>(best0) : last_bid);
-    return static_cast<double>(live1 > 0 ? static_cast<int64_t>(best1) : last_ask);
-  }
-
-  // env.hpp:445-464 (also accumulates slippage_total); lane 0 writes.
-  __device__ __forceinline__ void fill_info(int a) {
-    const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
-    AgentRec& st = sm.ag()[a];
-    const StepAcc& ac = sm.acc()[a];
-    mlob_agent_info info;
-    info.inventory = st.inventory;
-    info.cash = st.cash;
-    info.portfolio_value =
-        static_cast<double>(st.inventory) * reference_price(sp, st) + static_cast<double>(st.cash);
-    info.slippage_step = sp.type == MLOB_EXECUTOR ? ac.slip : 0.0;
-    const double total = st.slippage_total + info.slippage_step;
-    info.slippage_total = total;
-    info.task_remaining = st.task_remaining;
-    info.step_filled = ac.filled;
-    info.step_fill_count = ac.count;
-    info._pad = 0;
-    __syncwarp();
-    if (lane == 0) {
-      st.slippage_total = total;
-      kp.infos[env * cfg.n_agents + a] = info;
-    }
-    __syncwarp();
-  }
-
-  // env.hpp:409-433 + rewards.hpp
-  __device__ __forceinline__ double compute_reward(int a) {
-    const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
-    const AgentRec& st = sm.ag()[a];
-    const StepAcc& ac = sm.acc()[a];
-    double r = 0.0;
-    if (sp.reward == MLOB_REWARD_EXEC) {
-      r = -ac.slip;
-      if (terminal && st.task_remaining > 0)
-        r -= sp.unfilled_penalty_coef * static_cast<double>(st.task_remaining) * st.p_init;
-    } else {
-      double pb = 0.0, ps = 0.0;
-      const int nf = sm.scal()[0];
-      if (!sm.scal()[1]) {
-        // one pass: each side's sum still accumulates in fill order
-        for (int i = 0; i < nf; ++i) {
-          const FillEnt f = sm.fills()[i];
-          if (f.agent != a) continue;
-          if (f.side == MLOB_BID)
-            pb += (mbar - static_cast<double>(f.price)) * static_cast<double>(f.qty);
-          else
-            ps += (static_cast<double>(f.price) - mbar) * static_cast<double>(f.qty);
-        }
-      } else {
-        // exact-rational fallback beyond kFillLog fills in one env-step
-        pb = mbar * static_cast<double>(ac.sq[0]) - static_cast<double>(ac.spq[0]);
-        ps = static_cast<double>(ac.spq[1]) - mbar * static_cast<double>(ac.sq[1]);
-      }
-      if (sp.reward == MLOB_REWARD_BUYSELL) {
-        r = pb + ps;
-      } else {
-        const double mid = static_cast<double>(mid_half) / 2.0;
-        const double prev = static_cast<double>(prev_mid_half) / 2.0;
-        const double psi_inv = static_cast<double>(st.inventory) * (mid - prev);
-        r = pb + ps + psi_inv - (1.0 - sp.lambda) * (0.0 < psi_inv ? psi_inv : 0.0);
-      }
-      if (sp.quadratic_penalty) {
-        const double frac = static_cast<double>(st.inventory) / static_cast<double>(sp.inventory_cap);
-        r -= sp.rho * frac * frac;
-      }
-    }
-    return r * sp.reward_scale;
-  }
-
-  __device__ static double fmin_ref(double a, double x) { return x < a ? x : a; }  // std::min(a, x)
-  __device__ static double qty_feature(int64_t q, int64_t order_size) {
-    return static_cast<double>(q) / static_cast<double>(q + (order_size > 1 ? order_size : 1));
-  }
-  __device__ static double offset_feature(int64_t own, int64_t touch, bool bid_side) {
-    if (own < 0 || touch < 0) return -1.0;
-    const double off = static_cast<double>(bid_side ? touch - own : own - touch);
-    const double lo = -16.0 < off ? off : -16.0;
-    return lo < 16.0 ? lo : 16.0;
-  }
-
-  // env.hpp:466-503, observations.hpp:42-148; features staged in smem by lane
-  // 0 then written by lanes (coalesced).
-  __device__ __forceinline__ void build_observation(int a, const L2Lvl* l2b, int nb, const L2Lvl* l2a, int na) {
-    const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
-    const AgentRec& st = sm.ag()[a];
-    const int dim = sp.obs_dim;
-    if (lane == 0) {
-      const int64_t bb = live0 > 0 ? best0 : -1;
-      const int64_t ba = live1 > 0 ? best1 : -1;
-      const double time_frac = static_cast<double>(step) / static_cast<double>(cfg.steps_per_episode);
-      const int64_t bq = sumq0, aq = sumq1;
-      const double imb = bq + aq == 0 ? 0.0 : static_cast<double>(bq - aq) / static_cast<double>(bq + aq);
-      const double spread = (bb < 0 || ba < 0) ? 0.0 : fmin_ref(32.0, static_cast<double>(ba - bb));
-      int64_t own_bid = -1, own_ask = -1;
-      for (int i = 0; i < st.n_active; ++i) {
-        const ActiveRec ar = sm.act()[a * kMaxActive + i];
-        if ((ar.qty_side >> 31) == 0)
-          own_bid = own_bid < 0 ? ar.price : max(own_bid, static_cast<int64_t>(ar.price));
-        else
-          own_ask = own_ask < 0 ? ar.price : min(own_ask, static_cast<int64_t>(ar.price));
-      }
-      const double dmid = static_cast<double>(mid_half - prev_mid_half) / 2.0;
-      double* out = sm.obs();
-      if (sp.type == MLOB_EXECUTOR) {
-        const int dir = st.task_dir == MLOB_TASK_BUY ? 1 : -1;
-        out[0] = static_cast<double>(st.task_remaining) /
-                 static_cast<double>(sp.task_size > 1 ? sp.task_size : 1);
-        out[1] = time_frac;
-        out[2] = static_cast<double>(dir);
-        out[3] = spread;
-        out[4] = dmid;
-        out[5] = static_cast<double>(mid_half) / 2.0 - st.p_init;
-        out[6] = imb;
-        out[7] = nb > 0 ? qty_feature(topq0, sp.order_size) : 0.0;
-        out[8] = na > 0 ? qty_feature(topq1, sp.order_size) : 0.0;
-        const bool buy = dir > 0;
-        out[9] = offset_feature(buy ? own_bid : own_ask, buy ? bb : ba, buy);
-        for (int j = 10; j < dim; ++j) out[j] = 0.0;  // MMFull-sized executor obs
-      } else {
-        const int64_t cs = sp.inventory_cap * static_cast<int64_t>(st.p_init);
-        out[0] = static_cast<double>(st.inventory) / static_cast<double>(sp.inventory_cap);
-        out[1] = static_cast<double>(st.cash) / static_cast<double>(cs > 1 ? cs : 1);
-        out[2] = spread;
-        out[3] = dmid;
-        out[4] = imb;
-        out[5] = time_frac;
-        out[6] = offset_feature(own_bid, bb, true);
-        out[7] = offset_feature(own_ask, ba, false);
-        if (sp.obs_space == MLOB_OBS_MM_FULL) {
-          int k = 8;
-          const int levels = (dim - 8) / 4;
-          for (int d = 0; d < levels; ++d) {
-            const bool hb = d < nb, ha = d < na;
-            out[k++] = hb ? fmin_ref(32.0, static_cast<double>(bb - l2b[d].price)) : -1.0;
-            out[k++] = hb ? qty_feature(l2b[d].qty, sp.order_size) : 0.0;
-            out[k++] = ha ? fmin_ref(32.0, static_cast<double>(l2a[d].price - ba)) : -1.0;
-            out[k++] = ha ? qty_feature(l2a[d].qty, sp.order_size) : 0.0;
-          }
-        } else if (sp.obs_space == MLOB_OBS_EXEC) {
-          out[8] = 0.0;  // the reference leaves these two zero-initialised
-          out[9] = 0.0;
-        }
-      }
-    }
-    __syncwarp();
-    const int t = cfg.flat_spec[a];
-    const int kk = a - cfg.specs[t].flat_offset;
-    double* dst = kp.obs[t] + (env * static_cast<uint64_t>(cfg.specs[t].count) + kk) * dim;
-    for (int j = lane; j < dim; j += kWarp) dst[j] = sm.obs()[j];
-    __syncwarp();
-  }
-
   // Book-dependent part of the step outcomes: L2 top-D into smem.  After this
   // (and rebuild_active) the book registers can be stored and released, so no
   // book register is live across the double-division / 64-bit-modulo
   // subroutine calls of the reward/observation code (they forced the book
   // through local memory in v1).
   __device__ __forceinline__ void snapshot() {
-    if (!cfg.full_l2 && summarize_l2<0>() && summarize_l2<1>()) return;
-    nb_l2 = l2_levels<0>(sm.l2());
-    na_l2 = l2_levels<1>(sm.l2() + cfg.obs_depth);
-    sumq0 = sumq1 = topq0 = topq1 = 0;
-    for (int i = 0; i < nb_l2; ++i) sumq0 += sm.l2()[i].qty;
-    for (int i = 0; i < na_l2; ++i) sumq1 += sm.l2()[cfg.obs_depth + i].qty;
-    topq0 = nb_l2 > 0 ? sm.l2()[0].qty : 0;
-    topq1 = na_l2 > 0 ? sm.l2()[cfg.obs_depth].qty : 0;
+    if (cfg.full_l2 || !summarize_l2<0>() || !summarize_l2<1>()) {
+      nb_l2 = l2_levels<0>(sm.l2());
+      na_l2 = l2_levels<1>(sm.l2() + cfg.obs_depth);
+      sumq0 = sumq1 = topq0 = topq1 = 0;
+      for (int i = 0; i < nb_l2; ++i) sumq0 += sm.l2()[i].qty;
+      for (int i = 0; i < na_l2; ++i) sumq1 += sm.l2()[cfg.obs_depth + i].qty;
+      topq0 = nb_l2 > 0 ? sm.l2()[0].qty : 0;
+      topq1 = na_l2 > 0 ? sm.l2()[cfg.obs_depth].qty : 0;
+      if (cfg.full_l2) {  // the levels themselves, for MMFull observations
+        const int D = cfg.obs_depth;
+        L2Lvl* dst = kp.l2lv + env * 2 * D;
+        for (int i = lane; i < 2 * D; i += kWarp)
+          if ((i < D ? i < nb_l2 : i - D < na_l2)) dst[i] = sm.l2()[i];
+      }
+    }
+    if (lane == 0) kp.l2sum[env] = L2Sum{nb_l2, na_l2, sumq0, sumq1, topq0, topq1, 0};
   }
 
   // Warp-sum of a per-lane value < 2^36 (16-bit split keeps redux.sync exact).
@@ -1951,123 +1515,6 @@ struct WarpEnv {
     return true;
   }
 
-  __device__ __forceinline__ void outcomes(bool write_rewards) {
-    const L2Lvl* l2b = sm.l2();
-    const L2Lvl* l2a = sm.l2() + cfg.obs_depth;
-    const int nb = nb_l2, na = na_l2;
-    for (int a = 0; a < cfg.n_agents; ++a) {
-      if (write_rewards) {
-        const double r = compute_reward(a);
-        if (lane == 0) {
-          kp.rewards[env * cfg.n_agents + a] = r;
-          kp.dones[env * cfg.n_agents + a] = terminal ? 1 : 0;
-        }
-      }
-      fill_info(a);
-      build_observation(a, l2b, nb, l2a, na);
-    }
-  }
-
-  __device__ __forceinline__ void clear_step_acc() {
-    const int A = cfg.n_agents;
-    for (int i = lane; i < A; i += kWarp) sm.acc()[i] = StepAcc{0.0, 0, {0, 0}, {0, 0}, 0, 0};
-    if (lane == 0) {
-      sm.scal()[0] = 0;
-      sm.scal()[1] = 0;
-    }
-    __syncwarp();
-  }
-
-  // ---- reset (env.hpp:143-192, book.hpp:41-60) ---------------------------
-  __device__ __forceinline__ bool reset(uint64_t ep, bool write_rewards) {
-    const EpState es = kp.ep_state[ep];
-    if (!es.valid) {
-      err |= kErrMissingState;
-      return false;
-    }
-    if (static_cast<int>(es.nb) > cfg.capacity || static_cast<int>(es.na) > cfg.capacity) {
-      err |= kErrTooDeep;
-      return false;
-    }
-    episode = ep;
-    const DevLevel* lv = kp.levels + es.level_offset;
-    init_side<0>(lv, es.nb, cfg.synth_id_base, 0);
-    init_side<1>(lv + es.nb, es.na, cfg.synth_id_base + es.nb, es.nb);
-    next_seq = es.nb + es.na;
-    live0 = static_cast<int>(es.nb);
-    live1 = static_cast<int>(es.na);
-    best0 = es.nb ? lv[0].price : 0;
-    best1 = es.na ? lv[es.nb].price : 0;
-    {
-      const bool hb = live0 > 0, ha = live1 > 0;
-      const int64_t b0 = best0, b1 = best1;
-      mid_half = hb ? (ha ? b0 + b1 : 2 * b0) : (ha ? 2 * b1 : cfg.fallback_mid_half);
-    }
-    prev_mid_half = mid_half;
-    mbar = static_cast<double>(mid_half) / 2.0;
-    last_bid = live0 > 0 ? static_cast<int64_t>(best0) : mid_half / 2 - 1;
-    last_ask = live1 > 0 ? static_cast<int64_t>(best1) : (mid_half + 1) / 2 + 1;
-    step = 0;
-    terminal = false;
-    n_trades = 0;
-    const int A = cfg.n_agents;
-    for (int a = 0; a < A; ++a) {
-      const DevSpec& sp = cfg.specs[cfg.flat_spec[a]];
-      AgentRec st;
-      st.inventory = 0;
-      st.cash = 0;
-      st.filled_total = 0;
-      st.slippage_total = 0.0;
-      st.nonce = 0;
-      st.n_active = 0;
-      st.p_init = static_cast<double>(mid_half) / 2.0;
-      st.task_dir = sm.ag()[a].task_dir;
-      if (sp.type == MLOB_EXECUTOR) {
-        uint64_t h = splitmix64(seed);
-        h = key_fold(h, genv);
-        h = key_fold(h, ep);
-        h = key_fold(h, 0);
-        h = key_fold(h, kRngTaskDir);
-        h = key_fold(h, static_cast<uint64_t>(a));
-        Rng r{h};
-        st.task_dir = r.coin() ? MLOB_TASK_BUY : MLOB_TASK_SELL;
-        st.task_remaining = sp.task_size;
-      } else {
-        st.task_remaining = 0;
-      }
-      __syncwarp();
-      if (lane == 0) sm.ag()[a] = st;
-    }
-    __syncwarp();
-    clear_step_acc();
-    for (int a = 0; a < A && write_rewards; ++a)
-      if (lane == 0) {
-        kp.rewards[env * A + a] = 0.0;
-        kp.dones[env * A + a] = 0;
-      }
-    return true;  // caller: snapshot(), store_book(), outcomes(false)
-  }
-
-  template <int S>
-  __device__ __forceinline__ void init_side(const DevLevel* lv, uint32_t n, uint64_t id_base, uint32_t seq_base) {
-    SideT& d = sd<S>();
-    MLOB_ROWS(k) {
-      const uint32_t i = static_cast<uint32_t>(k * kWarp + lane);
-      if (i < n) {
-        const uint64_t id = id_base + i;
-        d.put(k, lv[i].price, lv[i].qty, static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32),
-              (seq_base + i) << 8);
-      } else {
-        d.put(k, empty_price<S>(), 0, 0, 0, kEmptySt);
-      }
-    }
-    if constexpr (SMEM) d.recompute_occ();  // occupancy + cached worst of the new book
-  }
-
-  __device__ __forceinline__ uint64_t episode_for(uint64_t k) const {  // rollout.hpp:286-288
-    const uint64_t i = (genv + k * kp.n_envs_global) % kp.pool_len;
-    return kp.pool ? kp.pool[i] : i;
-  }
 };
 
 }  // namespace mlob

@@ -112,6 +112,7 @@ _SIGS = {
     "mlob_venv_env_obs": (C.c_int, [_vp, C.c_uint64, _P(C.c_double), C.c_uint64]),
     "mlob_venv_episode_stats": (C.c_int, [_vp, C.c_int, _P(EpisodeStats)]),
     "mlob_venv_episode_stats_device": (C.c_int, [_vp, _vp]),
+    "mlob_venv_allreduce_episode_stats": (C.c_int, [_vp, _vp, _vp]),
     "mlob_venv_clear_episode_stats": (C.c_int, [_vp]),
     "mlob_venv_read_scalars": (C.c_int, [_vp, C.c_uint64, _P(EnvScalars)]),
     "mlob_venv_read_book": (C.c_int, [_vp, C.c_uint64, C.c_int, _P(RestingOrder), C.c_uint64,
@@ -529,8 +530,16 @@ class _Venv:
         return s
 
     def episode_stats_device(self, out_ptr: int) -> None:
-        """K4: per-type sums into a device buffer of 5*n_types doubles."""
+        """K4: per-type sums into a device buffer of STAT_WORDS*n_types doubles
+        (pv, slippage, completion, inventory², episodes, Σ remaining)."""
         _check(lib().mlob_venv_episode_stats_device(self.h, _vp(out_ptr)))
+
+    def allreduce_episode_stats(self, nccl_comm: int = 0) -> list:
+        """K4 + ncclAllReduce over `nccl_comm` (an ncclComm_t; 0 = this handle
+        alone) -> per-type EpisodeStats with the exact completion sum."""
+        out = (EpisodeStats * self.n_types())()
+        _check(lib().mlob_venv_allreduce_episode_stats(self.h, _vp(nccl_comm), out))
+        return list(out)
 
     def clear_episode_stats(self) -> None:
         _check(lib().mlob_venv_clear_episode_stats(self.h))

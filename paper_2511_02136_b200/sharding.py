@@ -38,14 +38,28 @@ def sharded_vec_env(store, cfg, n_total: int, rank: int, world: int, seed: int =
 
 def reduce_episode_stats(venv, group=None):
     """K4 per-type sums on this GPU, all-reduced (sum) over the process group:
-    returns a float64 CUDA tensor [n_types, 5] = (pv, slippage, completion,
-    inventory², episodes)."""
+    returns a float64 CUDA tensor [n_types, STAT_WORDS] = (pv, slippage,
+    completion, inventory², episodes, Σ remaining).  Only the completion
+    column depends on the summation order; exact_completion() rebuilds it
+    from the exact columns."""
     import torch
     import torch.distributed as dist
+    from .abi import STAT_WORDS
     n_types = venv.n_types()
-    out = torch.zeros(5 * n_types, dtype=torch.float64, device="cuda")
+    out = torch.zeros(STAT_WORDS * n_types, dtype=torch.float64, device="cuda")
     venv.episode_stats_device(out.data_ptr())
     venv.synchronize()
     if dist.is_available() and dist.is_initialized():
-        dist.all_reduce(out, group=group)
-    return out.view(n_types, 5)
+        x = out if dist.get_backend(group) == "nccl" else out.cpu()
+        dist.all_reduce(x, group=group)
+        out.copy_(x)
+    return out.view(n_types, STAT_WORDS)
+
+
+def exact_completion(row, spec) -> float:
+    """completion_sum of one type from its exact K4 columns:
+    Σ_episodes (1 − remaining / task_size) = episodes·count − Σremaining / task_size."""
+    from .abi import EXECUTOR
+    if spec.type != EXECUTOR:
+        return 0.0
+    return float(row[4]) * spec.count - float(row[5]) / float(spec.params.task_size)

@@ -11,6 +11,7 @@ import pytest
 
 from oracle.oracle import OEnv, OVecEnv, Oracle, bench_run
 from paper_2511_02136_b200 import abi
+from paper_2511_02136_b200.sharding import exact_completion
 from paper_2511_02136_b200.env import (DeviceStore, HostStore, LogicError, MarketEnvBatch,
                                        MarketVecEnv)
 from tests import kat
@@ -123,15 +124,21 @@ def test_vec_env_auto_reset_and_episode_stats(orc):
         a, b = g.episode_stats(ty), o.episode_stats(ty)
         assert bytes(a) == bytes(b)
     import torch
-    out = torch.zeros(5 * cfg.n_specs, dtype=torch.float64, device="cuda")
+    W = abi.STAT_WORDS
+    out = torch.zeros(W * cfg.n_specs, dtype=torch.float64, device="cuda")
     g.episode_stats_device(out.data_ptr())
     g.synchronize()
+    red = g.allreduce_episode_stats(0)  # K4 + the host-side exact completion, no communicator
     for ty in range(cfg.n_specs):
         s = o.episode_stats(ty)
-        d = out[5 * ty: 5 * ty + 5].cpu().numpy()
+        d = out[W * ty: W * ty + W].cpu().numpy()
         assert d[0] == s.pv_sum and d[1] == s.slippage_sum and d[3] == s.inventory_sq_sum
         assert abs(d[2] - s.completion_sum) <= 1e-12 * max(1.0, abs(s.completion_sum))
         assert d[4] == s.episodes
+        assert exact_completion(d, cfg.specs[ty]) == red[ty].completion_sum
+        assert abs(red[ty].completion_sum - s.completion_sum) <= 1e-12 * max(1.0, abs(s.completion_sum))
+        assert (red[ty].pv_sum, red[ty].slippage_sum, red[ty].inventory_sq_sum, red[ty].episodes) == \
+            (s.pv_sum, s.slippage_sum, s.inventory_sq_sum, s.episodes)
     g.clear_episode_stats()
     assert g.episode_stats(0).episodes == 0
 
