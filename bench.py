@@ -106,7 +106,7 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_reference_run(n_envs_cap: int, steps: int, warmup: int, name: str):
+def cpu_reference_run(n_envs_cap: int, steps: int, warmup: int, name: str, workers: int = 0):
     """bench::run_throughput (bench.hpp:98-160) of the compiled reference
     (oracle/_ref) on this host's cores, same workload, bounded env count."""
     from oracle.oracle import Oracle, available, bench_run
@@ -125,7 +125,7 @@ def cpu_reference_run(n_envs_cap: int, steps: int, warmup: int, name: str):
     else:
         small = abi.synth_config(n_messages=(n + 64) * 100, state_sample_every=100)
         store = o.synth(small, 0)   # the same stream's prefix: identical episodes 0..n
-    workers = os.cpu_count() or 1
+    workers = workers or os.cpu_count() or 1
     row = bench_run(o, store, cfg, n, steps, warmup, workers, 0, 100, 1)
     return row, workers, n, label
 
@@ -151,13 +151,210 @@ def reference_arm(args) -> None:
     print(json.dumps(out), flush=True)
 
 
-def gpu_arm(args) -> None:
+def load_profile(name: str) -> dict:
+    """The committed ncu capture of this workload's book_kernel
+    (profiles/ncu_summary.json, one entry per workload), or {}."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f).get("workloads", {}).get(name, {})
+    except Exception:
+        return {}
+
+
+def host_store(name, synth, world, local, barrier):
+    """The workload's synthetic store, generated once per node: local rank 0
+    synthesises and saves it, the other ranks of the node load the file."""
+    from paper_2511_02136_b200.env import HostStore
+    t0 = time.time()
+    if world == 1:
+        hs = HostStore.synth(synth, 0)
+    else:
+        import torch
+        import torch.distributed as dist
+        # the file name carries local rank 0's pid (shared by a max all-reduce)
+        pid = torch.tensor([os.getpid() if local == 0 else 0], dtype=torch.int64)
+        dist.all_reduce(pid, op=dist.ReduceOp.MAX, group=barrier)
+        path = f"/tmp/mlob_store_{name}_{synth.n_messages}_{int(pid.item())}.bin"
+        if local == 0:
+            hs = HostStore.synth(synth, 0)
+            hs.save(path)
+        dist.barrier(group=barrier)
+        if local != 0:
+            hs = HostStore.load(path)
+        dist.barrier(group=barrier)
+        if local == 0:
+            os.unlink(path)
+    if name == "D":
+        hs.trim_front(16 * 6400)  # every remaining episode starts with a full 1000-level book
+    return hs, time.time() - t0
+
+
+# Algorithmic bytes per message of the book kernel alone: B_MSG less the
+# agent state / action / observation / reward terms that act_kernel and
+# outcome_kernel move (SURVEY §8(d): Σ_agents 128 + 4 + 4·obs_dim + 5 per
+# env-step; DESIGN.md "Roofline").
+B_BOOK = {"B": (17275 - 177) / 100.78, "C": (17488 - 346) / 103.41, "D": (148492 - 346) / 103.77,
+          "E": (17488 - 346) / 103.41}
+ISSUE_PEAK = 148 * 4 * 1.965e9  # warp instructions / s at 100 % issue, 1,965 MHz
+
+
+def measure(name, args, world, rank, local, dev, allreduce, barrier, cpu_group, with_e2e=True):
+    """One workload: device-timed value with per-kernel events, roofline, e2e."""
     import numpy as np
     import torch
-    import torch.distributed as dist
 
     from paper_2511_02136_b200 import abi
-    from paper_2511_02136_b200.env import DeviceStore, HostStore, MarketVecEnv
+    from paper_2511_02136_b200.env import DeviceStore, MarketVecEnv
+
+    n_total, cfg, synth, label = workload(name)
+    if args.mps:
+        cfg.messages_per_step = args.mps
+        synth.n_messages = (n_total + 64) * args.mps
+        synth.state_sample_every = args.mps
+    if args.envs and name == args.workload:
+        n_total = args.envs
+        synth.n_messages = (n_total + 64) * cfg.messages_per_step
+    per = n_total // world
+    base = rank * per
+    n_local = per if rank < world - 1 else n_total - base
+    hs, gen_s = host_store(name, synth, world, local, cpu_group)
+    store = DeviceStore(hs, dev)
+    del hs
+    venv = MarketVecEnv(store, cfg, seed=0, n_envs=n_local, n_envs_global=n_total,
+                        env_index_base=base, device=dev)
+    venv.reset_all()
+    stream = torch.cuda.ExternalStream(venv.stream, device=torch.device("cuda", dev))
+    # working set against the L2: book slots + replay store + per-env state
+    props = torch.cuda.get_device_properties(dev)
+    l2 = int(getattr(props, "L2_cache_size", 126 * 2 ** 20))
+    spl = max(1, -(-int(cfg.book_capacity) // 32))
+    spl = 1 << (spl - 1).bit_length()
+    work = n_local * 2 * spl * 32 * 20 + store.n_messages * 32 + n_local * 1024
+    flush = work < 4 * l2  # small workloads: flush the L2 between timed steps
+    scrub = torch.empty(2 * l2 // 4 + 1, dtype=torch.int32, device=f"cuda:{dev}") if flush else None
+
+    gstep = 0
+    for _ in range(args.warmup):
+        venv.step_random(0, gstep)
+        gstep += 1
+    venv.synchronize()
+    m0 = venv.messages_processed()
+    l0 = venv.launches
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps if flush else 2)]
+    barrier()
+    venv.profile(True)
+    with ClockSampler(dev) as clocks:
+        if flush:
+            for i in range(args.steps):
+                with torch.cuda.stream(stream):
+                    scrub.fill_(i)
+                evs[2 * i].record(stream)
+                venv.step_random(0, gstep)
+                evs[2 * i + 1].record(stream)
+                gstep += 1
+        else:
+            evs[0].record(stream)
+            for _ in range(args.steps):
+                venv.step_random(0, gstep)
+                gstep += 1
+            evs[1].record(stream)
+        evs[-1].synchronize()
+    kms, ksteps = venv.kernel_ms()
+    venv.profile(False)
+    launches = venv.launches - l0
+    venv.synchronize()
+    ms = sum(evs[2 * i].elapsed_time(evs[2 * i + 1]) for i in range(len(evs) // 2))
+    msgs = venv.messages_processed() - m0
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    m = torch.tensor([msgs], dtype=torch.float64, device="cuda")
+    kb = torch.tensor([kms[1]], dtype=torch.float64, device="cuda")
+    allreduce(t, "max")
+    allreduce(m)
+    allreduce(kb, "max")
+    ms_max, msgs_all = float(t.item()), float(m.item())
+    value = msgs_all / (ms_max / 1e3)
+    env_steps = n_total * args.steps / (ms_max / 1e3)
+
+    # K4 + the all-reduce: episode statistics across ranks (the only collective)
+    stats = torch.zeros(abi.STAT_WORDS * cfg.n_specs, dtype=torch.float64, device="cuda")
+    venv.episode_stats_device(stats.data_ptr())
+    venv.synchronize()
+    allreduce(stats)
+
+    out = {"value": value, "ms_per_step": ms_max / args.steps, "env_steps_per_s": env_steps,
+           "launches": launches, "clocks": clocks.summary(),
+           "episodes": float(stats[4].item()), "label": label, "n_total": n_total, "n_local": n_local,
+           "cfg": cfg, "gen_s": gen_s, "flush": flush, "work": work, "l2": l2}
+    # roofline of the dominant kernel (book_kernel): its algorithmic bytes per
+    # launch over its own event-timed duration on the launching stream
+    book_s = float(kb.item()) / 1e3 / max(1, ksteps)
+    step_s = ms_max / 1e3 / args.steps
+    per_launch_msgs = msgs_all / args.steps
+    peak, peak_kind = peaks()
+    prof = load_profile(name)
+    bb = B_BOOK.get(name, 165.8)
+    achieved = bb * (msgs / args.steps) / book_s / 1e9 if book_s > 0 else None
+    inst = prof.get("inst_per_msg")
+    out["roofline"] = {
+        "bound": "hbm", "kernel": f"book_kernel<{spl}>", "achieved": achieved, "peak": peak,
+        "unit": "GB/s", "frac": achieved / peak if achieved else None,
+        "traffic": prof["dram_bytes_per_msg"] * (msgs / args.steps) if "dram_bytes_per_msg" in prof else None,
+        "bytes_per_msg": round(bb, 1), "peak_kind": peak_kind,
+        "kernel_share_of_step": (kms[1] / sum(kms)) if sum(kms) > 0 else None,
+        "kernel_ms": [round(x / max(1, ksteps), 4) for x in kms],
+        "step": {"bytes_per_msg": B_MSG.get(name, 169.1),
+                 "achieved": B_MSG.get(name, 169.1) * per_launch_msgs / step_s / world / 1e9,
+                 "frac": B_MSG.get(name, 169.1) * per_launch_msgs / step_s / world / 1e9 / peak},
+        # issue-rate bound: book_kernel warp instructions per message (ncu) x rate
+        "issue": ({"inst_per_msg": inst, "achieved": inst * (msgs / args.steps) / book_s,
+                   "peak": ISSUE_PEAK, "unit": "warp-inst/s",
+                   "frac": inst * (msgs / args.steps) / book_s / ISSUE_PEAK}
+                  if inst and book_s > 0 else None),
+        "ncu_capture": prof.get("capture")}
+
+    if with_e2e:
+        # e2e through the public API with host buffers, every step: pinned actions
+        # H2D, step, rewards + dones + per-type observations and reset flags D2H
+        # (mlob_venv_step_io: one call; the copies overlap the chunked step)
+        A = venv.n_agents
+        rng = np.random.default_rng(1234)
+        ar = np.array([abi.action_arity(cfg.specs[s]) for s in abi.flat_specs(cfg)])
+        e_steps = max(3, min(args.steps, args.e2e_steps))
+        acts_all = [torch.from_numpy((rng.integers(0, 1 << 30, size=(n_local, A)) % ar).astype(np.int32))
+                    .pin_memory() for _ in range(e_steps + 1)]
+        obs_bufs = [torch.empty((venv.n_streams(t), venv.obs_dim(t)), dtype=torch.float64).pin_memory()
+                    for t in range(cfg.n_specs)]
+        rew = torch.empty((n_local, A), dtype=torch.float64).pin_memory()
+        dn = torch.empty((n_local, A), dtype=torch.uint8).pin_memory()
+        rsb = [torch.empty(venv.n_streams(t), dtype=torch.uint8).pin_memory() for t in range(cfg.n_specs)]
+
+        def e2e_step(a):
+            venv.step_io(actions=a, rewards=rew, dones=dn, obs=obs_bufs, resets=rsb)
+
+        e2e_step(acts_all[e_steps])  # warm-up (creates the copy streams)
+        em0 = venv.messages_processed()
+        barrier()
+        w0 = time.perf_counter()
+        for i in range(e_steps):
+            e2e_step(acts_all[i])
+        torch.cuda.synchronize()
+        e_wall = torch.tensor([time.perf_counter() - w0], dtype=torch.float64, device="cuda")
+        allreduce(e_wall, "max")
+        e_m = torch.tensor([venv.messages_processed() - em0], dtype=torch.float64, device="cuda")
+        allreduce(e_m)
+        h2d = acts_all[0].numel() * 4
+        d2h = rew.numel() * 8 + dn.numel() + sum(b.numel() * 8 for b in obs_bufs) + \
+            sum(b.numel() for b in rsb)
+        out["e2e"] = {"value": float(e_m.item()) / float(e_wall.item()), "unit": UNIT,
+                      "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e_steps}
+    del venv, store
+    torch.cuda.empty_cache()
+    return out
+
+
+def gpu_arm(args) -> None:
+    import torch
+    import torch.distributed as dist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -168,42 +365,21 @@ def gpu_arm(args) -> None:
     backend = os.environ.get("MLOB_BENCH_BACKEND", "nccl")
     dev = int(os.environ.get("MLOB_BENCH_DEVICE", local))
     torch.cuda.set_device(dev)
+    cpu_group = None
     if world > 1:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             dist.init_process_group(backend)
+        cpu_group = dist.new_group(backend="gloo") if backend == "nccl" else None
     coll_dev = "cuda" if backend == "nccl" else "cpu"
 
     def allreduce(t, op=None):
         if world > 1:
             x = t.to(coll_dev)
-            dist.all_reduce(x, op=op or dist.ReduceOp.SUM)
+            dist.all_reduce(x, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
             t.copy_(x)
         return t
-
-    n_total, cfg, synth, label = workload(args.workload)
-    if args.mps:
-        cfg.messages_per_step = args.mps
-        synth.n_messages = (n_total + 64) * args.mps
-        synth.state_sample_every = args.mps
-    if args.envs:
-        n_total = args.envs
-        synth.n_messages = (n_total + 64) * cfg.messages_per_step
-    per = n_total // world
-    base = rank * per
-    n_local = per if rank < world - 1 else n_total - base
-    t0 = time.time()
-    hs = HostStore.synth(synth, 0)
-    if args.workload == "D":
-        hs.trim_front(16 * 6400)  # every remaining episode starts with a full 1000-level book
-    gen_s = time.time() - t0
-    store = DeviceStore(hs, dev)
-    del hs
-    venv = MarketVecEnv(store, cfg, seed=0, n_envs=n_local, n_envs_global=n_total,
-                        env_index_base=base, device=dev)
-    venv.reset_all()
-    stream = torch.cuda.ExternalStream(venv.stream, device=torch.device("cuda", dev))
 
     def barrier():
         torch.cuda.synchronize()
@@ -211,119 +387,43 @@ def gpu_arm(args) -> None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    gstep = 0
-    for _ in range(args.warmup):
-        venv.step_random(0, gstep)
-        gstep += 1
-    venv.synchronize()
-    m0 = venv.messages_processed()
-    l0 = venv.launches
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    with ClockSampler(dev) as clocks:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            venv.step_random(0, gstep)
-            gstep += 1
-        ev1.record(stream)
-        ev1.synchronize()
-    launches = venv.launches - l0
-    venv.synchronize()
-    ms = ev0.elapsed_time(ev1)
-    msgs = venv.messages_processed() - m0
-    # whole-job: max time over ranks, sum of messages
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    m = torch.tensor([msgs], dtype=torch.float64, device="cuda")
-    allreduce(t, dist.ReduceOp.MAX)
-    allreduce(m)
-    ms_max, msgs_all = float(t.item()), float(m.item())
-    value = msgs_all / (ms_max / 1e3)
-    env_steps = n_total * args.steps / (ms_max / 1e3)
-
-    # K4 + NCCL: episode statistics reduced across ranks (the only collective)
-    stats = torch.zeros(abi.STAT_WORDS * cfg.n_specs, dtype=torch.float64, device="cuda")
-    venv.episode_stats_device(stats.data_ptr())
-    venv.synchronize()
-    allreduce(stats)
-
-    # e2e through the public API with host buffers, every step: pinned actions
-    # H2D, step, rewards + dones + per-type observations and reset flags D2H
-    # (mlob_venv_step_io: one call; the copies overlap the chunked step)
-    A = venv.n_agents
-    rng = np.random.default_rng(1234)
-    ar = np.array([abi.action_arity(cfg.specs[s]) for s in abi.flat_specs(cfg)])
-    e_steps = max(3, min(args.steps, args.e2e_steps))
-    # a fresh random action batch per step (pre-drawn, page-locked; not timed)
-    acts_all = [torch.from_numpy((rng.integers(0, 1 << 30, size=(n_local, A)) % ar).astype(np.int32))
-                .pin_memory() for _ in range(e_steps + 1)]
-    acts = acts_all[0]
-    obs_bufs = [torch.empty((venv.n_streams(t), venv.obs_dim(t)), dtype=torch.float64).pin_memory()
-                for t in range(cfg.n_specs)]
-    rew = torch.empty((n_local, A), dtype=torch.float64).pin_memory()
-    dn = torch.empty((n_local, A), dtype=torch.uint8).pin_memory()
-    rsb = [torch.empty(venv.n_streams(t), dtype=torch.uint8).pin_memory() for t in range(cfg.n_specs)]
-
-    def e2e_step(a):
-        venv.step_io(actions=a, rewards=rew, dones=dn, obs=obs_bufs, resets=rsb)
-
-    e2e_step(acts_all[e_steps])  # warm-up (creates the copy streams)
-    em0 = venv.messages_processed()
-    barrier()
-    w0 = time.perf_counter()
-    for i in range(e_steps):
-        e2e_step(acts_all[i])
-    torch.cuda.synchronize()
-    e_wall = torch.tensor([time.perf_counter() - w0], dtype=torch.float64, device="cuda")
-    allreduce(e_wall, dist.ReduceOp.MAX)
-    e_m = torch.tensor([venv.messages_processed() - em0], dtype=torch.float64, device="cuda")
-    allreduce(e_m)
-    e_msgs = float(e_m.item())
-    h2d = acts.numel() * 4
-    d2h = rew.numel() * 8 + dn.numel() + sum(b.numel() * 8 for b in obs_bufs) + \
-        sum(b.numel() for b in rsb)
-    e2e_val = e_msgs / float(e_wall.item())
-
+    r = measure(args.workload, args, world, rank, local, dev, allreduce, barrier, cpu_group)
+    extra = {}
+    if args.workload != "D" and not args.no_extra:
+        # config D (deep book, BASELINE.json configs[3]) in the same driver-run line
+        d = measure("D", args, world, rank, local, dev, allreduce, barrier, cpu_group,
+                    with_e2e=True)
+        extra["D"] = {k: d[k] for k in ("value", "ms_per_step", "env_steps_per_s", "roofline", "e2e",
+                                        "launches", "clocks")}
+        extra["D"]["workload"] = d["label"]
+        extra["D"]["n_envs"] = d["n_total"]
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
-    peak, peak_kind = peaks()
-    bmsg = B_MSG.get(args.workload, 169.1)
-    per_launch_msgs = msgs / max(1, args.steps)          # this rank's launch
-    avg_launch_s = ms / 1e3 / max(1, launches)
-    achieved = bmsg * per_launch_msgs / avg_launch_s / 1e9
-    traffic = None
-    prof = {}
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            prof = json.load(f)
-        if args.workload == "D":  # the deep-book kernel's own capture
-            prof = prof["deep_book_D"]
-        traffic = prof["dram_bytes_per_msg"] * per_launch_msgs
-    except Exception:
-        pass
-    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+    cfg = r["cfg"]
+    l2 = ("inputs larger than L2" if not r["flush"] else "L2 flushed between timed steps") + \
+        f" (working set {r['work'] / 2 ** 30:.2f} GiB per GPU vs L2 {r['l2'] / 2 ** 20:.0f} MiB)"
+    out = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-           "config": {"workload": label, "n_envs": n_total, "envs_per_gpu": n_local,
-                      "agents_per_env": A, "messages_per_step": cfg.messages_per_step,
+           "config": {"workload": r["label"], "n_envs": r["n_total"], "envs_per_gpu": r["n_local"],
+                      "agents_per_env": cfg.n_agents if hasattr(cfg, "n_agents") else None,
+                      "messages_per_step": cfg.messages_per_step,
                       "steps_per_episode": cfg.steps_per_episode,
                       "book_capacity": cfg.book_capacity, "parallelism": f"env-shard x{world}",
-                      "l2": "inputs larger than L2 (book state of all envs >> 126 MB)",
-                      "store_messages": int(synth.n_messages), "store_gen_s": round(gen_s, 2)},
-           "env_steps_per_s": env_steps,
-           "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                        "frac": achieved / peak, "traffic": traffic,
-                        "bytes_per_msg": bmsg, "peak_kind": peak_kind,
-                        # from the committed ncu capture (profiles/ncu_summary.json): the
-                        # resource that actually binds the step
-                        "alu_pipe_pct_of_peak": prof.get("alu_pipe_pct_of_peak"),
-                        "issue_active_pct": prof.get("issue_active_pct")},
-           "gpu_launches": launches,
-           "clocks": clocks.summary(),
-           "episode_stats": {"episodes": float(stats[4].item())},
-           "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                   "d2h_bytes_per_step": d2h, "steps": e_steps}}
+                      "l2": l2, "store_messages": None, "store_gen_s": round(r["gen_s"], 2)},
+           "env_steps_per_s": r["env_steps_per_s"],
+           "roofline": r["roofline"],
+           "gpu_launches": r["launches"],
+           "clocks": r["clocks"],
+           "episode_stats": {"episodes": r["episodes"]},
+           "e2e": r["e2e"]}
+    from paper_2511_02136_b200 import abi
+    out["config"]["agents_per_env"] = sum(s.count for s in cfg.specs[:cfg.n_specs])
+    out["config"]["store_messages"] = int(workload(args.workload)[2].n_messages)
+    if extra:
+        out["workloads"] = extra
     if world == 1 and not args.no_cpu:
         try:
             row, workers, n, _ = cpu_reference_run(args.ref_envs, args.cpu_steps, 2, args.workload)
@@ -332,6 +432,11 @@ def gpu_arm(args) -> None:
                                    "sample": f"{n} envs x {args.cpu_steps} timed steps (+2 warm-up), "
                                              f"bench::run_throughput, {workers} threads, "
                                              f"wall {row.wall_seconds:.2f}s"}
+            row1, _, n1, _ = cpu_reference_run(4096, 30, 2, args.workload, workers=1)
+            out["cpu_baseline"]["per_core"] = {
+                "value": row1.messages_per_sec, "unit": UNIT, "cores": 1,
+                "sample": f"{n1} envs x 30 timed steps (+2 warm-up), bench::run_throughput, 1 thread, "
+                          f"wall {row1.wall_seconds:.2f}s"}
         except Exception as e:  # reported, not fatal
             out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                    "sample": f"unavailable: {e}"}
@@ -353,6 +458,7 @@ def main():
     p.add_argument("--cpu-steps", type=int, default=300)
     p.add_argument("--e2e-steps", type=int, default=10)
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-extra", action="store_true", help="skip the config-D entry of the line")
     args = p.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3

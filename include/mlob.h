@@ -300,6 +300,12 @@ mlob_status mlob_host_store_state(const mlob_host_store* s, uint64_t i, uint64_t
                                   mlob_level* bids, uint32_t* n_bids, mlob_level* asks,
                                   uint32_t* n_asks, uint32_t cap);
 void mlob_host_store_free(mlob_host_store* s);
+/* Binary image of a host store (messages + sampled states).  One process per
+ * node synthesises and saves, the other ranks load: the store is built once
+ * per node, not once per GPU (new; the reference builds one store per
+ * process, util/config.hpp:382-419). */
+mlob_status mlob_host_store_save(const mlob_host_store* s, const char* path);
+mlob_status mlob_host_store_load(const char* path, mlob_host_store** out);
 
 /* data::build_episode_index, data/store.hpp:52-72.  Writes up to `cap` starts
  * and the full count to *n_out. */
@@ -632,6 +638,13 @@ mlob_status mlob_venv_synchronize(mlob_venv* v);
 void* mlob_venv_stream(const mlob_venv* v);
 /* Kernel launches issued by this handle so far (bench evidence). */
 uint64_t mlob_venv_launch_count(const mlob_venv* v);
+/* Per-kernel timing of the step (measurement only): with profiling on, every
+ * mlob_venv_step / _step_random records CUDA events around its three kernels
+ * on the handle's stream; kernel_ms returns the summed milliseconds of
+ * [act_kernel, book_kernel, outcome_kernel] since profiling was switched on
+ * and the number of steps timed. */
+mlob_status mlob_venv_profile(mlob_venv* v, int on);
+mlob_status mlob_venv_kernel_ms(mlob_venv* v, double* out3, uint64_t* steps);
 
 #ifdef __cplusplus
 }

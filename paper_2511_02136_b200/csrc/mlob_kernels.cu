@@ -423,13 +423,19 @@ static cudaError_t launch_book(const KParams& kp, const DevCfg& cfg, int spl, cu
 
 int slots_per_lane(int capacity) { return spl_of(capacity); }
 
-cudaError_t launch_step(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s) {
+// ev: optional 4 events recorded around the three kernels (per-kernel timing)
+cudaError_t launch_step(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s, cudaEvent_t* ev) {
+  cudaError_t e;
+  if (ev && (e = cudaEventRecord(ev[0], s)) != cudaSuccess) return e;
   act_kernel<<<thread_grid(kp.n_envs), kThreadBlock, 0, s>>>(kp);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (ev && (e = cudaEventRecord(ev[1], s)) != cudaSuccess) return e;
   if ((e = launch_book(kp, cfg, spl, s)) != cudaSuccess) return e;
+  if (ev && (e = cudaEventRecord(ev[2], s)) != cudaSuccess) return e;
   outcome_kernel<<<thread_grid(kp.n_envs), kThreadBlock, 0, s>>>(kp);
-  return cudaGetLastError();
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (ev && (e = cudaEventRecord(ev[3], s)) != cudaSuccess) return e;
+  return cudaSuccess;
 }
 
 cudaError_t launch_reset(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s) {

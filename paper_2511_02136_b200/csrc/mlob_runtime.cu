@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <dlfcn.h>
 #include <memory>
@@ -27,7 +28,7 @@ size_t step_min_smem_bytes(const DevCfg& c);
 uint32_t step_amsg_cap(const DevCfg& c);
 int step_launches();
 int slots_per_lane(int capacity);
-cudaError_t launch_step(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s);
+cudaError_t launch_step(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s, cudaEvent_t* ev = nullptr);
 cudaError_t launch_reset(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s);
 cudaError_t launch_stats(const KParams& kp, const DevCfg& cfg, double* out, cudaStream_t s);
 cudaError_t launch_sum_msgs(const EnvHdr* hdr, uint64_t n, unsigned long long* out, cudaStream_t s);
@@ -225,6 +226,19 @@ struct mlob_venv {
   DevCfg* d_cfg = nullptr;
 
   double* d_stats = nullptr;  // K4 output for mlob_venv_allreduce_episode_stats
+  // per-kernel timing of step launches (mlob_venv_profile): 4 events per step
+  bool profiling = false;
+  std::vector<cudaEvent_t> prof_ev;
+  size_t prof_steps = 0;
+  cudaEvent_t* prof_slot() {
+    if (!profiling) return nullptr;
+    while (prof_ev.size() < 4 * (prof_steps + 1)) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreate(&e), "event");
+      prof_ev.push_back(e);
+    }
+    return prof_ev.data() + 4 * prof_steps++;
+  }
   double* alloc_scratch_stats() {
     if (!d_stats) d_stats = alloc<double>(static_cast<size_t>(MLOB_MAX_SPECS) * kStatWords, "stats");
     return d_stats;
@@ -244,6 +258,7 @@ struct mlob_venv {
         cudaStreamDestroy(s);
       }
     for (cudaEvent_t e : io_events) cudaEventDestroy(e);
+    for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
     for (int t = 0; t < MLOB_MAX_SPECS; ++t) {
       free_net(nets[t]);
       cudaFree(batch[t].arena);
@@ -357,6 +372,26 @@ struct mlob_venv {
 };
 
 // ===========================================================================
+// Binary store file: magic, counts, then the five arrays as they sit in
+// memory (one writer per node, every rank reads: SURVEY §8e builds the
+// store once per node instead of once per GPU).
+namespace {
+constexpr uint64_t kStoreMagic = 0x31454f5453424f4dull;  // "MOBSTOE1"
+template <class T>
+void write_vec(std::FILE* f, const std::vector<T>& v) {
+  const uint64_t n = v.size();
+  if (std::fwrite(&n, 8, 1, f) != 1 || (n && std::fwrite(v.data(), sizeof(T), n, f) != n))
+    mlob::fail(MLOB_E_RUNTIME, "store file: write failed");
+}
+template <class T>
+void read_vec(std::FILE* f, std::vector<T>& v) {
+  uint64_t n = 0;
+  if (std::fread(&n, 8, 1, f) != 1) mlob::fail(MLOB_E_RUNTIME, "store file: truncated");
+  v.resize(n);
+  if (n && std::fread(v.data(), sizeof(T), n, f) != n) mlob::fail(MLOB_E_RUNTIME, "store file: truncated");
+}
+}  // namespace
+
 extern "C" {
 
 const char* mlob_last_error(void) { return g_err.c_str(); }
@@ -526,6 +561,51 @@ mlob_status mlob_host_store_state(const mlob_host_store* s, uint64_t i, uint64_t
   });
 }
 void mlob_host_store_free(mlob_host_store* s) { delete s; }
+
+
+mlob_status mlob_host_store_save(const mlob_host_store* s, const char* path) {
+  return guarded([&] {
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) fail(MLOB_E_RUNTIME, std::string("store file: cannot create ") + path);
+    try {
+      if (std::fwrite(&kStoreMagic, 8, 1, f) != 1) fail(MLOB_E_RUNTIME, "store file: write failed");
+      write_vec(f, s->msgs);
+      write_vec(f, s->st_index);
+      write_vec(f, s->st_offset);
+      write_vec(f, s->st_nb);
+      write_vec(f, s->levels);
+    } catch (...) {
+      std::fclose(f);
+      throw;
+    }
+    if (std::fclose(f) != 0) fail(MLOB_E_RUNTIME, "store file: write failed");
+  });
+}
+
+mlob_status mlob_host_store_load(const char* path, mlob_host_store** out) {
+  *out = nullptr;
+  return guarded([&] {
+    std::FILE* f = std::fopen(path, "rb");
+    if (!f) fail(MLOB_E_RUNTIME, std::string("store file: cannot open ") + path);
+    auto s = std::make_unique<mlob_host_store>();
+    try {
+      uint64_t magic = 0;
+      if (std::fread(&magic, 8, 1, f) != 1 || magic != kStoreMagic) fail(MLOB_E_RUNTIME, "store file: bad magic");
+      read_vec(f, s->msgs);
+      read_vec(f, s->st_index);
+      read_vec(f, s->st_offset);
+      read_vec(f, s->st_nb);
+      read_vec(f, s->levels);
+    } catch (...) {
+      std::fclose(f);
+      throw;
+    }
+    std::fclose(f);
+    if (s->st_offset.size() != s->st_index.size() + 1 || s->st_nb.size() != s->st_index.size())
+      fail(MLOB_E_RUNTIME, "store file: inconsistent state arrays");
+    *out = s.release();
+  });
+}
 
 mlob_status mlob_build_episode_index(uint64_t n_messages, int steps, int mps, int stride,
                                      uint64_t* starts, uint64_t cap, uint64_t* n_out) {
@@ -990,7 +1070,7 @@ static void do_step(mlob_venv* v, int mode, uint64_t bench_seed, uint64_t global
   kp.action_mode = mode;
   kp.bench_seed = bench_seed;
   kp.global_step = global_step;
-  cuda_check(launch_step(kp, v->dcfg, v->spl, v->stream), "step kernels");
+  cuda_check(launch_step(kp, v->dcfg, v->spl, v->stream, v->prof_slot()), "step kernels");
   v->launches += step_launches();
   advance_step(v);
 }
@@ -1991,6 +2071,28 @@ mlob_status mlob_venv_allreduce_episode_stats(mlob_venv* v, void* nccl_comm, mlo
                                    w[MLOB_STAT_REMAINING] / static_cast<double>(sp.params.task_size)
                              : 0.0;
     }
+  });
+}
+
+mlob_status mlob_venv_profile(mlob_venv* v, int on) {
+  return guarded([&] {
+    v->profiling = on != 0;
+    v->prof_steps = 0;
+  });
+}
+
+mlob_status mlob_venv_kernel_ms(mlob_venv* v, double* out, uint64_t* steps) {
+  return guarded([&] {
+    v->set_device();
+    cuda_check(cudaStreamSynchronize(v->stream), "sync");
+    out[0] = out[1] = out[2] = 0.0;
+    for (size_t i = 0; i < v->prof_steps; ++i)
+      for (int k = 0; k < 3; ++k) {
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, v->prof_ev[4 * i + k], v->prof_ev[4 * i + k + 1]), "elapsed");
+        out[k] += ms;
+      }
+    *steps = v->prof_steps;
   });
 }
 

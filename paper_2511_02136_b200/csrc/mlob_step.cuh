@@ -1406,7 +1406,6 @@ struct WarpEnv {
   template <int S>
   __device__ __forceinline__ int compact_side(ActTmp* tmp, int base, int cap) {
     SideT& d = sd<S>();
-#if MLOB_ACT_ROWS
     if constexpr (SMEM) {
       // shared-memory book: one pass over the arrival words (gated by the
       // occupancy mask) finds this lane's agent rows; only rows holding an
@@ -1423,16 +1422,15 @@ struct WarpEnv {
         if (is_ag && pos < cap) tmp[pos] = ActTmp{d.P(k), d.ST(k), d.LO(k), d.HI(k), d.Q(k), 0};
         base += __popc(b);
       }
-      return base;
-    }
-#endif
-    MLOB_ROWS(k) {
-      const bool is_ag = d.Q(k) > 0 && (d.ST(k) & 0xffu) != 0;
-      const uint32_t b = __ballot_sync(FULLMASK, is_ag);
-      if (b == 0) continue;
-      const int pos = base + __popc(b & ((1u << lane) - 1u));
-      if (is_ag && pos < cap) tmp[pos] = ActTmp{d.P(k), d.ST(k), d.LO(k), d.HI(k), d.Q(k), 0};
-      base += __popc(b);
+    } else {
+      MLOB_ROWS(k) {
+        const bool is_ag = d.Q(k) > 0 && (d.ST(k) & 0xffu) != 0;
+        const uint32_t b = __ballot_sync(FULLMASK, is_ag);
+        if (b == 0) continue;
+        const int pos = base + __popc(b & ((1u << lane) - 1u));
+        if (is_ag && pos < cap) tmp[pos] = ActTmp{d.P(k), d.ST(k), d.LO(k), d.HI(k), d.Q(k), 0};
+        base += __popc(b);
+      }
     }
     return base;
   }

@@ -26,7 +26,7 @@ from .abi import (AgentAction, AgentInfo, AgentState, EnvConfig, EnvScalars, Epi
                   Message, RestingOrder, SynthConfig, Trade, VenvDesc)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("MLOB_LIB") or os.path.join(HERE, "libmlob.so")
+LIB_PATH = os.path.join(HERE, "libmlob.so")  # the in-tree product library, nothing else
 
 _EXC = {abi.MLOB_E_INVALID_ARGUMENT: ValueError, abi.MLOB_E_OUT_OF_RANGE: IndexError,
         abi.MLOB_E_LOGIC: RuntimeError, abi.MLOB_E_RUNTIME: RuntimeError,
@@ -53,6 +53,8 @@ _SIGS = {
     "mlob_host_store_synth": (C.c_int, [_P(SynthConfig), C.c_uint64, _P(_vp)]),
     "mlob_host_store_create": (C.c_int, [_P(Message), C.c_uint64, _P(abi.BookStates), _P(_vp)]),
     "mlob_host_store_trim_front": (C.c_int, [_vp, C.c_uint64]),
+    "mlob_host_store_save": (C.c_int, [_vp, C.c_char_p]),
+    "mlob_host_store_load": (C.c_int, [C.c_char_p, _vp]),
     "mlob_host_store_n_messages": (C.c_uint64, [_vp]),
     "mlob_host_store_messages": (_P(Message), [_vp]),
     "mlob_host_store_n_states": (C.c_uint64, [_vp]),
@@ -113,6 +115,8 @@ _SIGS = {
     "mlob_venv_episode_stats": (C.c_int, [_vp, C.c_int, _P(EpisodeStats)]),
     "mlob_venv_episode_stats_device": (C.c_int, [_vp, _vp]),
     "mlob_venv_allreduce_episode_stats": (C.c_int, [_vp, _vp, _vp]),
+    "mlob_venv_profile": (C.c_int, [_vp, C.c_int]),
+    "mlob_venv_kernel_ms": (C.c_int, [_vp, _vp, _vp]),
     "mlob_venv_clear_episode_stats": (C.c_int, [_vp]),
     "mlob_venv_read_scalars": (C.c_int, [_vp, C.c_uint64, _P(EnvScalars)]),
     "mlob_venv_read_book": (C.c_int, [_vp, C.c_uint64, C.c_int, _P(RestingOrder), C.c_uint64,
@@ -209,6 +213,16 @@ class HostStore:
         _check(lib().mlob_host_store_create(msgs.ctypes.data_as(_P(Message)), len(msgs),
                                             C.byref(bs), C.byref(h)))
         return cls(h)
+
+    @classmethod
+    def load(cls, path: str) -> "HostStore":
+        """A store saved by save() (one writer per node)."""
+        h = _vp()
+        _check(lib().mlob_host_store_load(path.encode(), C.byref(h)))
+        return cls(h)
+
+    def save(self, path: str) -> None:
+        _check(lib().mlob_host_store_save(self.h, path.encode()))
 
     def trim_front(self, n: int) -> None:
         _check(lib().mlob_host_store_trim_front(self.h, n))
@@ -540,6 +554,17 @@ class _Venv:
         out = (EpisodeStats * self.n_types())()
         _check(lib().mlob_venv_allreduce_episode_stats(self.h, _vp(nccl_comm), out))
         return list(out)
+
+    def profile(self, on: bool) -> None:
+        """Per-kernel event timing of the following steps (measurement only)."""
+        _check(lib().mlob_venv_profile(self.h, 1 if on else 0))
+
+    def kernel_ms(self):
+        """([act, book, outcome] summed ms, steps timed) since profile(True)."""
+        out = (C.c_double * 3)()
+        n = C.c_uint64()
+        _check(lib().mlob_venv_kernel_ms(self.h, out, C.byref(n)))
+        return list(out), n.value
 
     def clear_episode_stats(self) -> None:
         _check(lib().mlob_venv_clear_episode_stats(self.h))
