@@ -3,8 +3,30 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 
 #include "../../include/mlob.h"
+
+// Checked builds (libmlob_checked.so, -DMLOB_CHECKS=1): device-side bounds
+// and invariant assertions on the hand-off buffers, the book rows, the fill
+// log and the mbarrier waits; a failure prints its site and traps (the test
+// harness's stand-in for compute-sanitizer, which is closed on this pool).
+#ifndef MLOB_CHECKS
+#define MLOB_CHECKS 0
+#endif
+#if MLOB_CHECKS
+#define MLOB_CHECK(c)                                                            \
+  do {                                                                           \
+    if (!(c)) {                                                                  \
+      printf("MLOB_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c);           \
+      __trap();                                                                  \
+    }                                                                            \
+  } while (0)
+#else
+#define MLOB_CHECK(c) \
+  do {                \
+  } while (0)
+#endif
 
 namespace mlob {
 

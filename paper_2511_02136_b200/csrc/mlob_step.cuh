@@ -486,6 +486,18 @@ __device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t 
                : "memory");
 }
 __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+#if MLOB_CHECKS  // a lost bulk copy would hang: trap after ~2^28 polls instead
+  for (uint32_t spin = 0;; ++spin) {
+    uint32_t done;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    MLOB_CHECK(spin < (1u << 28));
+  }
+#endif
   asm volatile(
       "{\n.reg .pred p;\nWAIT_%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
@@ -576,7 +588,10 @@ struct WarpEnv {
     n_agents_ = c.n_agents;
   }
 
-  __device__ __forceinline__ void bind(uint64_t e) { env = e; }
+  __device__ __forceinline__ void bind(uint64_t e) {
+    MLOB_CHECK(e < kp.n_envs);
+    env = e;
+  }
 
   template <int S>
   __device__ __forceinline__ SideT& sd() {
@@ -776,6 +791,7 @@ struct WarpEnv {
   }
   // this step's agent messages (act_kernel's hand-off) into shared memory
   __device__ __forceinline__ void load_agent_msgs() {
+    MLOB_CHECK(n_amsg <= kp.amsg_cap);
     const uint4* src = reinterpret_cast<const uint4*>(kp.amsg + env * kp.amsg_cap);
     uint4* dst = reinterpret_cast<uint4*>(sm.amsg());
     for (uint32_t i = lane; i < 2 * n_amsg; i += kWarp) dst[i] = src[i];
@@ -1063,6 +1079,7 @@ struct WarpEnv {
           kp.fill_pool[static_cast<size_t>(fill_cur) * kFillChunk].price = static_cast<int32_t>(c);
         fill_cur = c;
       }
+      MLOB_CHECK(fill_cur < kp.fill_pool_chunks && off < kFillChunk);
       dst = kp.fill_pool + static_cast<size_t>(fill_cur) * kFillChunk + off;
     }
     if (lane == 0) *dst = FillEnt{price, qty, trader - 1, side};
@@ -1456,6 +1473,8 @@ struct WarpEnv {
           if ((i < D ? i < nb_l2 : i - D < na_l2)) dst[i] = sm.l2()[i];
       }
     }
+    MLOB_CHECK(nb_l2 <= cfg.obs_depth && na_l2 <= cfg.obs_depth);
+    MLOB_CHECK(live0 <= capacity() && live1 <= capacity() && live0 >= 0 && live1 >= 0);
     if (lane == 0) kp.l2sum[env] = L2Sum{nb_l2, na_l2, sumq0, sumq1, topq0, topq1, 0};
   }
 

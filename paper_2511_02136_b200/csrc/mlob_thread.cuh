@@ -35,6 +35,7 @@ struct ThreadEnv {
   uint32_t err = 0;
 
   __device__ ThreadEnv(const KParams& p, const DevCfg& c, uint64_t e) : kp(p), cfg(c), env(e) {
+    MLOB_CHECK(e < kp.n_envs);
     genv = kp.env_index ? kp.env_index[e] : kp.env_index_base + e;
     seed = kp.env_seed ? kp.env_seed[e] : kp.seed;
     h = kp.hdr[e];
@@ -312,6 +313,7 @@ struct ThreadEnv {
       if (i < kFillInline) return inl[i];
       const uint32_t k = i - kFillInline, off = k % (kFillChunk - 1) + 1;
       if (off == 1 && k > 0) chunk = static_cast<uint32_t>(pool[static_cast<size_t>(chunk) * kFillChunk].price);
+      MLOB_CHECK(chunk != kNoChunk);
       return pool[static_cast<size_t>(chunk) * kFillChunk + off];
     }
   };
@@ -483,6 +485,7 @@ struct ThreadEnv {
                             L2Lvl* l2out, int32_t& nl, int64_t& sumq, int64_t& topq) const {
     const int32_t empty_p = S == 0 ? INT_MIN : INT_MAX;
     const uint32_t rows = (n + kWarp - 1) / kWarp;
+    MLOB_CHECK(rows <= static_cast<uint32_t>(spl));
     const size_t base = (env * 2 + static_cast<uint64_t>(S)) * spl * kWarp;
     for (uint32_t i = 0; i < rows * kWarp; ++i) {
       const size_t x = base + i;

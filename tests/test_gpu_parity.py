@@ -92,6 +92,57 @@ def test_scenario_parity(orc, scenario):
                 compare_env_state(b.view(i), r)
 
 
+def _sweep(side, price, qty):
+    a = abi.AgentAction()
+    a.direct = 1
+    a.n_quotes = 1
+    a.quotes[0].side = side
+    a.quotes[0].price = price
+    a.quotes[0].quantity = qty
+    return a
+
+
+def test_fill_log_beyond_inline_and_chunks_exact(orc):
+    """Agent orders that sweep a whole side: more agent fills in one env-step
+    than the inline log (16) and several overflow chunks (31 each) hold.  The
+    MM rewards (Ψ sums in fill order against M̄, rewards.hpp:22-36), the
+    executor slippage and the agent accounting must stay bit-exact."""
+    A = abi
+    cfg = A.env_config([A.agent_spec(A.MARKET_MAKER, reward=A.REWARD_SPOONER),
+                        A.agent_spec(A.MARKET_MAKER, reward=A.REWARD_BUYSELL, inventory_cap=5000),
+                        A.agent_spec(A.EXECUTOR, task_size=100000)],
+                       steps_per_episode=12, messages_per_step=100, start_stride_steps=12)
+    dev = dev_store({})
+    ost = small_store(orc, {})
+    n_envs = 4
+    b = MarketEnvBatch(dev, cfg, n_envs=n_envs, seed=2)
+    refs = [OEnv(orc, ost, cfg, 2, i) for i in range(n_envs)]
+    b.reset(list(range(n_envs)))
+    for i, r in enumerate(refs):
+        r.reset(i)
+    rng = kat.CounterRng(77)
+    most = 0
+    for t in range(12):
+        acts = []
+        for e in range(n_envs):
+            for a in range(b.n_agents):
+                k = (t + a + e) % 3
+                if k == 0:   # buy through every ask level
+                    acts.append(_sweep(A.BID, 2000, 4000 + rng.below(100)))
+                elif k == 1:  # sell through every bid level
+                    acts.append(_sweep(A.ASK, 1, 4000 + rng.below(100)))
+                else:
+                    acts.append(random_direct_action(rng))
+        b.step_actions(acts)
+        for i, r in enumerate(refs):
+            r.step(acts[i * b.n_agents:(i + 1) * b.n_agents])
+        for i, r in enumerate(refs):
+            compare_env_state(b.view(i), r)
+            most = max(most, sum(b.view(i).info(a).step_fill_count for a in range(b.n_agents)))
+    # the sweeps overflowed the inline log and at least two overflow chunks
+    assert most > 16 + 2 * 31, most
+
+
 def test_vec_env_auto_reset_and_episode_stats(orc):
     cfg = abi.env_config([abi.agent_spec(abi.MARKET_MAKER, count=2), abi.agent_spec(abi.EXECUTOR)],
                          steps_per_episode=8, messages_per_step=20, start_stride_steps=3)
