@@ -79,11 +79,18 @@ __device__ inline uint32_t* book_region(char* base, const DevCfg& c) {
 // warps run the same phase's code together (the I-cache holds one phase).
 // Shared-memory (deep) books: blocks of as many warps as the shared memory
 // holds, one env per warp.
+#ifndef MLOB_ROUND_SYNC  // block barrier at each round start (measured -3 % since the split)
+#define MLOB_ROUND_SYNC 0
+#endif
+// warps per register-book block and the register budget they leave: C <= 128
+// (SPL <= 4) 28 warps x 72 registers (+2.4 % on C over 24 x 80, after the
+// header fields left the loop's registers); SPL = 8 keeps 80 book registers,
+// so 16 warps x 128
 #ifndef MLOB_SYNC_WARPS
-#define MLOB_SYNC_WARPS 24
+#define MLOB_SYNC_WARPS 28
 #endif
 #ifndef MLOB_SYNC_REGS
-#define MLOB_SYNC_REGS 80
+#define MLOB_SYNC_REGS 72
 #endif
 template <int SPL>
 __host__ __device__ constexpr bool rounds_of() {
@@ -91,14 +98,13 @@ __host__ __device__ constexpr bool rounds_of() {
 }
 template <int SPL>
 __host__ __device__ constexpr int warps_per_block() {
-  return rounds_of<SPL>() ? MLOB_SYNC_WARPS : 8;
+  return !rounds_of<SPL>() ? 8 : SPL <= 4 ? MLOB_SYNC_WARPS : 16;
 }
 template <int SPL>
 __host__ __device__ constexpr int min_blocks() {
-  return rounds_of<SPL>() ? (65536 / (MLOB_SYNC_REGS * 32 * MLOB_SYNC_WARPS) > 0
-                                 ? 65536 / (MLOB_SYNC_REGS * 32 * MLOB_SYNC_WARPS)
-                                 : 1)
-                          : 1;
+  return rounds_of<SPL>() && SPL <= 4 && 65536 / (MLOB_SYNC_REGS * 32 * MLOB_SYNC_WARPS) > 0
+             ? 65536 / (MLOB_SYNC_REGS * 32 * MLOB_SYNC_WARPS)
+             : 1;
 }
 constexpr int kThreadBlock = 128;  // thread-per-env kernels
 
@@ -222,37 +228,30 @@ __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL
   const uint64_t n_rounds = rounds ? (kp.n_envs + stride - 1) / stride : 1;
   uint64_t nenv = rounds ? first + stride : kp.n_envs;
   for (uint64_t env = first, round = 0; round < n_rounds; ++round) {
-    if constexpr (rounds) {
+    if constexpr (rounds && MLOB_ROUND_SYNC) {
       if (round > 0) __syncthreads();
     }
     if (!idle) {
       const bool has_next = nenv < kp.n_envs;
       w.bind(env);
+      const DevMsg* slice = slice_of(env);
       w.load_hdr();
       w.book_load_issue();  // shared-memory books: bulk loads in flight from here
-      const DevMsg* slice = kp.msgs + kp.ep_start[w.episode] + static_cast<uint64_t>(w.step) * mps;
       if (nch >= 2) w.stage(slice + kChunk, min(kChunk, mps - kChunk));
       const DevMsg* next_slice = has_next && mps > 0 ? slice_of(nenv) : nullptr;
       w.load_agent_msgs();
       w.book_load_wait();
       // (3) + (4): agent messages, then the replay slice
-      w.prev_mid_half = w.mid_half;
       w.n_trades = 0;
       w.n_fills = 0;
       w.fill_head = kNoChunk;
       w.process_messages(w.n_amsg, slice);
       if (next_slice) w.stage(next_slice, min(kChunk, mps));  // overlaps the step's tail
-      if (w.live0 > 0) w.last_bid = w.best0;
-      if (w.live1 > 0) w.last_ask = w.best1;
       // (5), book-dependent part
-      w.mbar = w.mid_count > 0 ? static_cast<double>(w.mid_sum) / (2.0 * static_cast<double>(w.mid_count))
-                               : static_cast<double>(w.prev_mid_half) / 2.0;
       w.rebuild_active();
-      ++w.step;
-      w.terminal = w.step >= cfg.steps_per_episode;
       w.snapshot();
       w.store_book();
-      w.store_hdr();
+      w.store_hdr(slice);
     }
     env = nenv;
     nenv = env + stride;
@@ -342,7 +341,8 @@ static size_t book_staged_bytes(const DevCfg& c) {  // dynamic-smem prefix (deep
 // as the shared memory holds for deep books (<= 8)
 static int book_warps(const DevCfg& c) {
   const bool deep = deep_book(c);
-  const int want = deep ? 8 : MLOB_SYNC_WARPS;
+  const int spl = spl_of(c.capacity);
+  const int want = deep ? 8 : spl <= 4 ? MLOB_SYNC_WARPS : 16;
   const size_t per = warp_smem_bytes(c);
   const size_t limit = deep ? 227 * 1024 - sizeof(SmemOff) - book_staged_bytes(c) - 256
                             : 227 * 1024 - sizeof(StagedParams) - sizeof(SmemOff) - 1024;

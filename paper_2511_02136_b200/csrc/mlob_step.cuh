@@ -553,11 +553,7 @@ struct WarpEnv {
   int live0, live1;
   int32_t best0, best1;
   uint32_t next_seq;
-  int64_t mid_half, prev_mid_half, last_bid, last_ask, last_time;
-  double mbar;
-  uint64_t episode, msgs;
-  int step;
-  bool terminal;
+  int64_t mid_half;
   int64_t mid_sum, mid_count;
   uint32_t n_trades;
   uint32_t n_fills, fill_head, fill_cur;  // agent-fill log (inline, then overflow chunks)
@@ -660,21 +656,19 @@ struct WarpEnv {
     return hwm;
   }
 
+  // Only the state the message loop needs is held in registers; the rest of
+  // the header is advanced in place after the loop (store_hdr).
   __device__ __forceinline__ void load_hdr() {
-    const EnvHdr& h = kp.hdr[env];
+    EnvHdr& h = kp.hdr[env];
     mid_half = h.mid_half;
-    last_bid = h.last_bid;
-    last_ask = h.last_ask;
-    last_time = h.last_time;
-    episode = h.episode;
-    msgs = h.msgs_processed;
     next_seq = h.next_seq;
-    step = h.step;
     live0 = h.live[0];
     live1 = h.live[1];
     best0 = h.best[0];
     best1 = h.best[1];
     n_amsg = h.n_amsg;
+    __syncwarp();
+    if (lane == 0) h.prev_mid_half = mid_half;  // env.hpp:220: the step's starting mid
   }
   __device__ __forceinline__ void load_book() {
     const EnvHdr& h = kp.hdr[env];
@@ -759,21 +753,26 @@ struct WarpEnv {
       if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
   }
-  // The header fields the book kernel advances (the outcome kernel owns
-  // the rest: episode bookkeeping, auto-reset).
-  __device__ __forceinline__ void store_hdr() {
+  // The header fields the book kernel advances (the outcome kernel owns the
+  // rest: episode bookkeeping, auto-reset): MarketEnv::step's tail after
+  // the message loop (env.hpp:233-247).  `slice` is the step's replay slice.
+  __device__ __forceinline__ void store_hdr(const DevMsg* slice) {
     const int h0 = hwm0, h1 = hwm1;
     if (lane == 0) {
       EnvHdr& h = kp.hdr[env];
-      h.mid_half = mid_half;
-      h.prev_mid_half = prev_mid_half;
-      h.mbar = mbar;
-      h.last_bid = last_bid;
-      h.last_ask = last_ask;
-      h.last_time = last_time;
-      h.msgs_processed = msgs;
-      h.next_seq = next_seq;
+      const int mps = cfg.mps;
+      const int total = static_cast<int>(n_amsg) + mps;
+      h.msgs_processed += static_cast<uint64_t>(total);
+      if (total > 0) h.last_time = mps > 0 ? slice[mps - 1].time : lds_msg(sm.amsg() + n_amsg - 1).time;
+      if (live0 > 0) h.last_bid = best0;  // env.hpp:238-239
+      if (live1 > 0) h.last_ask = best1;
+      h.mbar = mid_count > 0 ? static_cast<double>(mid_sum) / (2.0 * static_cast<double>(mid_count))
+                             : static_cast<double>(h.prev_mid_half) / 2.0;  // env.hpp:242-244
+      const int step = h.step + 1;
       h.step = step;
+      h.terminal = step >= cfg.steps_per_episode ? 1 : 0;
+      h.mid_half = mid_half;
+      h.next_seq = next_seq;
       h.live[0] = static_cast<uint16_t>(live0);
       h.live[1] = static_cast<uint16_t>(live1);
       h.hwm[0] = static_cast<uint16_t>(h0);
@@ -781,7 +780,6 @@ struct WarpEnv {
       h.best[0] = best0;
       h.best[1] = best1;
       h.n_trades = n_trades;
-      h.terminal = terminal ? 1 : 0;
       h.n_fills = n_fills;
       h.fill_head = fill_head;
     }
@@ -1324,11 +1322,7 @@ struct WarpEnv {
     mid_sum = *reinterpret_cast<const int64_t*>(sm.scal() + 4) + mid_half * (n_amsg + mps - sm.scal()[2]);
     // next_seq only grows: some arrival sequence reached kMaxSeq iff it ends above it
     if (next_seq > kMaxSeq) err |= kErrSeqRange;
-    const int total = n_amsg + mps;
-    msgs += static_cast<uint64_t>(total);
-    mid_count = total;
-    if (total > 0) last_time = mps > 0 ? slice[mps - 1].time : lds_msg(sm.amsg() + n_amsg - 1).time;
-    __syncwarp();  // lane 0's agent updates become visible to the warp
+    mid_count = n_amsg + mps;
   }
 
   // ---- step outcomes -------------------------------------------------------
