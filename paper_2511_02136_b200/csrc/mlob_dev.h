@@ -181,6 +181,7 @@ enum DevError : uint32_t {
   kErrBadTrader = 1u << 6,      // replay trader_id names a non-existent agent
   kErrFillPool = 1u << 7,       // agent-fill overflow pool exhausted in one step
   kErrAmsgCap = 1u << 8,        // more agent messages in one step than the hand-off buffer holds
+  kErrDeepRange = 1u << 9,      // deep-book 4-word slot: qty >= 2^24, order id >= 2^44 or seq >= 2^20
 };
 
 struct __align__(16) KParams {
@@ -217,10 +218,7 @@ struct __align__(16) KParams {
   int64_t* t_rem;          // Σ task_remaining of finished executor episodes [env * A + a]
   mlob_trade* trades;      // [env * trade_cap + i]
   uint32_t trade_cap;
-  uint32_t fill_overflows_unused;
-  unsigned long long* fill_overflow;  // count of env-steps whose MM fill log overflowed
-  unsigned long long* ticket;         // persistent step kernel: next-env ticket counter
-  long long* timing;                  // MLOB_PHASE_TIMING builds: [env][16] clock64 stamps
+  uint32_t _pad_tc;
   // env identity / episode pool
   const uint64_t* env_seed;   // optional
   const uint64_t* env_index;  // optional

@@ -18,7 +18,7 @@
 namespace mlob {
 
 __host__ __device__ inline size_t book_smem_bytes(int capacity) {
-  return static_cast<size_t>(2) * 5 * spl_of(capacity) * kWarp * sizeof(uint32_t);
+  return static_cast<size_t>(2) * 4 * spl_of(capacity) * kWarp * sizeof(uint32_t);  // SmemSide: 4 words a slot
 }
 // agent-message hand-off slots per env: every active order of every agent
 // may be deleted and two quotes placed (env.hpp:338-369); the same smem

@@ -348,6 +348,9 @@ struct mlob_venv {
     if (e & kErrBadTrader) fail(MLOB_E_RUNTIME, "replay trader_id names a non-existent agent");
     if (e & kErrFillPool) fail(MLOB_E_RUNTIME, "agent-fill log overflow pool exhausted in one step");
     if (e & kErrAmsgCap) fail(MLOB_E_RUNTIME, "more agent messages in one step than the hand-off buffer holds");
+    if (e & kErrDeepRange)
+      fail(MLOB_E_RUNTIME, "deep book (capacity > 256): resting quantity >= 2^24, order id >= 2^44 or more than "
+                           "2^20 arrivals in an episode");
     fail(MLOB_E_RUNTIME, "device error");
   }
 
@@ -878,6 +881,8 @@ mlob_status mlob_venv_create(const mlob_venv_desc* desc, mlob_venv** out) {
                                2 * max_depth;
     if (seq_bound >= kMaxSeq)
       fail(MLOB_E_INVALID_ARGUMENT, "episode too long for the device's 24-bit arrival sequence");
+    if (v->spl > 8 && seq_bound >= (1u << 20))
+      fail(MLOB_E_INVALID_ARGUMENT, "episode too long for the deep book's 20-bit arrival sequence");
     if (desc->episode_pool) {
       if (desc->pool_len == 0) fail(MLOB_E_INVALID_ARGUMENT, "MarketVecEnv: empty episode pool");
       v->pool.assign(desc->episode_pool, desc->episode_pool + desc->pool_len);
@@ -1849,7 +1854,10 @@ static KParams chunk_params(const mlob_venv* v, const KParams& k0, uint64_t c0, 
   const size_t bs = static_cast<size_t>(2 * v->spl * kWarp) * c0;
   k.bk_p += bs;
   k.bk_q += bs;
-  k.bk_id += bs;
+  if (v->spl > 8)  // deep books: the id buffer holds u32 low words (SmemSide layout)
+    k.bk_id = reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(k.bk_id) + bs);
+  else
+    k.bk_id += bs;
   k.bk_st += bs;
   k.hdr += c0;
   k.agents += c0 * A;
@@ -2143,21 +2151,34 @@ mlob_status mlob_venv_read_book(mlob_venv* v, uint64_t env, int side, mlob_resti
     v->set_device();
     cuda_check(cudaMemcpyAsync(p.data(), v->d_bk_p + base, m * 4, cudaMemcpyDeviceToHost, v->stream), "D2H");
     cuda_check(cudaMemcpyAsync(q.data(), v->d_bk_q + base, m * 4, cudaMemcpyDeviceToHost, v->stream), "D2H");
-    cuda_check(cudaMemcpyAsync(id.data(), v->d_bk_id + base, m * 8, cudaMemcpyDeviceToHost, v->stream), "D2H");
+    if (v->spl > 8)  // deep books keep the low id word as a u32 array in the id buffer
+      cuda_check(cudaMemcpyAsync(id.data(), reinterpret_cast<const uint32_t*>(v->d_bk_id) + base, m * 4,
+                                 cudaMemcpyDeviceToHost, v->stream), "D2H");
+    else
+      cuda_check(cudaMemcpyAsync(id.data(), v->d_bk_id + base, m * 8, cudaMemcpyDeviceToHost, v->stream), "D2H");
     cuda_check(cudaMemcpyAsync(st.data(), v->d_bk_st + base, m * 4, cudaMemcpyDeviceToHost, v->stream), "D2H");
     EnvHdr h;
     cuda_check(cudaMemcpyAsync(&h, v->d_hdr + env, sizeof h, cudaMemcpyDeviceToHost, v->stream), "D2H");
     v->check_device_errors();
     std::vector<mlob_resting_order> o;
+    const bool deep = v->spl > 8;  // 4-word slots: qt = q << 8 | trader, lo, hs = id_hi << 20 | seq
+    const uint32_t* lo = reinterpret_cast<const uint32_t*>(id.data());
     for (uint64_t i = 0; i < std::min<uint64_t>(m, h.hwm[side]); ++i) {
-      if (q[i] <= 0) continue;
+      const int64_t qi = deep ? static_cast<int64_t>(static_cast<uint32_t>(q[i]) >> 8) : q[i];
+      if (qi <= 0) continue;
       mlob_resting_order r;
       std::memset(&r, 0, sizeof r);
       r.price = p[i];
-      r.quantity = q[i];
-      r.order_id = (static_cast<uint64_t>(id[i].y) << 32) | id[i].x;
-      r.arrival_seq = st[i] >> 8;
-      r.trader_id = static_cast<int32_t>(st[i] & 0xffu);
+      r.quantity = qi;
+      if (deep) {
+        r.order_id = (static_cast<uint64_t>(st[i] >> 20) << 32) | lo[i];
+        r.arrival_seq = st[i] & 0xfffffu;
+        r.trader_id = static_cast<int32_t>(static_cast<uint32_t>(q[i]) & 0xffu);
+      } else {
+        r.order_id = (static_cast<uint64_t>(id[i].y) << 32) | id[i].x;
+        r.arrival_seq = st[i] >> 8;
+        r.trader_id = static_cast<int32_t>(st[i] & 0xffu);
+      }
       o.push_back(r);
     }
     // storage order of lob::OrderBook (book.hpp:134-143): worst-to-best, newer first at a price

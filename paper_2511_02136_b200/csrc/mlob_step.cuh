@@ -29,17 +29,15 @@
 
 #include "mlob_dev.h"
 
-#ifndef MLOB_ROUNDS  // phase-sync step kernel: one block per SM looping over env rounds
-#define MLOB_ROUNDS 1
+#ifndef MLOB_EXPECT  // branch-probability hints on the rare paths of the message loop (+0.7 % on C)
+#define MLOB_EXPECT 1
 #endif
-#ifndef MLOB_PERSIST  // persistent warps + ticketed envs: measured slower (r1 notes)
-#define MLOB_PERSIST 0
-#endif
-#if MLOB_PERSIST
-#error "ticketed mode needs KParams::ticket zeroed before every step launch (mlob_runtime.cu)"
-#endif
-#ifndef MLOB_PREFETCH  // L2 prefetch of the next env's header / agents / book rows (measured -1% with rounds)
-#define MLOB_PREFETCH 0
+#if MLOB_EXPECT
+#define MLOB_LIKELY(x) __builtin_expect(!!(x), 1)
+#define MLOB_UNLIKELY(x) __builtin_expect(!!(x), 0)
+#else
+#define MLOB_LIKELY(x) (x)
+#define MLOB_UNLIKELY(x) (x)
 #endif
 
 namespace mlob {
@@ -207,13 +205,17 @@ struct RegSide {
 // plain indexed accesses.
 template <int SPL>
 struct SmemSide {
-  // the HBM book layout of one side (KParams::bk_*): p[SPL*32], q[SPL*32],
-  // id[SPL*32] as uint2, st[SPL*32] — so whole arrays move with bulk copies
+  // Four words per slot, in the HBM layout of one side of a deep book (so
+  // whole arrays move with bulk copies): p[SPL*32]; qt = qty << 8 | trader;
+  // lo = order id bits 0..31; hs = order id bits 32..43 << 20 | arrival_seq.
+  // Four words instead of five is what fits a sixth 36.5 KB warp per SM at
+  // C = 1000.  Limits (loud errors, kErrDeepRange): qty < 2^24, order ids
+  // < 2^44, arrival_seq < 2^20 per episode.
   uint32_t* base_;
   int32_t* p_;
-  int32_t* q_;
-  uint2* id_;
-  uint32_t* st_;
+  uint32_t* qt_;
+  uint32_t* lo_;
+  uint32_t* hs_;
   uint32_t occ;  // this lane's occupied rows (bit k = row k), kept by every mutator
   // this lane's worst live price (bids: lowest, asks: highest; identity when
   // none), widened on inserts; a removal at that price marks it stale
@@ -228,97 +230,54 @@ struct SmemSide {
   __device__ __forceinline__ uint32_t free_mask() const {
     return ~occ & (SPL >= 32 ? 0xffffffffu : ((1u << SPL) - 1u));
   }
-#ifndef MLOB_HWM_OCC  // shared-memory books: high-water mark from the occupancy masks
-#define MLOB_HWM_OCC 1
-#endif
-#ifndef MLOB_LW_UNROLL
-#define MLOB_LW_UNROLL 1
-#endif
-#ifndef MLOB_ACT_ROWS  // shared-memory books: active-order rebuild visits only agent rows
-#define MLOB_ACT_ROWS 1
-#endif
-#ifndef MLOB_LW_OCC  // worst-price rescans read only the price row, gated by the occupancy mask
-#define MLOB_LW_OCC 1
-#endif
-#ifndef MLOB_LW_CNT  // experiment: count the lane's orders at its worst price (measured -30 % on D)
-#define MLOB_LW_CNT 0
-#endif
-  int lw_n;  // this lane's live orders at price lw (meaningful while !lw_stale)
-  __device__ __forceinline__ void lw_take(bool live, int32_t p) {
-    const bool w = live && (side_ ? p > lw : p < lw);  // strictly worse than lw
-    lw_n = w ? 1 : lw_n + ((live && p == lw) ? 1 : 0);
-    lw = w ? p : lw;
-  }
+  // this lane's worst live price, rescanned from the price row under the
+  // occupancy mask (a per-lane count at the worst price measured -30 % on D)
   __device__ __forceinline__ void refresh_lw() {
     lw = side_ ? INT_MIN : INT_MAX;
-    lw_n = 0;
-#if MLOB_LW_UNROLL
 #pragma unroll
-#endif
     for (int k = 0; k < SPL; ++k) {
-#if MLOB_LW_OCC
       const int32_t p = p_[k * 32];
-#if MLOB_LW_CNT
-      lw_take((occ >> k) & 1u, p);
-#else
       lw = (occ >> k) & 1u ? worse(lw, p) : lw;
-#endif
-#else
-      if (q_[k * 32] > 0) lw = worse(lw, p_[k * 32]);
-#endif
     }
     lw_stale = 0;
   }
+  // occupancy and worst price together, one pass (book load)
   __device__ __forceinline__ void recompute_occ() {
     occ = 0;
-#if MLOB_LW_OCC  // one pass: occupancy and worst price together
     lw = side_ ? INT_MIN : INT_MAX;
-    lw_n = 0;
-#if MLOB_LW_UNROLL
 #pragma unroll
-#endif
     for (int k = 0; k < SPL; ++k) {
-      const int32_t q = q_[k * 32], p = p_[k * 32];
+      const int32_t q = Q(k), p = p_[k * 32];
       occ |= (q > 0 ? 1u : 0u) << k;
-#if MLOB_LW_CNT
-      lw_take(q > 0, p);
-#else
       lw = q > 0 ? worse(lw, p) : lw;
-#endif
     }
     lw_stale = 0;
-#else
-    for (int k = 0; k < SPL; ++k) occ |= (q_[k * 32] > 0 ? 1u : 0u) << k;
-    refresh_lw();
-#endif
   }
   __device__ __forceinline__ int32_t P(int k) const { return p_[k * 32]; }
-  __device__ __forceinline__ int32_t Q(int k) const { return q_[k * 32]; }
-  __device__ __forceinline__ uint32_t LO(int k) const { return id_[k * 32].x; }
-  __device__ __forceinline__ uint32_t HI(int k) const { return id_[k * 32].y; }
-  __device__ __forceinline__ uint32_t ST(int k) const { return st_[k * 32]; }
+  __device__ __forceinline__ int32_t Q(int k) const { return static_cast<int32_t>(qt_[k * 32] >> 8); }
+  __device__ __forceinline__ uint32_t LO(int k) const { return lo_[k * 32]; }
+  __device__ __forceinline__ uint32_t HI(int k) const { return hs_[k * 32] >> 20; }
+  // the reference record's arrival word seq << 8 | trader (ordered like seq)
+  __device__ __forceinline__ uint32_t ST(int k) const {
+    return ((hs_[k * 32] & 0xfffffu) << 8) | (qt_[k * 32] & 0xffu);
+  }
   __device__ __forceinline__ void put(int k, int32_t p, int32_t q, uint32_t lo, uint32_t hi,
                                       uint32_t st) {
     p_[k * 32] = p;
-    q_[k * 32] = q;
-    id_[k * 32] = make_uint2(lo, hi);
-    st_[k * 32] = st;
+    qt_[k * 32] = (static_cast<uint32_t>(q) << 8) | (st & 0xffu);
+    lo_[k * 32] = lo;
+    hs_[k * 32] = (hi << 20) | ((st >> 8) & 0xfffffu);
     occ_set(k, q > 0);
-#if MLOB_LW_CNT
-    lw_take(q > 0, p);
-#else
     if (q > 0) lw = worse(lw, p);
-#endif
   }
   __device__ __forceinline__ void get_pq(int k, int32_t& p, int32_t& q) const {
     p = p_[k * 32];
-    q = q_[k * 32];
+    q = Q(k);
   }
   __device__ __forceinline__ void get_qid(int k, int32_t& q, uint32_t& lo, uint32_t& hi) const {
-    q = q_[k * 32];
-    const uint2 id = id_[k * 32];
-    lo = id.x;
-    hi = id.y;
+    q = Q(k);
+    lo = lo_[k * 32];
+    hi = hs_[k * 32] >> 20;
   }
   __device__ __forceinline__ void set(int k, bool pred, int32_t p, int32_t q, uint32_t lo,
                                       uint32_t hi, uint32_t st) {
@@ -329,32 +288,26 @@ struct SmemSide {
     set(k, pred, p, q, lo, hi, st);
   }
   __device__ __forceinline__ void setq(int k, bool pred, int32_t q) {
-    if (pred) q_[k * 32] = q;
+    if (pred) qt_[k * 32] = (static_cast<uint32_t>(q) << 8) | (qt_[k * 32] & 0xffu);
   }
   __device__ __forceinline__ void clear(int k, bool pred, int32_t empty_p) {
     if (pred) {
-#if MLOB_LW_CNT
-      if (p_[k * 32] == lw && --lw_n <= 0) lw_stale = 1;
-#else
       if (p_[k * 32] == lw) lw_stale = 1;
-#endif
       p_[k * 32] = empty_p;
-      q_[k * 32] = 0;
-      st_[k * 32] = kEmptySt;
+      qt_[k * 32] = 0;
       occ_set(k, false);
     }
   }
-  __device__ __forceinline__ void bind(uint32_t* base, int lane, int side) {  // 5 x SPL*32 words
+  __device__ __forceinline__ void bind(uint32_t* base, int lane, int side) {  // 4 x SPL*32 words
     side_ = side;
     lw = side ? INT_MIN : INT_MAX;
-    lw_n = 0;
     lw_stale = 1;
     occ = 0;
     base_ = base;
     p_ = reinterpret_cast<int32_t*>(base) + lane;
-    q_ = reinterpret_cast<int32_t*>(base + SPL * 32) + lane;
-    id_ = reinterpret_cast<uint2*>(base + 2 * SPL * 32) + lane;
-    st_ = base + 4 * SPL * 32 + lane;
+    qt_ = base + SPL * 32 + lane;
+    lo_ = base + 2 * SPL * 32 + lane;
+    hs_ = base + 3 * SPL * 32 + lane;
   }
 };
 
@@ -576,7 +529,7 @@ struct WarpEnv {
       : kp(p), cfg(c), sm(s), lane(ln), env(e) {
     if constexpr (SMEM) {
       bid.bind(book_smem, ln, 0);
-      ask.bind(book_smem + 5 * SPL * 32, ln, 1);
+      ask.bind(book_smem + 4 * SPL * 32, ln, 1);
     }
     err = 0;
     capacity_ = c.capacity;
@@ -618,7 +571,7 @@ struct WarpEnv {
   __device__ __forceinline__ int store_side() {
     SideT& d = sd<S>();
     int hwm = 0;
-    if constexpr (SMEM && MLOB_HWM_OCC) {  // from the occupancy masks: one redux + one ballot
+    if constexpr (SMEM) {  // from the occupancy masks: one redux + one ballot
       const uint32_t rows = __reduce_or_sync(FULLMASK, d.occ);
       if (rows) {
         const int k = 31 - __clz(rows);
@@ -639,8 +592,8 @@ struct WarpEnv {
         const uint32_t* b = d.base_;
         bulk_store(kp.bk_p + g, b, rows * kWarp * 4);
         bulk_store(kp.bk_q + g, b + SPL * kWarp, rows * kWarp * 4);
-        bulk_store(kp.bk_id + g, b + 2 * SPL * kWarp, rows * kWarp * 8);
-        bulk_store(kp.bk_st + g, b + 4 * SPL * kWarp, rows * kWarp * 4);
+        bulk_store(reinterpret_cast<uint32_t*>(kp.bk_id) + g, b + 2 * SPL * kWarp, rows * kWarp * 4);
+        bulk_store(kp.bk_st + g, b + 3 * SPL * kWarp, rows * kWarp * 4);
       }
     } else {
       MLOB_ROWS(k) {
@@ -711,7 +664,7 @@ struct WarpEnv {
       for (int k = rows0; k < SPL; ++k) bid.put(k, INT_MIN, 0, 0, 0, kEmptySt);
       for (int k = rows1; k < SPL; ++k) ask.put(k, INT_MAX, 0, 0, 0, kEmptySt);
       if (lane == 0) {
-        bar_arrive_tx(&sm.bar()[2], static_cast<uint32_t>(rows0 + rows1) * kWarp * 20u);
+        bar_arrive_tx(&sm.bar()[2], static_cast<uint32_t>(rows0 + rows1) * kWarp * 16u);
 #pragma unroll
         for (int S = 0; S < 2; ++S) {
           const uint32_t rows = static_cast<uint32_t>(S ? rows1 : rows0);
@@ -720,8 +673,9 @@ struct WarpEnv {
           uint32_t* b = S ? ask.base_ : bid.base_;
           bulk_load_tx(b, kp.bk_p + g, rows * kWarp * 4, &sm.bar()[2]);
           bulk_load_tx(b + SPL * kWarp, kp.bk_q + g, rows * kWarp * 4, &sm.bar()[2]);
-          bulk_load_tx(b + 2 * SPL * kWarp, kp.bk_id + g, rows * kWarp * 8, &sm.bar()[2]);
-          bulk_load_tx(b + 4 * SPL * kWarp, kp.bk_st + g, rows * kWarp * 4, &sm.bar()[2]);
+          bulk_load_tx(b + 2 * SPL * kWarp, reinterpret_cast<const uint32_t*>(kp.bk_id) + g, rows * kWarp * 4,
+                       &sm.bar()[2]);
+          bulk_load_tx(b + 3 * SPL * kWarp, kp.bk_st + g, rows * kWarp * 4, &sm.bar()[2]);
         }
       }
     }
@@ -1030,7 +984,7 @@ struct WarpEnv {
   // ---- message handlers (runtime side) -------------------------------------
   __device__ __forceinline__ void record_trade(int32_t price, int32_t qty, const MsgRef& m,
                                                uint32_t lo, uint32_t hi, uint32_t st, int aside) {
-    if (rec_trades() && lane == 0 && n_trades < kp.trade_cap) {
+    if (MLOB_UNLIKELY(rec_trades()) && lane == 0 && n_trades < kp.trade_cap) {
       mlob_trade t;
       t.price = price;
       t.quantity = qty;
@@ -1046,7 +1000,7 @@ struct WarpEnv {
     }
     ++n_trades;
     const uint32_t pt = st & 0xffu;
-    if (pt | static_cast<uint32_t>(m.trader)) {  // an agent may be involved: env.hpp:372-379 order
+    if (MLOB_UNLIKELY(pt | static_cast<uint32_t>(m.trader))) {  // an agent may be involved: env.hpp:372-379 order
       log_fill(price, qty, static_cast<int>(pt), 1 - aside);
       log_fill(price, qty, m.trader, aside);
     }
@@ -1059,7 +1013,7 @@ struct WarpEnv {
     if (trader <= 0 || trader > n_agents()) return;
     const uint32_t i = n_fills;
     FillEnt* dst;
-    if (i < static_cast<uint32_t>(kFillInline)) {
+    if (MLOB_LIKELY(i < static_cast<uint32_t>(kFillInline))) {
       dst = kp.fills + env * kFillInline + i;
     } else {
       const uint32_t k = i - kFillInline, off = k % (kFillChunk - 1) + 1;
@@ -1173,6 +1127,7 @@ struct WarpEnv {
       else
         insert_t<0>(m.price, rem, ilo, ihi, st);
     } else {
+      if (rem >= (1 << 24) || ihi >= (1u << 12) || seq >= (1u << 20)) err |= kErrDeepRange;  // 4-word slot
       int pk, pl;
       if (s)
         free_slot_t<1>(pk, pl);
@@ -1205,7 +1160,7 @@ struct WarpEnv {
       uint32_t st = 0;
       const uint32_t tot = s ? id_gather_t<1>(lo, hi, p, q, st) : id_gather_t<0>(lo, hi, p, q, st);
       if (tot == 0) return false;
-      if (tot == 1) {
+      if (MLOB_LIKELY(tot == 1)) {
         const int32_t nq = remove ? 0 : q - min(q, m.qty);
         if (nq == 0) {
           if (s) {

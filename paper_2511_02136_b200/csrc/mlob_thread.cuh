@@ -482,24 +482,38 @@ struct ThreadEnv {
   // Writes the new episode's book straight into the HBM layout, one synthetic
   // order per L2 level, and the L2 summary of that book.
   __device__ void init_side(int S, const DevLevel* lv, uint32_t n, uint64_t id_base, uint32_t seq_base, int spl,
-                            L2Lvl* l2out, int32_t& nl, int64_t& sumq, int64_t& topq) const {
+                            L2Lvl* l2out, int32_t& nl, int64_t& sumq, int64_t& topq) {
     const int32_t empty_p = S == 0 ? INT_MIN : INT_MAX;
     const uint32_t rows = (n + kWarp - 1) / kWarp;
     MLOB_CHECK(rows <= static_cast<uint32_t>(spl));
     const size_t base = (env * 2 + static_cast<uint64_t>(S)) * spl * kWarp;
-    for (uint32_t i = 0; i < rows * kWarp; ++i) {
-      const size_t x = base + i;
-      if (i < n) {
+    if (spl > 8) {  // deep book: 4-word slots (SmemSide): p, q << 8 | trader, id lo, id hi << 20 | seq
+      uint32_t* lo = reinterpret_cast<uint32_t*>(kp.bk_id);
+      for (uint32_t i = 0; i < rows * kWarp; ++i) {
+        const size_t x = base + i;
         const uint64_t id = id_base + i;
-        kp.bk_p[x] = lv[i].price;
-        kp.bk_q[x] = lv[i].qty;
-        kp.bk_id[x] = make_uint2(static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32));
-        kp.bk_st[x] = (seq_base + i) << 8;
-      } else {
-        kp.bk_p[x] = empty_p;
-        kp.bk_q[x] = 0;
-        kp.bk_id[x] = make_uint2(0u, 0u);
-        kp.bk_st[x] = kEmptySt;
+        const bool live = i < n;
+        if (live && (lv[i].qty >= (1 << 24) || (id >> 44) != 0)) err |= kErrDeepRange;
+        kp.bk_p[x] = live ? lv[i].price : empty_p;
+        kp.bk_q[x] = live ? static_cast<int32_t>(static_cast<uint32_t>(lv[i].qty) << 8) : 0;
+        lo[x] = live ? static_cast<uint32_t>(id) : 0u;
+        kp.bk_st[x] = live ? (static_cast<uint32_t>(id >> 32) << 20) | (seq_base + i) : kEmptySt;
+      }
+    } else {
+      for (uint32_t i = 0; i < rows * kWarp; ++i) {
+        const size_t x = base + i;
+        if (i < n) {
+          const uint64_t id = id_base + i;
+          kp.bk_p[x] = lv[i].price;
+          kp.bk_q[x] = lv[i].qty;
+          kp.bk_id[x] = make_uint2(static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32));
+          kp.bk_st[x] = (seq_base + i) << 8;
+        } else {
+          kp.bk_p[x] = empty_p;
+          kp.bk_q[x] = 0;
+          kp.bk_id[x] = make_uint2(0u, 0u);
+          kp.bk_st[x] = kEmptySt;
+        }
       }
     }
     // aggregate_levels (book.hpp:209-220) over the new book, best-first:

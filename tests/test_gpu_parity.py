@@ -657,3 +657,41 @@ def test_bench_workload_sampled_envs_match_oracle(orc, workload):
                 o.reset((e + cursor * n) % n_ep)
                 cursor += 1
         compare_env_state(g.view(e), o, trades=False)  # the bench runs without the trade log
+
+
+@pytest.mark.parametrize("scenario", ["mm_fixed_exec", "deep_evict"])
+def test_step_io_chunked_matches_oracle(orc, scenario, monkeypatch):
+    """mlob_venv_step_io split into env chunks on two streams (every per-env
+    hand-off buffer offset by the chunk, the fill-overflow pool shared out per
+    chunk), for a register book and a 4-word-slot deep book, across an
+    episode boundary: every env equals its oracle replay (MarketVecEnv
+    auto-reset, rollout.hpp:290-318)."""
+    monkeypatch.setenv("MLOB_IO_CHUNKS", "3")
+    cfg, synth_kw, _ = scenario_configs()[scenario]
+    dev = dev_store(synth_kw)
+    ost = small_store(orc, synth_kw)
+    n = 9
+    g = MarketVecEnv(dev, cfg, seed=4, n_envs=n)
+    g.reset_all()
+    refs = [OEnv(orc, ost, cfg, 4, e) for e in range(n)]
+    n_ep = refs[0].n_episodes
+    for e, r in enumerate(refs):
+        r.reset(e % n_ep)
+    cursor = [1] * n
+    arities = [abi.action_arity(cfg.specs[t]) for t in abi.flat_specs(cfg)]
+    rew = np.zeros((n, g.n_agents))
+    dn = np.zeros((n, g.n_agents), dtype=np.uint8)
+    for t in range(cfg.steps_per_episode + 3):
+        acts = np.array([kat.bench_actions(0, e, t, arities) for e in range(n)], dtype=np.int32)
+        g.step_io(actions=acts, rewards=rew, dones=dn)
+        for e, r in enumerate(refs):
+            r.step_ids(list(acts[e]))
+            for a in range(g.n_agents):
+                assert rew[e, a] == r.reward(a) and dn[e, a] == r.done(a)
+            if r.scalars().terminal:  # the device env has auto-reset already
+                r.reset((e + cursor[e] * n) % n_ep)
+                cursor[e] += 1
+                for side in (0, 1):
+                    assert g.view(e).book(side).tobytes() == r.book(side).tobytes()
+            else:
+                compare_env_state(g.view(e), r, trades=False)
