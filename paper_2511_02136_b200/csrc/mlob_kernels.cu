@@ -40,6 +40,8 @@ __host__ __device__ inline size_t warp_smem_bytes(const DevCfg& c) {
   b += 32;  // scalars (WarpSmem::scal: mid anchor / segment base, Σmid)
   b += static_cast<size_t>(2 * c.obs_depth) * sizeof(L2Lvl);
   b = (b + 15) / 16 * 16;
+  if (MLOB_PREFIX_WALK && !smem_book(c.capacity))  // register books: the price-level walk's scratch
+    b += static_cast<size_t>(spl_of(c.capacity)) * kWarp * sizeof(WalkEnt);
   if (smem_book(c.capacity)) b += book_smem_bytes(c.capacity);
   return (b + 127) / 128 * 128;
 }
@@ -65,6 +67,8 @@ __device__ void carve_block(const DevCfg& c) {
   o.scal = p;
   p += 32;
   o.l2 = p;
+  p += static_cast<uint32_t>(2 * c.obs_depth * sizeof(L2Lvl));
+  o.walk = (p + 15) / 16 * 16;
 }
 
 // deep-book smem region of a warp (after the WarpSmem carve-out)

@@ -29,6 +29,15 @@
 
 #include "mlob_dev.h"
 
+// Crossing orders walk a whole price level by a warp prefix sum over the
+// resting quantities (walk_level_t).  Bit-exact (40 GPU parity tests) but
+// 2.5x slower on C / E than one fill per iteration (2.07e9 vs 5.12e9 on C):
+// a crossing order fills ~2.4 orders, so the compaction, rank and update
+// passes cost more than they save, and the extra code pushes the 72-register
+// message loop into spills (470 B vs 288 B).  Off by default; DESIGN.md §4.
+#ifndef MLOB_PREFIX_WALK
+#define MLOB_PREFIX_WALK 0
+#endif
 #ifndef MLOB_EXPECT  // branch-probability hints on the rare paths of the message loop (+0.7 % on C)
 #define MLOB_EXPECT 1
 #endif
@@ -339,7 +348,14 @@ static_assert(sizeof(ActTmp) <= sizeof(DevMsg), "ActTmp reuses the agent-message
 // region pointers held in registers across the message loop forced spills
 // at the 80-register cap.
 struct SmemOff {
-  uint32_t chunk0, chunk1, bar, amsg, act, nact, scal, l2;
+  uint32_t chunk0, chunk1, bar, amsg, act, nact, scal, l2, walk, _pad[3];
+};
+// One resting order of the price level being walked (walk_level_t).
+struct WalkEnt {
+  uint32_t st;
+  int32_t q;
+  int32_t fill;
+  int32_t order;  // the entry filled at this priority rank
 };
 __shared__ __align__(16) SmemOff g_smem_off;  // written once per block by carve_block()
 struct WarpSmem {
@@ -352,6 +368,7 @@ struct WarpSmem {
   __device__ __forceinline__ int32_t* nact() const { return reinterpret_cast<int32_t*>(base + g_smem_off.nact); }
   __device__ __forceinline__ int32_t* scal() const { return reinterpret_cast<int32_t*>(base + g_smem_off.scal); }
   __device__ __forceinline__ L2Lvl* l2() const { return reinterpret_cast<L2Lvl*>(base + g_smem_off.l2); }
+  __device__ __forceinline__ WalkEnt* walk() const { return reinterpret_cast<WalkEnt*>(base + g_smem_off.walk); }
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -981,6 +998,81 @@ struct WarpEnv {
     return tot;
   }
 
+  // The order walk of process_new_limit (book.hpp:154-165) over one whole
+  // price level at once, by a warp prefix sum over the resting quantities in
+  // priority order: the level's orders are compacted into shared memory, each
+  // one's priority rank and the quantity resting ahead of it (Σ q of the
+  // orders with a smaller arrival word) give its fill min(q, max(0, rem −
+  // ahead)); the trades are then recorded in priority order and every slot
+  // of the level is updated in place.  Returns the remaining quantity.
+  template <int S>
+  __device__ __forceinline__ int32_t walk_level_t(int32_t bp, int32_t rem, const MsgRef& m, int aside) {
+    SideT& d = sd<S>();
+    WalkEnt* w = sm.walk();
+    const uint32_t lt = (1u << lane) - 1u;
+    int n = 0;
+    MLOB_ROWS(k) {
+      const bool at = d.P(k) == bp;
+      const uint32_t b = __ballot_sync(FULLMASK, at);
+      if (at) {
+        WalkEnt& e = w[n + __popc(b & lt)];
+        e.st = d.ST(k);
+        e.q = d.Q(k);
+      }
+      n += __popc(b);
+    }
+    __syncwarp();
+    for (int i = lane; i < n; i += kWarp) {
+      const WalkEnt e = w[i];
+      int64_t ahead = 0;
+      int rank = 0;
+      for (int j = 0; j < n; ++j) {
+        const WalkEnt f = w[j];
+        const bool before = f.st < e.st;
+        ahead += before ? f.q : 0;
+        rank += before ? 1 : 0;
+      }
+      const int64_t left = static_cast<int64_t>(rem) - ahead;
+      w[i].fill = left <= 0 ? 0 : static_cast<int32_t>(min(left, static_cast<int64_t>(e.q)));
+      w[rank].order = i;
+    }
+    __syncwarp();
+    // trades in priority order (env.hpp:226-229 attribution order)
+    int32_t total = 0;
+    for (int r = 0; r < n; ++r) {
+      const WalkEnt e = w[w[r].order];
+      if (e.fill == 0) break;
+      total += e.fill;
+      uint32_t idlo = 0, idhi = 0;
+      if (MLOB_UNLIKELY(rec_trades())) q_of_st_t<S>(e.st, true, idlo, idhi);
+      record_trade(bp, e.fill, m, idlo, idhi, e.st, aside);
+    }
+    // every slot of the level: quantity down by its fill, filled orders removed
+    int base = 0, cleared = 0;
+    MLOB_ROWS(k) {
+      const bool at = d.P(k) == bp;
+      const uint32_t b = __ballot_sync(FULLMASK, at);
+      int32_t nq = 1;
+      if (at) {
+        nq = d.Q(k) - w[base + __popc(b & lt)].fill;
+        if (nq == 0)
+          d.clear_row(k, true, empty_price<S>());
+        else
+          d.setq_row(k, true, nq);
+      }
+      cleared += __popc(__ballot_sync(FULLMASK, at && nq == 0));
+      base += __popc(b);
+    }
+    __syncwarp();  // the walk scratch is reused by the next level
+    if (cleared) {
+      moved = true;
+      int& live = S ? live1 : live0;
+      live -= cleared;
+      if (cleared == n && live > 0) (S ? best1 : best0) = side_best_t<S>();
+    }
+    return rem - total;
+  }
+
   // ---- message handlers (runtime side) -------------------------------------
   __device__ __forceinline__ void record_trade(int32_t price, int32_t qty, const MsgRef& m,
                                                uint32_t lo, uint32_t hi, uint32_t st, int aside) {
@@ -1056,6 +1148,10 @@ struct WarpEnv {
         const uint32_t gst = o ? oldest_st_t<1>(bp) : oldest_st_t<0>(bp);
         uint32_t idlo = 0, idhi = 0;
         const int32_t q = o ? q_of_st_t<1>(gst, pass_ids, idlo, idhi) : q_of_st_t<0>(gst, pass_ids, idlo, idhi);
+        if (MLOB_PREFIX_WALK && q < rem) {  // the order walk goes past the level's oldest order
+          rem = o ? walk_level_t<1>(bp, rem, m, s) : walk_level_t<0>(bp, rem, m, s);
+          continue;
+        }
         const int32_t fill = min(rem, q);
         rem -= fill;
         if (fill == q) {
