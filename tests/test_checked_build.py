@@ -1,6 +1,8 @@
 """The checked build (libmlob_checked.so = the product sources with
 -DMLOB_CHECKS=1: device-side bounds and invariant assertions on the hand-off
-buffers, book rows, fill log and the mbarrier waits, trapping on failure)
+buffers, book rows, fill log and the mbarrier waits, trapping on failure;
+and -DMLOB_PREFIX_WALK=1: crossing orders walk each price level by a warp
+prefix sum over the resting quantities, mlob_step.cuh walk_level_t)
 runs a register-book and a shared-memory-book workload — act / book /
 outcome / reset / stats kernels, TMA bulk copies, evictions, auto-reset —
 without a trap, and produces outputs bit-identical to the product library.
