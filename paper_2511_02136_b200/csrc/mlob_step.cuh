@@ -38,14 +38,6 @@
 #ifndef MLOB_PREFIX_WALK
 #define MLOB_PREFIX_WALK 0
 #endif
-#ifndef MLOB_VOTE_BRANCH  // warp-uniform message-loop branches via a vote (uniform predicate, no BSSY)
-#define MLOB_VOTE_BRANCH 0
-#endif
-#if MLOB_VOTE_BRANCH
-#define MLOB_UNI(c) __any_sync(0xffffffffu, (c))
-#else
-#define MLOB_UNI(c) (c)
-#endif
 #ifndef MLOB_EXPECT  // branch-probability hints on the rare paths of the message loop (+0.7 % on C)
 #define MLOB_EXPECT 1
 #endif
@@ -1151,7 +1143,7 @@ struct WarpEnv {
     while (rem > 0) {
       const int lo_ = o ? live1 : live0;
       const int32_t bp = o ? best1 : best0;
-      if (MLOB_UNI(lo_ == 0 || (bp ^ flip) > kprice)) break;
+      if (lo_ == 0 || (bp ^ flip) > kprice) break;
       if constexpr (!SMEM && MLOB_ST_MATCH) {
         const uint32_t gst = o ? oldest_st_t<1>(bp) : oldest_st_t<0>(bp);
         uint32_t idlo = 0, idhi = 0;
@@ -1162,7 +1154,7 @@ struct WarpEnv {
         }
         const int32_t fill = min(rem, q);
         rem -= fill;
-        if (MLOB_UNI(fill == q)) {
+        if (fill == q) {
           moved = true;
           if (o) {
             clear_st_t<1>(gst);
@@ -1213,7 +1205,7 @@ struct WarpEnv {
     }
     if (rem <= 0) return;
     // rest_order
-    if (MLOB_UNI((s ? live1 : live0) == capacity())) {
+    if ((s ? live1 : live0) == capacity()) {
       const bool ev = s ? evict_t<1>(m.price) : evict_t<0>(m.price);
       if (!ev) return;  // newcomer dropped: no sequence number consumed
       moved = true;
@@ -1263,10 +1255,10 @@ struct WarpEnv {
       int32_t p = 0, q = 0;
       uint32_t st = 0;
       const uint32_t tot = s ? id_gather_t<1>(lo, hi, p, q, st) : id_gather_t<0>(lo, hi, p, q, st);
-      if (MLOB_UNI(tot == 0)) return false;
+      if (tot == 0) return false;
       if (MLOB_LIKELY(tot == 1)) {
         const int32_t nq = remove ? 0 : q - min(q, m.qty);
-        if (MLOB_UNI(nq == 0)) {
+        if (nq == 0) {
           if (s) {
             clear_st_t<1>(st);
             if (--live1 > 0 && p == best1) best1 = side_best_t<1>();
@@ -1326,7 +1318,7 @@ struct WarpEnv {
   __device__ __forceinline__ void refresh_mid(int i) {
     const int64_t b0 = best0, b1 = best1;
     const int64_t nm = live0 > 0 ? (live1 > 0 ? b0 + b1 : 2 * b0) : (live1 > 0 ? 2 * b1 : mid_half);
-    if (MLOB_UNI(nm != mid_half)) {
+    if (nm != mid_half) {
       int32_t* sc = sm.scal();
       const int j = sc[3] + i;
       int64_t& ms = *reinterpret_cast<int64_t*>(sc + 4);
@@ -1340,14 +1332,14 @@ struct WarpEnv {
   // derived once after the loop: they only depend on the message count).
   // i: the message's index within its segment (see refresh_mid)
   __device__ __forceinline__ void run_message(const MsgRef& m, int i) {
-    if (MLOB_UNI(m.kind == MLOB_NEW_LIMIT)) {
-      if (MLOB_UNI(m.qty > 0)) {
+    if (m.kind == MLOB_NEW_LIMIT) {
+      if (m.qty > 0) {
         moved = false;
         new_limit(m);
-        if (MLOB_UNI(moved)) refresh_mid(i);
+        if (moved) refresh_mid(i);
       }
-    } else if (MLOB_UNI(m.kind <= MLOB_EXECUTE_VISIBLE)) {
-      if (MLOB_UNI(by_id(m, m.kind == MLOB_DELETE))) refresh_mid(i);
+    } else if (m.kind <= MLOB_EXECUTE_VISIBLE) {
+      if (by_id(m, m.kind == MLOB_DELETE)) refresh_mid(i);
     }
   }
 
