@@ -92,84 +92,61 @@ enum : uint64_t { kRngShuffle = 1, kRngTaskDir = 2, kRngBenchAction = 7, kRngEpi
 // Book side held in registers: SPL rows of 32 slots (lane-major).
 // Empty slot: q == 0, p == side sentinel (bid INT_MIN, ask INT_MAX), st == ~0.
 // st = arrival_seq << 8 | trader_id, so a u32 min over st is a min over seq.
+// MLOB_IDS_SMEM: the order ids (touched only by id matches, inserts, trade
+// records and the book store) live in shared memory, row k of this lane at
+// ids_[k * 32], which takes 4·SPL registers off the message loop (spills
+// 288 -> 76 B) but costs the id scans their shared-memory loads: measured
+// -2.5 % on C at 28 x 72, -7 % at 32 x 64, -9 % at 24 x 80.  Off.
+#ifndef MLOB_IDS_SMEM
+#define MLOB_IDS_SMEM 0
+#endif
 template <int SPL>
 struct RegSide {
   int32_t p_[SPL], q_[SPL];
-  uint32_t lo_[SPL], hi_[SPL], st_[SPL];
-  __device__ __forceinline__ int32_t P(int k) const { return p_[k]; }
-  __device__ __forceinline__ int32_t Q(int k) const { return q_[k]; }
+  uint32_t st_[SPL];
+#if MLOB_IDS_SMEM
+  uint2* ids_;
+  __device__ __forceinline__ uint32_t LO(int k) const { return ids_[k * 32].x; }
+  __device__ __forceinline__ uint32_t HI(int k) const { return ids_[k * 32].y; }
+  __device__ __forceinline__ uint2 ID(int k) const { return ids_[k * 32]; }
+  __device__ __forceinline__ void put_id(int k, uint32_t lo, uint32_t hi) { ids_[k * 32] = make_uint2(lo, hi); }
+#else
+  uint32_t lo_[SPL], hi_[SPL];
   __device__ __forceinline__ uint32_t LO(int k) const { return lo_[k]; }
   __device__ __forceinline__ uint32_t HI(int k) const { return hi_[k]; }
+  __device__ __forceinline__ uint2 ID(int k) const { return make_uint2(lo_[k], hi_[k]); }
+  __device__ __forceinline__ void put_id(int k, uint32_t lo, uint32_t hi) {
+    lo_[k] = lo;
+    hi_[k] = hi;
+  }
+#endif
+  __device__ __forceinline__ int32_t P(int k) const { return p_[k]; }
+  __device__ __forceinline__ int32_t Q(int k) const { return q_[k]; }
   __device__ __forceinline__ uint32_t ST(int k) const { return st_[k]; }
   __device__ __forceinline__ void put(int k, int32_t p, int32_t q, uint32_t lo, uint32_t hi,
                                       uint32_t st) {
     p_[k] = p;
     q_[k] = q;
-    lo_[k] = lo;
-    hi_[k] = hi;
+    put_id(k, lo, hi);
     st_[k] = st;
   }
-  // dynamic-index access through select chains (no local memory)
-  __device__ __forceinline__ void get_pq(int k, int32_t& p, int32_t& q) const {
-    p = p_[0];
-    q = q_[0];
-#pragma unroll
-    for (int kk = 1; kk < SPL; ++kk)
-      if (k == kk) {
-        p = p_[kk];
-        q = q_[kk];
-      }
-  }
-  __device__ __forceinline__ void get_qid(int k, int32_t& q, uint32_t& lo, uint32_t& hi) const {
-    q = q_[0];
-    lo = lo_[0];
-    hi = hi_[0];
-#pragma unroll
-    for (int kk = 1; kk < SPL; ++kk)
-      if (k == kk) {
-        q = q_[kk];
-        lo = lo_[kk];
-        hi = hi_[kk];
-      }
-  }
-  __device__ __forceinline__ void set(int k, bool pred, int32_t p, int32_t q, uint32_t lo,
-                                      uint32_t hi, uint32_t st) {
-#pragma unroll
-    for (int kk = 0; kk < SPL; ++kk)
-      if (pred && k == kk) put(kk, p, q, lo, hi, st);
-  }
-  __device__ __forceinline__ void setq(int k, bool pred, int32_t q) {
-#pragma unroll
-    for (int kk = 0; kk < SPL; ++kk)
-      if (pred && k == kk) q_[kk] = q;
-  }
-  // insert at a warp-uniform row: uniform branch + predicated writes
-  __device__ __forceinline__ void set_u(int k, bool pred, int32_t p, int32_t q, uint32_t lo,
-                                        uint32_t hi, uint32_t st) {
-#pragma unroll
-    for (int kk = 0; kk < SPL; ++kk) {
-      if (k == kk) {
-        if (pred) put(kk, p, q, lo, hi, st);
-      }
-    }
-  }
-  __device__ __forceinline__ void clear(int k, bool pred, int32_t empty_p) {
-#pragma unroll
-    for (int kk = 0; kk < SPL; ++kk)
-      if (pred && k == kk) {
-        p_[kk] = empty_p;
-        q_[kk] = 0;
-        st_[kk] = kEmptySt;
-      }
-  }  // compile-time row K, runtime predicate.  The asm text differs per row
+  // compile-time row K, runtime predicate.  The asm text differs per row
   // (the "row K" comment), so LLVM cannot merge the per-row branches of
   // insert_t into one runtime-indexed write (that demotes the book to local
   // memory).
+#if MLOB_IDS_SMEM
+#define MLOB_PUT_IF(K)                                                                          \
+  asm volatile("{\n.reg .pred pp; // row " #K "\nsetp.ne.b32 pp, %3, 0;\n@pp mov.b32 %0, %4;\n"    \
+               "@pp mov.b32 %1, %5;\n@pp mov.b32 %2, %6;\n}"                                     \
+               : "+r"(p_[K]), "+r"(q_[K]), "+r"(st_[K])                                          \
+               : "r"(static_cast<uint32_t>(pred)), "r"(p), "r"(q), "r"(st))
+#else
 #define MLOB_PUT_IF(K)                                                                          \
   asm volatile("{\n.reg .pred pp; // row " #K "\nsetp.ne.b32 pp, %5, 0;\n@pp mov.b32 %0, %6;\n"    \
                "@pp mov.b32 %1, %7;\n@pp mov.b32 %2, %8;\n@pp mov.b32 %3, %9;\n@pp mov.b32 %4, %10;\n}" \
                : "+r"(p_[K]), "+r"(q_[K]), "+r"(lo_[K]), "+r"(hi_[K]), "+r"(st_[K])                 \
                : "r"(static_cast<uint32_t>(pred)), "r"(p), "r"(q), "r"(lo), "r"(hi), "r"(st))
+#endif
   template <int K>
   __device__ __forceinline__ void put_if(bool pred, int32_t p, int32_t q, uint32_t lo, uint32_t hi, uint32_t st) {
     static_assert(K < SPL && K < 8, "row");
@@ -181,6 +158,9 @@ struct RegSide {
     else if constexpr (K == 5) MLOB_PUT_IF(5);
     else if constexpr (K == 6) MLOB_PUT_IF(6);
     else MLOB_PUT_IF(7);
+#if MLOB_IDS_SMEM
+    if (pred) ids_[K * 32] = make_uint2(lo, hi);
+#endif
   }
 #undef MLOB_PUT_IF
   // first row K.. with a free lane (ballots b), warp-uniform branches
@@ -348,7 +328,7 @@ static_assert(sizeof(ActTmp) <= sizeof(DevMsg), "ActTmp reuses the agent-message
 // region pointers held in registers across the message loop forced spills
 // at the 80-register cap.
 struct SmemOff {
-  uint32_t chunk0, chunk1, bar, amsg, act, nact, scal, l2, walk, _pad[3];
+  uint32_t chunk0, chunk1, bar, amsg, act, nact, scal, l2, walk, ids, _pad[2];
 };
 // One resting order of the price level being walked (walk_level_t).
 struct WalkEnt {
@@ -369,6 +349,8 @@ struct WarpSmem {
   __device__ __forceinline__ int32_t* scal() const { return reinterpret_cast<int32_t*>(base + g_smem_off.scal); }
   __device__ __forceinline__ L2Lvl* l2() const { return reinterpret_cast<L2Lvl*>(base + g_smem_off.l2); }
   __device__ __forceinline__ WalkEnt* walk() const { return reinterpret_cast<WalkEnt*>(base + g_smem_off.walk); }
+  // register books with MLOB_IDS_SMEM: order ids [side][row * 32 + lane]
+  __device__ __forceinline__ uint2* ids() const { return reinterpret_cast<uint2*>(base + g_smem_off.ids); }
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -548,6 +530,12 @@ struct WarpEnv {
       bid.bind(book_smem, ln, 0);
       ask.bind(book_smem + 4 * SPL * 32, ln, 1);
     }
+#if MLOB_IDS_SMEM
+    if constexpr (!SMEM) {
+      bid.ids_ = s.ids() + ln;
+      ask.ids_ = s.ids() + SPL * kWarp + ln;
+    }
+#endif
     err = 0;
     capacity_ = c.capacity;
     rec_trades_ = (p.flags & MLOB_VENV_RECORD_TRADES) != 0;
@@ -618,7 +606,10 @@ struct WarpEnv {
           const size_t i = row_index(S, k);
           kp.bk_p[i] = d.P(k);
           kp.bk_q[i] = d.Q(k);
-          kp.bk_id[i] = make_uint2(d.LO(k), d.HI(k));
+          if constexpr (SMEM)
+            kp.bk_id[i] = make_uint2(d.LO(k), d.HI(k));
+          else
+            kp.bk_id[i] = d.ID(k);
           kp.bk_st[i] = d.ST(k);
         }
       }
@@ -889,12 +880,16 @@ struct WarpEnv {
     const int32_t worst = S == 0 ? __reduce_min_sync(FULLMASK, lw) : __reduce_max_sync(FULLMASK, lw);
     const bool better = S == 0 ? price > worst : price < worst;
     if (!better) return false;
-    uint32_t m;
-    int lk;
-    scan_oldest_t<S>(worst, m, lk);
-    const uint32_t g = __reduce_min_sync(FULLMASK, m);
-    const int owner = __ffs(__ballot_sync(FULLMASK, m == g)) - 1;
-    d.clear(lk, lane == owner, empty_price<S>());
+    if constexpr (SMEM) {
+      uint32_t m;
+      int lk;
+      scan_oldest_t<S>(worst, m, lk);
+      const uint32_t g = __reduce_min_sync(FULLMASK, m);
+      const int owner = __ffs(__ballot_sync(FULLMASK, m == g)) - 1;
+      d.clear(lk, lane == owner, empty_price<S>());
+    } else {  // register book: the oldest at the worst price by its arrival word
+      clear_st_t<S>(oldest_st_t<S>(worst));
+    }
     return true;
   }
   // Duplicate live ids: the reference takes the first match in storage order
@@ -938,14 +933,15 @@ struct WarpEnv {
   template <int S>
   __device__ __forceinline__ int32_t q_of_st_t(uint32_t st, bool ids, uint32_t& lo, uint32_t& hi) {
     SideT& d = sd<S>();
-    uint32_t qv = 0, lv = 0, hv = 0;
-    MLOB_ROWS(k) {
-      const bool h = d.ST(k) == st;  // one-hot: a select chain, no OR
-      qv = h ? static_cast<uint32_t>(d.Q(k)) : qv;
-      lv = h ? d.LO(k) : lv;
-      hv = h ? d.HI(k) : hv;
-    }
-    if (ids) {
+    uint32_t qv = 0;
+    MLOB_ROWS(k) qv = d.ST(k) == st ? static_cast<uint32_t>(d.Q(k)) : qv;  // one-hot: a select chain
+    if (MLOB_UNLIKELY(ids)) {  // the passive order's id (trade log only)
+      uint32_t lv = 0, hv = 0;
+      MLOB_ROWS(k) {
+        const bool h = d.ST(k) == st;
+        lv = h ? d.LO(k) : lv;
+        hv = h ? d.HI(k) : hv;
+      }
       lo = __reduce_or_sync(FULLMASK, lv);
       hi = __reduce_or_sync(FULLMASK, hv);
     }
@@ -1073,6 +1069,25 @@ struct WarpEnv {
     return rem - total;
   }
 
+  // Duplicate live ids on a register book: the reference takes the first
+  // match in storage order (book.hpp:191-206; bids: lowest price then newest,
+  // asks: highest price then newest): the price by one reduction, then the
+  // newest arrival word at that price by another.  Returns its st; p = price.
+  template <int S>
+  __device__ __forceinline__ uint32_t dup_st_t(uint32_t lo, uint32_t hi, int32_t& p) {
+    SideT& d = sd<S>();
+    int32_t kp_ = S == 0 ? INT_MAX : INT_MIN;
+    MLOB_ROWS(k) {
+      if (d.Q(k) > 0 && d.LO(k) == lo && d.HI(k) == hi) kp_ = S == 0 ? min(kp_, d.P(k)) : max(kp_, d.P(k));
+    }
+    p = S == 0 ? __reduce_min_sync(FULLMASK, kp_) : __reduce_max_sync(FULLMASK, kp_);
+    uint32_t ms = 0;
+    MLOB_ROWS(k) {
+      if (d.Q(k) > 0 && d.LO(k) == lo && d.HI(k) == hi && d.P(k) == p) ms = max(ms, d.ST(k));
+    }
+    return __reduce_max_sync(FULLMASK, ms);
+  }
+
   // ---- message handlers (runtime side) -------------------------------------
   __device__ __forceinline__ void record_trade(int32_t price, int32_t qty, const MsgRef& m,
                                                uint32_t lo, uint32_t hi, uint32_t st, int aside) {
@@ -1169,39 +1184,39 @@ struct WarpEnv {
           setq_st_t<0>(gst, q - fill);
         }
         record_trade(bp, fill, m, idlo, idhi, gst, s);
-        continue;
-      }
-      uint32_t lm;
-      int lk;
-      if (o)
-        scan_oldest_t<1>(bp, lm, lk);
-      else
-        scan_oldest_t<0>(bp, lm, lk);
-      const uint32_t gst = __reduce_min_sync(FULLMASK, lm);
-      const int owner = __ffs(__ballot_sync(FULLMASK, lm == gst)) - 1;
-      int32_t q;
-      uint32_t idlo, idhi;
-      slot_get_qid(o, lk, q, idlo, idhi);
-      q = __shfl_sync(FULLMASK, q, owner);
-      if (pass_ids) {
-        idlo = __shfl_sync(FULLMASK, idlo, owner);
-        idhi = __shfl_sync(FULLMASK, idhi, owner);
-      }
-      const int32_t fill = min(rem, q);
-      const bool me = lane == owner;
-      rem -= fill;
-      if (fill == q) {
-        slot_clear(o, lk, me);
-        moved = true;
-        if (o) {
-          if (--live1 > 0) best1 = side_best_t<1>();
-        } else {
-          if (--live0 > 0) best0 = side_best_t<0>();
+      } else {  // shared-memory (deep) books
+        uint32_t lm;
+        int lk;
+        if (o)
+          scan_oldest_t<1>(bp, lm, lk);
+        else
+          scan_oldest_t<0>(bp, lm, lk);
+        const uint32_t gst = __reduce_min_sync(FULLMASK, lm);
+        const int owner = __ffs(__ballot_sync(FULLMASK, lm == gst)) - 1;
+        int32_t q;
+        uint32_t idlo, idhi;
+        slot_get_qid(o, lk, q, idlo, idhi);
+        q = __shfl_sync(FULLMASK, q, owner);
+        if (pass_ids) {
+          idlo = __shfl_sync(FULLMASK, idlo, owner);
+          idhi = __shfl_sync(FULLMASK, idhi, owner);
         }
-      } else {
-        slot_setq(o, lk, me, q - fill);
+        const int32_t fill = min(rem, q);
+        const bool me = lane == owner;
+        rem -= fill;
+        if (fill == q) {
+          slot_clear(o, lk, me);
+          moved = true;
+          if (o) {
+            if (--live1 > 0) best1 = side_best_t<1>();
+          } else {
+            if (--live0 > 0) best0 = side_best_t<0>();
+          }
+        } else {
+          slot_setq(o, lk, me, q - fill);
+        }
+        record_trade(bp, fill, m, idlo, idhi, gst, s);
       }
-      record_trade(bp, fill, m, idlo, idhi, gst, s);
     }
     if (rem <= 0) return;
     // rest_order
@@ -1256,53 +1271,56 @@ struct WarpEnv {
       uint32_t st = 0;
       const uint32_t tot = s ? id_gather_t<1>(lo, hi, p, q, st) : id_gather_t<0>(lo, hi, p, q, st);
       if (tot == 0) return false;
-      if (MLOB_LIKELY(tot == 1)) {
-        const int32_t nq = remove ? 0 : q - min(q, m.qty);
-        if (nq == 0) {
-          if (s) {
-            clear_st_t<1>(st);
-            if (--live1 > 0 && p == best1) best1 = side_best_t<1>();
-          } else {
-            clear_st_t<0>(st);
-            if (--live0 > 0 && p == best0) best0 = side_best_t<0>();
-          }
-          return true;
+      if (MLOB_UNLIKELY(tot > 1)) {  // duplicate live ids: the first in storage order
+        st = s ? dup_st_t<1>(lo, hi, p) : dup_st_t<0>(lo, hi, p);
+        uint32_t ilo, ihi;
+        q = s ? q_of_st_t<1>(st, false, ilo, ihi) : q_of_st_t<0>(st, false, ilo, ihi);
+      }
+      const int32_t nq = remove ? 0 : q - min(q, m.qty);
+      if (nq == 0) {
+        if (s) {
+          clear_st_t<1>(st);
+          if (--live1 > 0 && p == best1) best1 = side_best_t<1>();
+        } else {
+          clear_st_t<0>(st);
+          if (--live0 > 0 && p == best0) best0 = side_best_t<0>();
         }
-        if (s)
-          setq_st_t<1>(st, nq);
-        else
-          setq_st_t<0>(st, nq);
-        return false;
+        return true;
       }
-      // duplicate live ids: the generic path below
-    }
-    int nm, lk;
-    if (s)
-      scan_id_t<1>(lo, hi, nm, lk);
-    else
-      scan_id_t<0>(lo, hi, nm, lk);
-    const uint32_t b = __ballot_sync(FULLMASK, nm > 0);
-    if (b == 0) return false;
-    int owner = __ffs(b) - 1;
-    if (__reduce_add_sync(FULLMASK, static_cast<uint32_t>(nm)) != 1)
-      owner = s ? dup_owner_t<1>(lo, hi, lk) : dup_owner_t<0>(lo, hi, lk);
-    int32_t p, q;
-    slot_get_pq(s, lk, p, q);
-    p = __shfl_sync(FULLMASK, p, owner);
-    q = __shfl_sync(FULLMASK, q, owner);
-    const int32_t nq = remove ? 0 : q - min(q, m.qty);
-    const bool me = lane == owner;
-    if (nq == 0) {
-      slot_clear(s, lk, me);
-      if (s) {
-        if (--live1 > 0 && p == best1) best1 = side_best_t<1>();
-      } else {
-        if (--live0 > 0 && p == best0) best0 = side_best_t<0>();
+      if (s)
+        setq_st_t<1>(st, nq);
+      else
+        setq_st_t<0>(st, nq);
+      return false;
+    } else {  // shared-memory (deep) books
+      int nm, lk;
+      if (s)
+        scan_id_t<1>(lo, hi, nm, lk);
+      else
+        scan_id_t<0>(lo, hi, nm, lk);
+      const uint32_t b = __ballot_sync(FULLMASK, nm > 0);
+      if (b == 0) return false;
+      int owner = __ffs(b) - 1;
+      if (__reduce_add_sync(FULLMASK, static_cast<uint32_t>(nm)) != 1)
+        owner = s ? dup_owner_t<1>(lo, hi, lk) : dup_owner_t<0>(lo, hi, lk);
+      int32_t p, q;
+      slot_get_pq(s, lk, p, q);
+      p = __shfl_sync(FULLMASK, p, owner);
+      q = __shfl_sync(FULLMASK, q, owner);
+      const int32_t nq = remove ? 0 : q - min(q, m.qty);
+      const bool me = lane == owner;
+      if (nq == 0) {
+        slot_clear(s, lk, me);
+        if (s) {
+          if (--live1 > 0 && p == best1) best1 = side_best_t<1>();
+        } else {
+          if (--live0 > 0 && p == best0) best0 = side_best_t<0>();
+        }
+        return true;
       }
-      return true;
+      slot_setq(s, lk, me, nq);
+      return false;
     }
-    slot_setq(s, lk, me, nq);
-    return false;
   }
 
   // env.hpp:230: the mid follows the tops; it is refreshed only on the paths
