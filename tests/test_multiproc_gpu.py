@@ -148,3 +148,26 @@ def test_two_process_shards_match_single_process():
         assert (loc[k].pv_sum, loc[k].slippage_sum, loc[k].inventory_sq_sum, loc[k].episodes) == \
             (s.pv_sum, s.slippage_sum, s.inventory_sq_sum, s.episodes)
         assert loc[k].completion_sum == exact_completion(red[k], cfg.specs[k])
+
+
+def test_bench_two_ranks_one_line():
+    """bench.py's multi-rank path (the driver's N > 1 runs): two ranks
+    (gloo, both on cuda:0 — diagnostics mode), the store synthesised once per
+    node and loaded by the other rank, max-over-ranks timing, the stats
+    all-reduce, one JSON line from rank 0 with the whole-job figures."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MLOB_BENCH_BACKEND="gloo", MLOB_BENCH_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+           "--workload", "C", "--envs", "8192", "--steps", "4", "--warmup", "3", "--e2e-steps", "3",
+           "--no-extra"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root, env=env)
+    assert p.returncode == 0, (p.stdout + p.stderr)[-4000:]
+    lines = [json.loads(x) for x in p.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["config"]["envs_per_gpu"] == 4096 and d["value"] > 0
+    assert d["e2e"]["value"] > 0 and d["roofline"]["kernel"] == "book_kernel<4>"
