@@ -42,8 +42,6 @@ __host__ __device__ inline size_t warp_smem_bytes(const DevCfg& c) {
   b = (b + 15) / 16 * 16;
   if (MLOB_PREFIX_WALK && !smem_book(c.capacity))  // register books: the price-level walk's scratch
     b += static_cast<size_t>(spl_of(c.capacity)) * kWarp * sizeof(WalkEnt);
-  if (MLOB_IDS_SMEM && !smem_book(c.capacity))  // register books: the order ids
-    b += static_cast<size_t>(2) * spl_of(c.capacity) * kWarp * sizeof(uint2);
   if (smem_book(c.capacity)) b += book_smem_bytes(c.capacity);
   return (b + 127) / 128 * 128;
 }
@@ -72,8 +70,6 @@ __device__ void carve_block(const DevCfg& c) {
   p += static_cast<uint32_t>(2 * c.obs_depth * sizeof(L2Lvl));
   p = (p + 15) / 16 * 16;
   o.walk = p;
-  if (MLOB_PREFIX_WALK && !smem_book(c.capacity)) p += static_cast<uint32_t>(spl_of(c.capacity) * kWarp * sizeof(WalkEnt));
-  o.ids = p;
 }
 
 // deep-book smem region of a warp (after the WarpSmem carve-out)

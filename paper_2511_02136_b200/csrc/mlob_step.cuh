@@ -92,25 +92,10 @@ enum : uint64_t { kRngShuffle = 1, kRngTaskDir = 2, kRngBenchAction = 7, kRngEpi
 // Book side held in registers: SPL rows of 32 slots (lane-major).
 // Empty slot: q == 0, p == side sentinel (bid INT_MIN, ask INT_MAX), st == ~0.
 // st = arrival_seq << 8 | trader_id, so a u32 min over st is a min over seq.
-// MLOB_IDS_SMEM: the order ids (touched only by id matches, inserts, trade
-// records and the book store) live in shared memory, row k of this lane at
-// ids_[k * 32], which takes 4·SPL registers off the message loop (spills
-// 288 -> 76 B) but costs the id scans their shared-memory loads: measured
-// -2.5 % on C at 28 x 72, -7 % at 32 x 64, -9 % at 24 x 80.  Off.
-#ifndef MLOB_IDS_SMEM
-#define MLOB_IDS_SMEM 0
-#endif
 template <int SPL>
 struct RegSide {
   int32_t p_[SPL], q_[SPL];
   uint32_t st_[SPL];
-#if MLOB_IDS_SMEM
-  uint2* ids_;
-  __device__ __forceinline__ uint32_t LO(int k) const { return ids_[k * 32].x; }
-  __device__ __forceinline__ uint32_t HI(int k) const { return ids_[k * 32].y; }
-  __device__ __forceinline__ uint2 ID(int k) const { return ids_[k * 32]; }
-  __device__ __forceinline__ void put_id(int k, uint32_t lo, uint32_t hi) { ids_[k * 32] = make_uint2(lo, hi); }
-#else
   uint32_t lo_[SPL], hi_[SPL];
   __device__ __forceinline__ uint32_t LO(int k) const { return lo_[k]; }
   __device__ __forceinline__ uint32_t HI(int k) const { return hi_[k]; }
@@ -119,7 +104,6 @@ struct RegSide {
     lo_[k] = lo;
     hi_[k] = hi;
   }
-#endif
   __device__ __forceinline__ int32_t P(int k) const { return p_[k]; }
   __device__ __forceinline__ int32_t Q(int k) const { return q_[k]; }
   __device__ __forceinline__ uint32_t ST(int k) const { return st_[k]; }
@@ -134,19 +118,11 @@ struct RegSide {
   // (the "row K" comment), so LLVM cannot merge the per-row branches of
   // insert_t into one runtime-indexed write (that demotes the book to local
   // memory).
-#if MLOB_IDS_SMEM
-#define MLOB_PUT_IF(K)                                                                          \
-  asm volatile("{\n.reg .pred pp; // row " #K "\nsetp.ne.b32 pp, %3, 0;\n@pp mov.b32 %0, %4;\n"    \
-               "@pp mov.b32 %1, %5;\n@pp mov.b32 %2, %6;\n}"                                     \
-               : "+r"(p_[K]), "+r"(q_[K]), "+r"(st_[K])                                          \
-               : "r"(static_cast<uint32_t>(pred)), "r"(p), "r"(q), "r"(st))
-#else
 #define MLOB_PUT_IF(K)                                                                          \
   asm volatile("{\n.reg .pred pp; // row " #K "\nsetp.ne.b32 pp, %5, 0;\n@pp mov.b32 %0, %6;\n"    \
                "@pp mov.b32 %1, %7;\n@pp mov.b32 %2, %8;\n@pp mov.b32 %3, %9;\n@pp mov.b32 %4, %10;\n}" \
                : "+r"(p_[K]), "+r"(q_[K]), "+r"(lo_[K]), "+r"(hi_[K]), "+r"(st_[K])                 \
                : "r"(static_cast<uint32_t>(pred)), "r"(p), "r"(q), "r"(lo), "r"(hi), "r"(st))
-#endif
   template <int K>
   __device__ __forceinline__ void put_if(bool pred, int32_t p, int32_t q, uint32_t lo, uint32_t hi, uint32_t st) {
     static_assert(K < SPL && K < 8, "row");
@@ -158,9 +134,6 @@ struct RegSide {
     else if constexpr (K == 5) MLOB_PUT_IF(5);
     else if constexpr (K == 6) MLOB_PUT_IF(6);
     else MLOB_PUT_IF(7);
-#if MLOB_IDS_SMEM
-    if (pred) ids_[K * 32] = make_uint2(lo, hi);
-#endif
   }
 #undef MLOB_PUT_IF
   // first row K.. with a free lane (ballots b), warp-uniform branches
@@ -328,7 +301,7 @@ static_assert(sizeof(ActTmp) <= sizeof(DevMsg), "ActTmp reuses the agent-message
 // region pointers held in registers across the message loop forced spills
 // at the 80-register cap.
 struct SmemOff {
-  uint32_t chunk0, chunk1, bar, amsg, act, nact, scal, l2, walk, ids, _pad[2];
+  uint32_t chunk0, chunk1, bar, amsg, act, nact, scal, l2, walk, _pad[3];
 };
 // One resting order of the price level being walked (walk_level_t).
 struct WalkEnt {
@@ -349,8 +322,6 @@ struct WarpSmem {
   __device__ __forceinline__ int32_t* scal() const { return reinterpret_cast<int32_t*>(base + g_smem_off.scal); }
   __device__ __forceinline__ L2Lvl* l2() const { return reinterpret_cast<L2Lvl*>(base + g_smem_off.l2); }
   __device__ __forceinline__ WalkEnt* walk() const { return reinterpret_cast<WalkEnt*>(base + g_smem_off.walk); }
-  // register books with MLOB_IDS_SMEM: order ids [side][row * 32 + lane]
-  __device__ __forceinline__ uint2* ids() const { return reinterpret_cast<uint2*>(base + g_smem_off.ids); }
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -459,15 +430,6 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // ---------------------------------------------------------------------------
-#ifndef MLOB_ST_MATCH  // register books: address slots by their unique arrival word
-#define MLOB_ST_MATCH 1
-#endif
-#ifndef MLOB_BALLOT_INSERT  // register books: per-row ballots + uniform branch for inserts
-#define MLOB_BALLOT_INSERT 1
-#endif
-#ifndef MLOB_SMEM_BOOK  // 1: shared-memory book for every capacity (experiment)
-#define MLOB_SMEM_BOOK 0
-#endif
 // row loop over a side's SPL rows, unrolled kUnr at a time
 #define MLOB_ROWS(k)                                        \
   _Pragma("unroll 1") for (int k##_g = 0; k##_g < SPL; k##_g += kUnr) \
@@ -480,7 +442,7 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
 #ifndef MLOB_SCAN_UNR  // candidate-filter scans fully unrolled: 32 loads in flight
 #define MLOB_SCAN_UNR 32
 #endif
-template <int SPL, bool SMEM = (SPL > 8) || MLOB_SMEM_BOOK>
+template <int SPL, bool SMEM = (SPL > 8)>
 struct WarpEnv {
   using SideT = typename std::conditional<SMEM, SmemSide<SPL>, RegSide<SPL>>::type;
   // rows per unrolled group: all rows for register books (a full unroll keeps
@@ -530,12 +492,6 @@ struct WarpEnv {
       bid.bind(book_smem, ln, 0);
       ask.bind(book_smem + 4 * SPL * 32, ln, 1);
     }
-#if MLOB_IDS_SMEM
-    if constexpr (!SMEM) {
-      bid.ids_ = s.ids() + ln;
-      ask.ids_ = s.ids() + SPL * kWarp + ln;
-    }
-#endif
     err = 0;
     capacity_ = c.capacity;
     rec_trades_ = (p.flags & MLOB_VENV_RECORD_TRADES) != 0;
@@ -1159,7 +1115,7 @@ struct WarpEnv {
       const int lo_ = o ? live1 : live0;
       const int32_t bp = o ? best1 : best0;
       if (lo_ == 0 || (bp ^ flip) > kprice) break;
-      if constexpr (!SMEM && MLOB_ST_MATCH) {
+      if constexpr (!SMEM) {
         const uint32_t gst = o ? oldest_st_t<1>(bp) : oldest_st_t<0>(bp);
         uint32_t idlo = 0, idhi = 0;
         const int32_t q = o ? q_of_st_t<1>(gst, pass_ids, idlo, idhi) : q_of_st_t<0>(gst, pass_ids, idlo, idhi);
@@ -1232,7 +1188,7 @@ struct WarpEnv {
     const uint32_t seq = next_seq++;  // range checked once after the loop (process_messages)
     const uint32_t st = (seq << 8) | static_cast<uint32_t>(m.trader & 0xff);
     const uint32_t ilo = static_cast<uint32_t>(m.order_id()), ihi = static_cast<uint32_t>(m.order_id() >> 32);
-    if constexpr (!SMEM && MLOB_BALLOT_INSERT) {
+    if constexpr (!SMEM) {
       if (s)
         insert_t<1>(m.price, rem, ilo, ihi, st);
       else
@@ -1266,7 +1222,7 @@ struct WarpEnv {
   __device__ __forceinline__ bool by_id(const MsgRef& m, bool remove) {
     const int s = m.side;
     const uint32_t lo = static_cast<uint32_t>(m.order_id()), hi = static_cast<uint32_t>(m.order_id() >> 32);
-    if constexpr (!SMEM && MLOB_ST_MATCH) {
+    if constexpr (!SMEM) {
       int32_t p = 0, q = 0;
       uint32_t st = 0;
       const uint32_t tot = s ? id_gather_t<1>(lo, hi, p, q, st) : id_gather_t<0>(lo, hi, p, q, st);

@@ -131,3 +131,25 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError):
         env.DeviceStore(env.synth_store(0, n_messages=1000), 0)
+
+
+def test_host_store_save_load_roundtrip(tmp_path):
+    """mlob_host_store_save / _load: the binary image one rank per node writes
+    for the others (bench.py host_store) carries messages and book states
+    unchanged; a foreign or truncated file is a runtime_error."""
+    from paper_2511_02136_b200.env import HostStore
+    h = HostStore.synth(abi.synth_config(n_messages=30000, state_sample_every=100), 5)
+    path = str(tmp_path / "store.bin")
+    h.save(path)
+    g = HostStore.load(path)
+    assert g.n_messages == h.n_messages
+    assert (g.messages() == h.messages()).all()
+    assert g.states() == h.states()
+    with open(path, "r+b") as f:
+        f.truncate(1000)
+    with pytest.raises(RuntimeError):
+        HostStore.load(path)
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(b"not a store" * 10)
+    with pytest.raises(RuntimeError):
+        HostStore.load(str(bad))
