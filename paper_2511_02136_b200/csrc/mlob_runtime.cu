@@ -2163,7 +2163,10 @@ mlob_status mlob_venv_read_book(mlob_venv* v, uint64_t env, int side, mlob_resti
     std::vector<mlob_resting_order> o;
     const bool deep = v->spl > 8;  // 4-word slots: qt = q << 8 | trader, lo, hs = id_hi << 20 | seq
     const uint32_t* lo = reinterpret_cast<const uint32_t*>(id.data());
-    for (uint64_t i = 0; i < std::min<uint64_t>(m, h.hwm[side]); ++i) {
+    for (uint64_t s = 0; s < std::min<uint64_t>(m, h.hwm[side]); ++s) {
+      // slot s = row k, lane l; deep books group four rows: (k / 4) * 128 + l * 4 + k % 4
+      const uint64_t k = s / kWarp, l = s % kWarp;
+      const uint64_t i = deep ? (k >> 2) * 128 + l * 4 + (k & 3) : s;
       const int64_t qi = deep ? static_cast<int64_t>(static_cast<uint32_t>(q[i]) >> 8) : q[i];
       if (qi <= 0) continue;
       mlob_resting_order r;

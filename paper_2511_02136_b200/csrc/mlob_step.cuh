@@ -162,11 +162,15 @@ struct RegSide {
   }
 };
 
-// Book side in shared memory (deep books, capacity > 256): same interface and
-// slot layout as RegSide (row k, lane l at [k * 32 + l]); dynamic rows are
-// plain indexed accesses.
+// Book side in shared memory (deep books, capacity > 256): same interface as
+// RegSide.  Slots are laid out in groups of four rows: slot (row k, lane l)
+// of an array at [(k / 4) * 128 + l * 4 + k % 4], so one 16-byte
+// ld.shared.v4 brings a lane four consecutive rows and a warp's v4 load of a
+// group is conflict-free; the row scans (best price, oldest at a price, id
+// candidates, worst price) take SPL / 4 loads instead of SPL.
 template <int SPL>
 struct SmemSide {
+  static_assert(SPL % 4 == 0, "rows in groups of four");
   // Four words per slot, in the HBM layout of one side of a deep book (so
   // whole arrays move with bulk copies): p[SPL*32]; qt = qty << 8 | trader;
   // lo = order id bits 0..31; hs = order id bits 32..43 << 20 | arrival_seq.
@@ -184,6 +188,11 @@ struct SmemSide {
   int32_t lw;
   uint32_t lw_stale;
   int side_;
+  // word offset of row k from this lane's base (compile-time for unrolled k)
+  __device__ __forceinline__ static int at(int k) { return (k >> 2) * 128 + (k & 3); }
+  __device__ __forceinline__ int4 P4(int g) const { return *reinterpret_cast<const int4*>(p_ + g * 128); }
+  __device__ __forceinline__ uint4 QT4(int g) const { return *reinterpret_cast<const uint4*>(qt_ + g * 128); }
+  __device__ __forceinline__ uint4 LO4(int g) const { return *reinterpret_cast<const uint4*>(lo_ + g * 128); }
   __device__ __forceinline__ int32_t worse(int32_t a, int32_t b) const { return side_ ? max(a, b) : min(a, b); }
   __device__ __forceinline__ void occ_set(int k, bool on) {
     const uint32_t b = 1u << k;
@@ -192,14 +201,18 @@ struct SmemSide {
   __device__ __forceinline__ uint32_t free_mask() const {
     return ~occ & (SPL >= 32 ? 0xffffffffu : ((1u << SPL) - 1u));
   }
-  // this lane's worst live price, rescanned from the price row under the
+  // this lane's worst live price, rescanned from the price rows under the
   // occupancy mask (a per-lane count at the worst price measured -30 % on D)
   __device__ __forceinline__ void refresh_lw() {
     lw = side_ ? INT_MIN : INT_MAX;
 #pragma unroll
-    for (int k = 0; k < SPL; ++k) {
-      const int32_t p = p_[k * 32];
-      lw = (occ >> k) & 1u ? worse(lw, p) : lw;
+    for (int g = 0; g < SPL / 4; ++g) {
+      const int4 p = P4(g);
+      const uint32_t o = occ >> (4 * g);
+      lw = (o & 1u) ? worse(lw, p.x) : lw;
+      lw = (o & 2u) ? worse(lw, p.y) : lw;
+      lw = (o & 4u) ? worse(lw, p.z) : lw;
+      lw = (o & 8u) ? worse(lw, p.w) : lw;
     }
     lw_stale = 0;
   }
@@ -208,38 +221,45 @@ struct SmemSide {
     occ = 0;
     lw = side_ ? INT_MIN : INT_MAX;
 #pragma unroll
-    for (int k = 0; k < SPL; ++k) {
-      const int32_t q = Q(k), p = p_[k * 32];
-      occ |= (q > 0 ? 1u : 0u) << k;
-      lw = q > 0 ? worse(lw, p) : lw;
+    for (int g = 0; g < SPL / 4; ++g) {
+      const int4 p = P4(g);
+      const uint4 qt = QT4(g);
+      const int32_t pv[4] = {p.x, p.y, p.z, p.w};
+      const uint32_t qv[4] = {qt.x, qt.y, qt.z, qt.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool live = (qv[j] >> 8) != 0;
+        occ |= (live ? 1u : 0u) << (4 * g + j);
+        lw = live ? worse(lw, pv[j]) : lw;
+      }
     }
     lw_stale = 0;
   }
-  __device__ __forceinline__ int32_t P(int k) const { return p_[k * 32]; }
-  __device__ __forceinline__ int32_t Q(int k) const { return static_cast<int32_t>(qt_[k * 32] >> 8); }
-  __device__ __forceinline__ uint32_t LO(int k) const { return lo_[k * 32]; }
-  __device__ __forceinline__ uint32_t HI(int k) const { return hs_[k * 32] >> 20; }
+  __device__ __forceinline__ int32_t P(int k) const { return p_[at(k)]; }
+  __device__ __forceinline__ int32_t Q(int k) const { return static_cast<int32_t>(qt_[at(k)] >> 8); }
+  __device__ __forceinline__ uint32_t LO(int k) const { return lo_[at(k)]; }
+  __device__ __forceinline__ uint32_t HI(int k) const { return hs_[at(k)] >> 20; }
   // the reference record's arrival word seq << 8 | trader (ordered like seq)
   __device__ __forceinline__ uint32_t ST(int k) const {
-    return ((hs_[k * 32] & 0xfffffu) << 8) | (qt_[k * 32] & 0xffu);
+    return ((hs_[at(k)] & 0xfffffu) << 8) | (qt_[at(k)] & 0xffu);
   }
   __device__ __forceinline__ void put(int k, int32_t p, int32_t q, uint32_t lo, uint32_t hi,
                                       uint32_t st) {
-    p_[k * 32] = p;
-    qt_[k * 32] = (static_cast<uint32_t>(q) << 8) | (st & 0xffu);
-    lo_[k * 32] = lo;
-    hs_[k * 32] = (hi << 20) | ((st >> 8) & 0xfffffu);
+    p_[at(k)] = p;
+    qt_[at(k)] = (static_cast<uint32_t>(q) << 8) | (st & 0xffu);
+    lo_[at(k)] = lo;
+    hs_[at(k)] = (hi << 20) | ((st >> 8) & 0xfffffu);
     occ_set(k, q > 0);
     if (q > 0) lw = worse(lw, p);
   }
   __device__ __forceinline__ void get_pq(int k, int32_t& p, int32_t& q) const {
-    p = p_[k * 32];
+    p = p_[at(k)];
     q = Q(k);
   }
   __device__ __forceinline__ void get_qid(int k, int32_t& q, uint32_t& lo, uint32_t& hi) const {
     q = Q(k);
-    lo = lo_[k * 32];
-    hi = hs_[k * 32] >> 20;
+    lo = lo_[at(k)];
+    hi = hs_[at(k)] >> 20;
   }
   __device__ __forceinline__ void set(int k, bool pred, int32_t p, int32_t q, uint32_t lo,
                                       uint32_t hi, uint32_t st) {
@@ -250,13 +270,13 @@ struct SmemSide {
     set(k, pred, p, q, lo, hi, st);
   }
   __device__ __forceinline__ void setq(int k, bool pred, int32_t q) {
-    if (pred) qt_[k * 32] = (static_cast<uint32_t>(q) << 8) | (qt_[k * 32] & 0xffu);
+    if (pred) qt_[at(k)] = (static_cast<uint32_t>(q) << 8) | (qt_[at(k)] & 0xffu);
   }
   __device__ __forceinline__ void clear(int k, bool pred, int32_t empty_p) {
     if (pred) {
-      if (p_[k * 32] == lw) lw_stale = 1;
-      p_[k * 32] = empty_p;
-      qt_[k * 32] = 0;
+      if (p_[at(k)] == lw) lw_stale = 1;
+      p_[at(k)] = empty_p;
+      qt_[at(k)] = 0;
       occ_set(k, false);
     }
   }
@@ -266,10 +286,10 @@ struct SmemSide {
     lw_stale = 1;
     occ = 0;
     base_ = base;
-    p_ = reinterpret_cast<int32_t*>(base) + lane;
-    qt_ = base + SPL * 32 + lane;
-    lo_ = base + 2 * SPL * 32 + lane;
-    hs_ = base + 3 * SPL * 32 + lane;
+    p_ = reinterpret_cast<int32_t*>(base) + lane * 4;
+    qt_ = base + SPL * 32 + lane * 4;
+    lo_ = base + 2 * SPL * 32 + lane * 4;
+    hs_ = base + 3 * SPL * 32 + lane * 4;
   }
 };
 
@@ -547,7 +567,8 @@ struct WarpEnv {
     if constexpr (SMEM) {  // rows below the high-water mark: four bulk stores
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // lanes' smem writes -> async proxy
       __syncwarp();
-      const uint32_t rows = static_cast<uint32_t>((hwm + kWarp - 1) / kWarp);
+      // whole four-row groups (the grouped layout's contiguous prefix)
+      const uint32_t rows = static_cast<uint32_t>((hwm + 4 * kWarp - 1) / (4 * kWarp) * 4);
       if (lane == 0 && rows) {
         const size_t g = (env * 2 + S) * SPL * kWarp;
         const uint32_t* b = d.base_;
@@ -624,7 +645,8 @@ struct WarpEnv {
   __device__ __forceinline__ void book_load_issue() {
     if constexpr (SMEM) {
       const EnvHdr& h = kp.hdr[env];
-      const int rows0 = (h.hwm[0] + kWarp - 1) / kWarp, rows1 = (h.hwm[1] + kWarp - 1) / kWarp;
+      // whole four-row groups below the high-water marks (stored / reset as groups)
+      const int rows0 = (h.hwm[0] + 4 * kWarp - 1) / (4 * kWarp) * 4, rows1 = (h.hwm[1] + 4 * kWarp - 1) / (4 * kWarp) * 4;
       for (int k = rows0; k < SPL; ++k) bid.put(k, INT_MIN, 0, 0, 0, kEmptySt);
       for (int k = rows1; k < SPL; ++k) ask.put(k, INT_MAX, 0, 0, 0, kEmptySt);
       if (lane == 0) {
@@ -719,7 +741,15 @@ struct WarpEnv {
   __device__ __forceinline__ int32_t side_best_t() {
     SideT& d = sd<S>();
     int32_t b = empty_price<S>();
-    MLOB_SCAN_ROWS(k) b = better_of<S>(b, d.P(k));
+    if constexpr (SMEM) {  // four rows per 16-byte load
+#pragma unroll
+      for (int g = 0; g < SPL / 4; ++g) {
+        const int4 v = d.P4(g);
+        b = better_of<S>(better_of<S>(b, v.x), better_of<S>(v.y, better_of<S>(v.z, v.w)));
+      }
+    } else {
+      MLOB_SCAN_ROWS(k) b = better_of<S>(b, d.P(k));
+    }
     return redux_best<S>(b);
   }
   // lane-local oldest slot (min st) at `price`
@@ -732,7 +762,12 @@ struct WarpEnv {
       // shared-memory book: one load per row for the price, the arrival word
       // only for the (few) rows at that price
       uint32_t cand = 0;
-      MLOB_SCAN_ROWS(k) cand |= (d.P(k) == price ? 1u : 0u) << k;
+#pragma unroll
+      for (int g = 0; g < SPL / 4; ++g) {
+        const int4 v = d.P4(g);
+        cand |= ((v.x == price ? 1u : 0u) | (v.y == price ? 2u : 0u) | (v.z == price ? 4u : 0u) |
+                 (v.w == price ? 8u : 0u)) << (4 * g);
+      }
       while (cand) {
         const int k = __ffs(cand) - 1;
         cand &= cand - 1;
@@ -760,7 +795,12 @@ struct WarpEnv {
       // shared-memory book: filter rows on the low id word (one load per row),
       // then check the high word and liveness of the candidates only
       uint32_t cand = 0;
-      MLOB_SCAN_ROWS(k) cand |= (d.LO(k) == lo ? 1u : 0u) << k;
+#pragma unroll
+      for (int g = 0; g < SPL / 4; ++g) {
+        const uint4 v = d.LO4(g);
+        cand |= ((v.x == lo ? 1u : 0u) | (v.y == lo ? 2u : 0u) | (v.z == lo ? 4u : 0u) | (v.w == lo ? 8u : 0u))
+                << (4 * g);
+      }
       while (cand) {
         const int k = __ffs(cand) - 1;
         cand &= cand - 1;

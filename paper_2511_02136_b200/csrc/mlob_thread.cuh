@@ -487,10 +487,13 @@ struct ThreadEnv {
     const uint32_t rows = (n + kWarp - 1) / kWarp;
     MLOB_CHECK(rows <= static_cast<uint32_t>(spl));
     const size_t base = (env * 2 + static_cast<uint64_t>(S)) * spl * kWarp;
-    if (spl > 8) {  // deep book: 4-word slots (SmemSide): p, q << 8 | trader, id lo, id hi << 20 | seq
+    if (spl > 8) {  // deep book: 4-word slots (SmemSide): p, q << 8 | trader, id lo, id hi << 20 | seq,
+                    // slot (row k, lane l) at (k / 4) * 128 + l * 4 + k % 4, written in whole four-row groups
       uint32_t* lo = reinterpret_cast<uint32_t*>(kp.bk_id);
-      for (uint32_t i = 0; i < rows * kWarp; ++i) {
-        const size_t x = base + i;
+      const uint32_t grows = (rows + 3) / 4 * 4;
+      for (uint32_t i = 0; i < grows * kWarp; ++i) {
+        const uint32_t k = i / kWarp, l = i % kWarp;
+        const size_t x = base + (k >> 2) * 128 + l * 4 + (k & 3);
         const uint64_t id = id_base + i;
         const bool live = i < n;
         if (live && (lv[i].qty >= (1 << 24) || (id >> 44) != 0)) err |= kErrDeepRange;
