@@ -8,13 +8,13 @@
 //   backward warp per stream, t = T-1..0: head gradients into dh, the GRU cell
 //            backward, the recurrent carry (net.hpp:193-277); gate gradients
 //            stored per (t, stream)
-//   weights  every parameter gradient is a sum over K = T x S rows: skinny
-//            fp64 GEMMs / GEMVs (cuBLAS DGEMM — plain library GEMMs) straight
-//            into the PolicyGrad layout
+//   weights  every parameter gradient is a sum over K = T x S rows: a
+//            hand-written split-K fp64 contraction (gemm_tn: K-chunks staged
+//            in shared memory, per-block partials summed in block order, so
+//            the result is deterministic) straight into the PolicyGrad layout
 //   step     global-norm clip + Adam (net.hpp:281-331), one block
 // The reductions run in a different order than the reference's sequential
 // loops, so parity is to a tolerance (tests: 1e-8 relative on parameters).
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -357,17 +357,104 @@ cudaError_t launch_fill(double* x, uint64_t n, double v, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// Out (R x C, row-major) = L^T (R x K) . M (K x C), L (K x R) and M (K x C) row-major
-bool gemm_tn(cublasHandle_t h, const double* L, const double* M, uint64_t K, int R, int C, double* out) {
-  const double one = 1.0, zero = 0.0;
-  return cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, C, R, static_cast<int>(K), &one, M, C, L, R, &zero, out, C) ==
-         CUBLAS_STATUS_SUCCESS;
+namespace {
+// Thread work unit: one output column c and kGemmRB consecutive output rows
+// r0.. (out[r][c] = sum_k L[k][r] M[k][c]): per staged row k, one M value and
+// kGemmRB L values feed kGemmRB fused multiply-adds (explicit __fma_rn: the
+// file is built with --fmad=false for the env kernels' bit-exactness; the
+// learner is compared to 1e-8).
+constexpr int kGemmThreads = 256, kGemmTK = 32, kGemmRB = 8;
+
+// Block b sums rows [b * chunk, (b + 1) * chunk) for work units
+// [u0, u0 + nu) into part[b * E + e].  Narrow outputs (fewer units than
+// threads) split each staged tile's rows over `ks` = blockDim / nu thread
+// groups whose accumulators are then added in group order (deterministic).
+__global__ void __launch_bounds__(kGemmThreads) gemm_tn_partial_kernel(const double* __restrict__ L,
+                                                                      const double* __restrict__ M, uint64_t K,
+                                                                      int R, int C, uint64_t chunk, int u0, int nu,
+                                                                      double* __restrict__ part) {
+  extern __shared__ double gsm[];
+  double* Ls = gsm;                  // [kGemmTK][R]
+  double* Ms = gsm + kGemmTK * R;    // [kGemmTK][C]
+  double* red = Ms + kGemmTK * C;    // [kGemmThreads][kGemmRB] group partials
+  const int E = R * C;
+  const int ks = kGemmThreads / nu;  // row groups
+  const int grp = static_cast<int>(threadIdx.x) / nu, lu = static_cast<int>(threadIdx.x) % nu;
+  const bool active = grp < ks;
+  const int u = u0 + lu;
+  const int c = u % C, r0 = (u / C) * kGemmRB;
+  const uint64_t k0 = static_cast<uint64_t>(blockIdx.x) * chunk;
+  const uint64_t k1 = k0 + chunk < K ? k0 + chunk : K;
+  double acc[kGemmRB];
+#pragma unroll
+  for (int j = 0; j < kGemmRB; ++j) acc[j] = 0.0;
+  for (uint64_t kt = k0; kt < k1; kt += kGemmTK) {
+    const int n = static_cast<int>(k1 - kt < kGemmTK ? k1 - kt : kGemmTK);
+    for (int x = threadIdx.x; x < n * R; x += kGemmThreads) Ls[x] = L[kt * R + x];
+    if (M)
+      for (int x = threadIdx.x; x < n * C; x += kGemmThreads) Ms[x] = M[kt * C + x];
+    __syncthreads();
+    if (active) {
+      for (int i = grp; i < n; i += ks) {
+        const double mv = M ? Ms[i * C + c] : 1.0;
+        const double* lr = Ls + i * R + r0;
+#pragma unroll
+        for (int j = 0; j < kGemmRB; ++j)
+          if (r0 + j < R) acc[j] = __fma_rn(lr[j], mv, acc[j]);
+      }
+    }
+    __syncthreads();
+  }
+  if (ks > 1) {  // fold the row groups, in group order
+#pragma unroll
+    for (int j = 0; j < kGemmRB; ++j) red[threadIdx.x * kGemmRB + j] = acc[j];
+    __syncthreads();
+    if (grp == 0) {
+      for (int g = 1; g < ks; ++g)
+#pragma unroll
+        for (int j = 0; j < kGemmRB; ++j) acc[j] += red[(g * nu + lu) * kGemmRB + j];
+    }
+  }
+  if (grp == 0) {
+#pragma unroll
+    for (int j = 0; j < kGemmRB; ++j)
+      if (r0 + j < R) part[static_cast<size_t>(blockIdx.x) * E + (r0 + j) * C + c] = acc[j];
+  }
 }
-// out (R) = column sums of L (K x R, row-major)
-bool colsum(cublasHandle_t h, const double* L, const double* ones, uint64_t K, int R, double* out) {
-  const double one = 1.0, zero = 0.0;
-  return cublasDgemv(h, CUBLAS_OP_N, R, static_cast<int>(K), &one, L, R, ones, 1, &zero, out, 1) ==
-         CUBLAS_STATUS_SUCCESS;
+
+__global__ void gemm_tn_sum_kernel(const double* __restrict__ part, int P, int E, double* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  double s = 0.0;
+  for (int b = 0; b < P; ++b) s += part[static_cast<size_t>(b) * E + e];
+  out[e] = s;
+}
+}  // namespace
+
+cudaError_t gemm_tn(const double* L, const double* M, uint64_t K, int R, int C, double* out, double* part,
+                    cudaStream_t s) {
+  const int E = R * C;
+  if (E <= 0) return cudaSuccess;
+  uint64_t chunk = (K + kGemmBlocks - 1) / kGemmBlocks;
+  chunk = (chunk + kGemmTK - 1) / kGemmTK * kGemmTK;
+  const int P = static_cast<int>(K == 0 ? 1 : (K + chunk - 1) / chunk);
+  const size_t smem = (static_cast<size_t>(kGemmTK) * (R + C) + kGemmThreads * kGemmRB) * sizeof(double);
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(gemm_tn_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  const int units = (R + kGemmRB - 1) / kGemmRB * C;
+  if (K == 0) {
+    const cudaError_t e = cudaMemsetAsync(part, 0, static_cast<size_t>(E) * sizeof(double), s);
+    if (e != cudaSuccess) return e;
+  }
+  for (int u0 = 0; u0 < units && K > 0; u0 += kGemmThreads) {
+    const int nu = units - u0 < kGemmThreads ? units - u0 : kGemmThreads;
+    gemm_tn_partial_kernel<<<P, kGemmThreads, smem, s>>>(L, M, K, R, C, chunk, u0, nu, part);
+  }
+  gemm_tn_sum_kernel<<<(E + 255) / 256, 256, 0, s>>>(part, P, E, out);
+  return cudaGetLastError();
 }
 
 }  // namespace mlob

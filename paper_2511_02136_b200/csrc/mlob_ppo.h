@@ -1,7 +1,6 @@
 // mlob_ppo.h — device PPO update (mlob_ppo.cu): kernel arguments and launchers.
 #pragma once
 
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -48,7 +47,15 @@ cudaError_t launch_clip_adam(double* p, double* g, double* m, double* v, uint64_
                              double c1, double c2, double* norm_out, cudaStream_t s);
 cudaError_t launch_to_inference(const double* p, int D, int H, int A, double* w, cudaStream_t s);
 cudaError_t launch_fill(double* x, uint64_t n, double v, cudaStream_t s);
-bool gemm_tn(cublasHandle_t h, const double* L, const double* M, uint64_t K, int R, int C, double* out);
-bool colsum(cublasHandle_t h, const double* L, const double* ones, uint64_t K, int R, double* out);
+// Parameter-gradient contractions over the K = T x S rows of a minibatch
+// (hand-written split-K fp64 reductions, deterministic: per-block partials
+// summed in block order).  out (R x C, row-major) = L^T (R x K) . M (K x C);
+// M == nullptr: column sums of L.  `part` holds kGemmBlocks x R x C doubles.
+constexpr int kGemmBlocks = 296;
+cudaError_t gemm_tn(const double* L, const double* M, uint64_t K, int R, int C, double* out, double* part,
+                    cudaStream_t s);
+inline cudaError_t colsum(const double* L, uint64_t K, int R, double* out, double* part, cudaStream_t s) {
+  return gemm_tn(L, nullptr, K, R, 1, out, part, s);
+}
 
 }  // namespace mlob

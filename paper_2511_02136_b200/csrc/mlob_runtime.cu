@@ -20,7 +20,6 @@
 #include "mlob_policy.h"
 #include "mlob_ppo.h"
 
-#include <cublas_v2.h>
 #include <sstream>
 
 namespace mlob {
@@ -159,7 +158,6 @@ struct mlob_venv {
   // ppo_update workspace (mlob_ppo.cu), grown on demand
   char* ppo_ws = nullptr;
   uint64_t ppo_ws_bytes = 0;
-  cublasHandle_t blas = nullptr;
   struct Batch {
     uint64_t T = 0, B = 0;
     char* arena = nullptr;
@@ -266,7 +264,6 @@ struct mlob_venv {
     for (NetState& n : eval_nets) free_net(n);
     if (roll_graph) cudaGraphExecDestroy(roll_graph);
     cudaFree(ppo_ws);
-    if (blas) cublasDestroy(blas);
     for (void* p : allocs) cudaFree(p);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
@@ -1450,15 +1447,13 @@ mlob_status mlob_venv_ppo_update(mlob_venv* v, int type, const mlob_ppo_config* 
     const int D = ns.dn.D, H = ns.dn.H, A = ns.dn.A, H3 = 3 * H;
     const uint64_t T = bt.T, B = bt.B;
     const int n_mb = std::max(1, std::min<int>(cfg->minibatches, static_cast<int>(std::min<uint64_t>(B, INT32_MAX))));
-    if (!v->blas) {
-      if (cublasCreate(&v->blas) != CUBLAS_STATUS_SUCCESS) fail(MLOB_E_CUDA, "cublasCreate failed");
-    }
-    cublasSetStream(v->blas, v->stream);
-    // workspace for the largest minibatch
+    // workspace for the largest minibatch + the contractions' per-block partials
     const uint64_t Kmax = T * ((B + n_mb - 1) / n_mb + 1);
-    const uint64_t ones_n = std::max(Kmax, T * B);
+    const uint64_t max_e = std::max<uint64_t>({static_cast<uint64_t>(H3) * std::max(D, H), static_cast<uint64_t>(A) * H,
+                                               static_cast<uint64_t>(H3), 8});
+    const uint64_t part_n = static_cast<uint64_t>(kGemmBlocks) * max_e;
     const uint64_t cols = static_cast<uint64_t>(D) + 6ull * H + A + 1 + 5 + 2ull * H3 + 1;  // per row
-    const uint64_t need = (Kmax * cols + ones_n + 16) * 8 + B * 4 + 4096;
+    const uint64_t need = (Kmax * cols + part_n + 16) * 8 + B * 4 + 4096;
     if (need > v->ppo_ws_bytes) {
       cudaFree(v->ppo_ws);
       v->ppo_ws = nullptr;
@@ -1466,11 +1461,10 @@ mlob_status mlob_venv_ppo_update(mlob_venv* v, int type, const mlob_ppo_config* 
       v->ppo_ws_bytes = need;
     }
     double* wsd = reinterpret_cast<double*>(v->ppo_ws);
-    double* ones = wsd;
-    double* sums = ones + ones_n;  // [0..4] terms, [5] grad norm, [6] reward sum
+    double* part = wsd;            // gemm_tn partials
+    double* sums = part + part_n;  // [0..4] terms, [5] grad norm, [6] reward sum
     double* rows = sums + 16;
     int32_t* d_order = reinterpret_cast<int32_t*>(rows + Kmax * cols);
-    cuda_check(launch_fill(ones, ones_n, 1.0, v->stream), "fill");
     // reference-layout offsets (PolicyGrad mirrors PolicyNet)
     const uint64_t o_wih = 0, o_whh = o_wih + static_cast<uint64_t>(H3) * D, o_bih = o_whh + static_cast<uint64_t>(H3) * H,
                    o_bhh = o_bih + H3, o_wa = o_bhh + H3, o_ba = o_wa + static_cast<uint64_t>(A) * H, o_wc = o_ba + A,
@@ -1546,14 +1540,17 @@ mlob_status mlob_venv_ppo_update(mlob_venv* v, int type, const mlob_ppo_config* 
         cuda_check(launch_gather_adv(bt.adv, a.mb, T, B, S, adv, cfg->normalize_adv != 0, v->stream), "advantages");
         cuda_check(launch_ppo_forward(a, v->stream), "ppo forward");
         cuda_check(launch_ppo_backward(a, v->stream), "ppo backward");
-        cublasHandle_t hb = v->blas;
         double* g = ns.g;
-        if (!gemm_tn(hb, a.dA, a.X, K, H3, D, g + o_wih) || !gemm_tn(hb, a.dB, a.Hin, K, H3, H, g + o_whh) ||
-            !colsum(hb, a.dA, ones, K, H3, g + o_bih) || !colsum(hb, a.dB, ones, K, H3, g + o_bhh) ||
-            !gemm_tn(hb, a.dL, a.Hout, K, A, H, g + o_wa) || !colsum(hb, a.dL, ones, K, A, g + o_ba) ||
-            !gemm_tn(hb, a.dV, a.Hout, K, 1, H, g + o_wc) || !colsum(hb, a.dV, ones, K, 1, g + o_bc) ||
-            !colsum(hb, a.terms, ones, K, 5, sums))
-          fail(MLOB_E_CUDA, "cuBLAS gradient GEMM failed");
+        cudaStream_t st = v->stream;
+        cuda_check(gemm_tn(a.dA, a.X, K, H3, D, g + o_wih, part, st), "gradient w_ih");
+        cuda_check(gemm_tn(a.dB, a.Hin, K, H3, H, g + o_whh, part, st), "gradient w_hh");
+        cuda_check(colsum(a.dA, K, H3, g + o_bih, part, st), "gradient b_ih");
+        cuda_check(colsum(a.dB, K, H3, g + o_bhh, part, st), "gradient b_hh");
+        cuda_check(gemm_tn(a.dL, a.Hout, K, A, H, g + o_wa, part, st), "gradient w_actor");
+        cuda_check(colsum(a.dL, K, A, g + o_ba, part, st), "gradient b_actor");
+        cuda_check(gemm_tn(a.dV, a.Hout, K, 1, H, g + o_wc, part, st), "gradient w_critic");
+        cuda_check(colsum(a.dV, K, 1, g + o_bc, part, st), "gradient b_critic");
+        cuda_check(colsum(a.terms, K, 5, sums, part, st), "loss terms");
         double tsum[5];
         cuda_check(cudaMemcpyAsync(tsum, sums, sizeof tsum, cudaMemcpyDeviceToHost, v->stream), "D2H");
         cuda_check(cudaStreamSynchronize(v->stream), "sync");
@@ -1594,7 +1591,7 @@ mlob_status mlob_venv_ppo_update(mlob_venv* v, int type, const mlob_ppo_config* 
     mt.approx_kl *= inv;
     mt.clip_frac *= inv;
     mt.grad_norm *= inv;
-    if (!colsum(v->blas, bt.rewards, ones, T * B, 1, sums + 6)) fail(MLOB_E_CUDA, "cuBLAS reduction failed");
+    cuda_check(colsum(bt.rewards, T * B, 1, sums + 6, part, v->stream), "reward sum");
     double rsum = 0.0;
     cuda_check(cudaMemcpyAsync(&rsum, sums + 6, 8, cudaMemcpyDeviceToHost, v->stream), "D2H");
     // the next rollout's network: transposed copy + b_critic
