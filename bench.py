@@ -7,9 +7,17 @@ auto-reset).  The unit of the metric is the message-level LOB step — one MBO
 message (agent or replay) through one env's book — counted exactly like the
 reference's messages_processed (env.hpp:233, bench.hpp:133-154).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload E|B|C]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload E|B|C|D] [--no-extra]
   torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
   python bench.py --impl reference ...                    (the reference on the host cores)
+
+One step = act_kernel + book_kernel + outcome_kernel.  The line
+carries the default workload (E) and, unless --no-extra, config D (deep book)
+under "workloads"; "roofline" is the dominant kernel's (book_kernel: its own
+algorithmic bytes over its CUDA-event time on the launching stream), with the
+whole-step figure, the kernel's share of the step, the matching ncu capture's
+DRAM traffic and an issue-rate roofline beside it.  Small workloads (working
+set < 4 x L2) get the L2 flushed between timed steps, outside the events.
 """
 from __future__ import annotations
 
