@@ -188,7 +188,9 @@ __global__ void __launch_bounds__(kThreadBlock) reset_kernel(const __grid_consta
 // (C <= 256): a grid of one phase-synchronised block per SM walks the envs in
 // rounds (env = first + r * stride), the next round's first replay chunk
 // staged while the current env finishes.  Deep books: one env per warp.
-template <int SPL>
+// REC: the trade log is on (MLOB_VENV_RECORD_TRADES) — a separate
+// instantiation, so the fill loop of the plain step carries no log flag
+template <int SPL, bool REC>
 __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL>())
     book_kernel(const __grid_constant__ KParams kparam) {
   const int kWarps = static_cast<int>(blockDim.x) / kWarp;
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL
   const DevCfg& cfg = sp_.cfg;
   char* wbase = smem + warp * warp_smem_bytes(cfg);
   WarpSmem sm{wbase};
-  WarpEnv<SPL> w(kp, cfg, sm, idle ? 0 : first, lane, book_region(wbase, cfg));
+  WarpEnv<SPL, REC> w(kp, cfg, sm, idle ? 0 : first, lane, book_region(wbase, cfg));
   const int mps = cfg.mps;
   const int nch = (mps + kChunk - 1) / kChunk;
   if (lane == 0) {
@@ -367,7 +369,7 @@ static unsigned grid_for(uint64_t n) {
 }
 static unsigned thread_grid(uint64_t n) { return static_cast<unsigned>((n + kThreadBlock - 1) / kThreadBlock); }
 
-template <int SPL>
+template <int SPL, bool REC>
 static cudaError_t launch_book_t(const KParams& kp, const DevCfg& cfg, cudaStream_t s) {
   int warps = book_warps(cfg);
   const size_t staged = book_staged_bytes(cfg);
@@ -381,7 +383,7 @@ static cudaError_t launch_book_t(const KParams& kp, const DevCfg& cfg, cudaStrea
   if (e != cudaSuccess) return e;
   size_t& done = sm_set[cur_dev & 63];
   if (full_sm > done) {
-    e = cudaFuncSetAttribute(book_kernel<SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(full_sm));
+    e = cudaFuncSetAttribute(book_kernel<SPL, REC>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(full_sm));
     if (e != cudaSuccess) return e;
     done = full_sm;
     per_sm_of[cur_dev & 63] = 0;  // re-query the occupancy for the new block size
@@ -394,7 +396,7 @@ static cudaError_t launch_book_t(const KParams& kp, const DevCfg& cfg, cudaStrea
     if (n_sm == 0 && (e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, cur_dev)) != cudaSuccess)
       return e;
     if (per_sm == 0) {
-      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, book_kernel<SPL>, warps * kWarp, full_sm)) !=
+      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, book_kernel<SPL, REC>, warps * kWarp, full_sm)) !=
           cudaSuccess)
         return e;
       if (per_sm < 1) per_sm = 1;
@@ -410,20 +412,25 @@ static cudaError_t launch_book_t(const KParams& kp, const DevCfg& cfg, cudaStrea
     blocks = need < cap ? need : cap;
   }
   const size_t sm = staged + warp_smem_bytes(cfg) * warps;
-  book_kernel<SPL><<<static_cast<unsigned>(blocks), warps * kWarp, sm, s>>>(kp);
+  book_kernel<SPL, REC><<<static_cast<unsigned>(blocks), warps * kWarp, sm, s>>>(kp);
   return cudaGetLastError();
 }
 
-static cudaError_t launch_book(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s) {
+template <bool REC>
+static cudaError_t launch_book_r(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s) {
   switch (spl) {
-    case 1: return launch_book_t<1>(kp, cfg, s);
-    case 2: return launch_book_t<2>(kp, cfg, s);
-    case 4: return launch_book_t<4>(kp, cfg, s);
-    case 8: return launch_book_t<8>(kp, cfg, s);
-    case 16: return launch_book_t<16>(kp, cfg, s);
-    case 32: return launch_book_t<32>(kp, cfg, s);
+    case 1: return launch_book_t<1, REC>(kp, cfg, s);
+    case 2: return launch_book_t<2, REC>(kp, cfg, s);
+    case 4: return launch_book_t<4, REC>(kp, cfg, s);
+    case 8: return launch_book_t<8, REC>(kp, cfg, s);
+    case 16: return launch_book_t<16, REC>(kp, cfg, s);
+    case 32: return launch_book_t<32, REC>(kp, cfg, s);
   }
   return cudaErrorInvalidValue;
+}
+static cudaError_t launch_book(const KParams& kp, const DevCfg& cfg, int spl, cudaStream_t s) {
+  return (kp.flags & MLOB_VENV_RECORD_TRADES) ? launch_book_r<true>(kp, cfg, spl, s)
+                                              : launch_book_r<false>(kp, cfg, spl, s);
 }
 
 int slots_per_lane(int capacity) { return spl_of(capacity); }

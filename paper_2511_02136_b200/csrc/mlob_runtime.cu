@@ -2226,8 +2226,8 @@ mlob_status mlob_venv_read_trades(mlob_venv* v, uint64_t env, mlob_trade* out, u
     if (env >= v->n_envs) fail(MLOB_E_OUT_OF_RANGE, "env index out of range");
     EnvHdr h;
     d2h(v, &h, v->d_hdr + env, 1);
-    *n_out = h.n_trades;
     if (!(v->flags & MLOB_VENV_RECORD_TRADES)) fail(MLOB_E_LOGIC, "trade log disabled (MLOB_VENV_RECORD_TRADES)");
+    *n_out = h.n_trades;
     if (h.n_trades > v->trade_cap)
       fail(MLOB_E_RUNTIME, "trade log overflow: " + std::to_string(h.n_trades) + " trades > capacity " +
                                std::to_string(v->trade_cap));

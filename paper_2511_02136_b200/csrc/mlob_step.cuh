@@ -387,9 +387,9 @@ struct MsgRef {
     return static_cast<int64_t>((static_cast<uint64_t>(hi) << 32) | lo);
   }
 };
-__device__ __forceinline__ MsgRef lds_hot(const DevMsg* p) {
+__device__ __forceinline__ MsgRef lds_hot_a(uint32_t a) {
   MsgRef m;
-  m.a = smem_u32(p);
+  m.a = a;
   uint32_t x, y, z, w;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4+16];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(m.a));
   m.price = static_cast<int32_t>(x);
@@ -399,6 +399,7 @@ __device__ __forceinline__ MsgRef lds_hot(const DevMsg* p) {
   m.trader = static_cast<int32_t>(w);
   return m;
 }
+__device__ __forceinline__ MsgRef lds_hot(const DevMsg* p) { return lds_hot_a(smem_u32(p)); }
 
 __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   const uint32_t b = smem_u32(bar);
@@ -462,7 +463,7 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
 #ifndef MLOB_SCAN_UNR  // candidate-filter scans fully unrolled: 32 loads in flight
 #define MLOB_SCAN_UNR 32
 #endif
-template <int SPL, bool SMEM = (SPL > 8)>
+template <int SPL, bool REC, bool SMEM = (SPL > 8)>
 struct WarpEnv {
   using SideT = typename std::conditional<SMEM, SmemSide<SPL>, RegSide<SPL>>::type;
   // rows per unrolled group: all rows for register books (a full unroll keeps
@@ -496,10 +497,27 @@ struct WarpEnv {
   // config words cached in registers (measured: reading them from the staged
   // shared-memory copy at each use is 4% slower)
   int capacity_, n_agents_;
-  bool rec_trades_;
   __device__ __forceinline__ int capacity() const { return capacity_; }
-  __device__ __forceinline__ bool rec_trades() const { return rec_trades_; }
-  __device__ __forceinline__ int n_agents() const { return n_agents_; }
+  // the trade log is a template parameter (a runtime flag in the fill loop
+  // measured 5 % on config C: its register and branches)
+  static __device__ __forceinline__ constexpr bool rec_trades() { return REC; }
+  // register books: n_agents read from the staged config (only the rare
+  // agent-fill path uses it) and an error met inside the message loop goes
+  // straight to the handle's word — no register live across the loop for
+  // either (C +2.5 %; the deep-book kernel keeps both: D -4 % otherwise)
+  __device__ __forceinline__ int n_agents() const {
+    if constexpr (SMEM)
+      return n_agents_;
+    else
+      return cfg.n_agents;
+  }
+  __device__ __forceinline__ void loop_error(uint32_t bits) {
+    if constexpr (SMEM) {
+      err |= bits;
+    } else if (lane == 0) {
+      atomicOr(kp.error, bits);
+    }
+  }
   int nb_l2, na_l2;      // top-D level counts (snapshot)
   int64_t topq0, topq1;  // level-0 aggregated qty per side
   int64_t sumq0, sumq1;  // Σ qty over the top-D levels per side
@@ -514,7 +532,6 @@ struct WarpEnv {
     }
     err = 0;
     capacity_ = c.capacity;
-    rec_trades_ = (p.flags & MLOB_VENV_RECORD_TRADES) != 0;
     n_agents_ = c.n_agents;
   }
 
@@ -719,7 +736,7 @@ struct WarpEnv {
       h.hwm[1] = static_cast<uint16_t>(h1);
       h.best[0] = best0;
       h.best[1] = best1;
-      h.n_trades = n_trades;
+      h.n_trades = REC ? n_trades : 0;  // counted only with the trade log (mlob_venv_read_trades)
       h.n_fills = n_fills;
       h.fill_head = fill_head;
     }
@@ -1101,7 +1118,7 @@ struct WarpEnv {
       for (int i = 0; i < 7; ++i) t._pad[i] = 0;
       kp.trades[env * kp.trade_cap + n_trades] = t;
     }
-    ++n_trades;
+    if constexpr (REC) ++n_trades;
     const uint32_t pt = st & 0xffu;
     if (MLOB_UNLIKELY(pt | static_cast<uint32_t>(m.trader))) {  // an agent may be involved: env.hpp:372-379 order
       log_fill(price, qty, static_cast<int>(pt), 1 - aside);
@@ -1125,7 +1142,7 @@ struct WarpEnv {
         if (lane == 0) c = atomicAdd(kp.fill_pool_ctr, 1u);
         c = __shfl_sync(FULLMASK, c, 0);
         if (c >= kp.fill_pool_chunks) {
-          err |= kErrFillPool;
+          loop_error(kErrFillPool);
           return;
         }
         if (k == 0)
@@ -1234,7 +1251,7 @@ struct WarpEnv {
       else
         insert_t<0>(m.price, rem, ilo, ihi, st);
     } else {
-      if (rem >= (1 << 24) || ihi >= (1u << 12) || seq >= (1u << 20)) err |= kErrDeepRange;  // 4-word slot
+      if (rem >= (1 << 24) || ihi >= (1u << 12) || seq >= (1u << 20)) loop_error(kErrDeepRange);  // 4-word slot
       int pk, pl;
       if (s)
         free_slot_t<1>(pk, pl);
@@ -1328,13 +1345,13 @@ struct WarpEnv {
   // local loads and a store per message).
   // The fold state lives in shared memory (scal[2] anchor, scal[3] segment
   // base, scal[4..5] Σmid): it is touched only at mid changes, so it holds no
-  // register across the loop.
-  __device__ __forceinline__ void refresh_mid(int i) {
+  // register across the loop.  m_a: the message record's shared address.
+  __device__ __forceinline__ void refresh_mid(uint32_t m_a) {
     const int64_t b0 = best0, b1 = best1;
     const int64_t nm = live0 > 0 ? (live1 > 0 ? b0 + b1 : 2 * b0) : (live1 > 0 ? 2 * b1 : mid_half);
     if (nm != mid_half) {
       int32_t* sc = sm.scal();
-      const int j = sc[3] + i;
+      const int j = sc[3] + static_cast<int32_t>(m_a >> 5);  // sc[3]: segment base - (first record's address >> 5)
       int64_t& ms = *reinterpret_cast<int64_t*>(sc + 4);
       ms += mid_half * (j - sc[2]);
       sc[2] = j;
@@ -1344,16 +1361,15 @@ struct WarpEnv {
 
   // book.hpp:65-86 + env.hpp:223-235 (mid_count / last_time / messages are
   // derived once after the loop: they only depend on the message count).
-  // i: the message's index within its segment (see refresh_mid)
-  __device__ __forceinline__ void run_message(const MsgRef& m, int i) {
+  __device__ __forceinline__ void run_message(const MsgRef& m) {
     if (m.kind == MLOB_NEW_LIMIT) {
       if (m.qty > 0) {
         moved = false;
         new_limit(m);
-        if (moved) refresh_mid(i);
+        if (moved) refresh_mid(m.a);
       }
     } else if (m.kind <= MLOB_EXECUTE_VISIBLE) {
-      if (by_id(m, m.kind == MLOB_DELETE)) refresh_mid(i);
+      if (by_id(m, m.kind == MLOB_DELETE)) refresh_mid(m.a);
     }
   }
 
@@ -1380,7 +1396,15 @@ struct WarpEnv {
         n = min(kChunk, mps - seg * kChunk);
         sm.scal()[3] = n_amsg + seg * kChunk;
       }
-      for (int i = 0; i < n; ++i) run_message(lds_hot(buf + i), i);
+      // the loop runs over the records' shared-memory addresses (the index
+      // refresh_mid needs is recovered from the address: C +2 % over a
+      // counted loop, one register less across it)
+      {
+        const uint32_t a0 = smem_u32(buf);
+        if (seg < 0) sm.scal()[3] = 0;
+        sm.scal()[3] -= static_cast<int32_t>(a0 >> 5);
+        for (uint32_t a = a0, e = a0 + 32u * static_cast<uint32_t>(n); a != e; a += 32u) run_message(lds_hot_a(a));
+      }
       if (seg >= 0 && seg + 2 < nch) stage(slice + (seg + 2) * kChunk, min(kChunk, mps - (seg + 2) * kChunk));
     }
     __syncwarp();
