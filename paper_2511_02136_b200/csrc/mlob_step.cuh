@@ -1160,55 +1160,60 @@ struct WarpEnv {
 
   bool moved;  // a top (best price or side emptiness) changed: refresh the mid
 
-  // book.hpp:150-187 (process_new_limit + rest_order)
-  __device__ __forceinline__ void new_limit(const MsgRef& m) {
-    const int s = m.side, o = s ^ 1;
+  // side-specialised handlers: the message's side is dispatched once per
+  // message (C +10.6 %, E +8.7 %, D +6 % over handlers branching on a runtime
+  // side at every use)
+  template <int S>
+  __device__ __forceinline__ int& live_() {
+    if constexpr (S == 0)
+      return live0;
+    else
+      return live1;
+  }
+  template <int S>
+  __device__ __forceinline__ int32_t& best_() {
+    if constexpr (S == 0)
+      return best0;
+    else
+      return best1;
+  }
+  // book.hpp:150-187 (process_new_limit + rest_order), S: the order's side
+  template <int S>
+  __device__ __forceinline__ void new_limit_t(const MsgRef& m) {
+    constexpr int O = S ^ 1;
     int32_t rem = m.qty;
     const bool pass_ids = rec_trades();
-    // crossing test with the sign folded in: ~x reverses the int32 order, so
-    // for a sell (s = 1, flip = -1) (bp ^ flip) <= (price ^ flip) is bp >= price
-    const int32_t flip = -s, kprice = m.price ^ flip;
     while (rem > 0) {
-      const int lo_ = o ? live1 : live0;
-      const int32_t bp = o ? best1 : best0;
-      if (lo_ == 0 || (bp ^ flip) > kprice) break;
+      const int32_t bp = best_<O>();
+      // a buy crosses asks at or below its price, a sell bids at or above
+      if (live_<O>() == 0 || (S == 0 ? bp > m.price : bp < m.price)) break;
       if constexpr (!SMEM) {
-        const uint32_t gst = o ? oldest_st_t<1>(bp) : oldest_st_t<0>(bp);
+        const uint32_t gst = oldest_st_t<O>(bp);
         uint32_t idlo = 0, idhi = 0;
-        const int32_t q = o ? q_of_st_t<1>(gst, pass_ids, idlo, idhi) : q_of_st_t<0>(gst, pass_ids, idlo, idhi);
+        const int32_t q = q_of_st_t<O>(gst, pass_ids, idlo, idhi);
         if (MLOB_PREFIX_WALK && q < rem) {  // the order walk goes past the level's oldest order
-          rem = o ? walk_level_t<1>(bp, rem, m, s) : walk_level_t<0>(bp, rem, m, s);
+          rem = walk_level_t<O>(bp, rem, m, S);
           continue;
         }
         const int32_t fill = min(rem, q);
         rem -= fill;
         if (fill == q) {
           moved = true;
-          if (o) {
-            clear_st_t<1>(gst);
-            if (--live1 > 0) best1 = side_best_t<1>();
-          } else {
-            clear_st_t<0>(gst);
-            if (--live0 > 0) best0 = side_best_t<0>();
-          }
-        } else if (o) {
-          setq_st_t<1>(gst, q - fill);
+          clear_st_t<O>(gst);
+          if (--live_<O>() > 0) best_<O>() = side_best_t<O>();
         } else {
-          setq_st_t<0>(gst, q - fill);
+          setq_st_t<O>(gst, q - fill);
         }
-        record_trade(bp, fill, m, idlo, idhi, gst, s);
+        record_trade(bp, fill, m, idlo, idhi, gst, S);
       } else {  // shared-memory (deep) books
         uint32_t lm;
         int lk;
-        if (o)
-          scan_oldest_t<1>(bp, lm, lk);
-        else
-          scan_oldest_t<0>(bp, lm, lk);
+        scan_oldest_t<O>(bp, lm, lk);
         const uint32_t gst = __reduce_min_sync(FULLMASK, lm);
         const int owner = __ffs(__ballot_sync(FULLMASK, lm == gst)) - 1;
         int32_t q;
         uint32_t idlo, idhi;
-        slot_get_qid(o, lk, q, idlo, idhi);
+        slot_get_qid(O, lk, q, idlo, idhi);
         q = __shfl_sync(FULLMASK, q, owner);
         if (pass_ids) {
           idlo = __shfl_sync(FULLMASK, idlo, owner);
@@ -1218,120 +1223,80 @@ struct WarpEnv {
         const bool me = lane == owner;
         rem -= fill;
         if (fill == q) {
-          slot_clear(o, lk, me);
+          slot_clear(O, lk, me);
           moved = true;
-          if (o) {
-            if (--live1 > 0) best1 = side_best_t<1>();
-          } else {
-            if (--live0 > 0) best0 = side_best_t<0>();
-          }
+          if (--live_<O>() > 0) best_<O>() = side_best_t<O>();
         } else {
-          slot_setq(o, lk, me, q - fill);
+          slot_setq(O, lk, me, q - fill);
         }
-        record_trade(bp, fill, m, idlo, idhi, gst, s);
+        record_trade(bp, fill, m, idlo, idhi, gst, S);
       }
     }
     if (rem <= 0) return;
     // rest_order
-    if ((s ? live1 : live0) == capacity()) {
-      const bool ev = s ? evict_t<1>(m.price) : evict_t<0>(m.price);
-      if (!ev) return;  // newcomer dropped: no sequence number consumed
+    if (live_<S>() == capacity()) {
+      if (!evict_t<S>(m.price)) return;  // newcomer dropped: no sequence number consumed
       moved = true;
-      if (s)
-        --live1;
-      else
-        --live0;
+      --live_<S>();
     }
     const uint32_t seq = next_seq++;  // range checked once after the loop (process_messages)
     const uint32_t st = (seq << 8) | static_cast<uint32_t>(m.trader & 0xff);
     const uint32_t ilo = static_cast<uint32_t>(m.order_id()), ihi = static_cast<uint32_t>(m.order_id() >> 32);
     if constexpr (!SMEM) {
-      if (s)
-        insert_t<1>(m.price, rem, ilo, ihi, st);
-      else
-        insert_t<0>(m.price, rem, ilo, ihi, st);
+      insert_t<S>(m.price, rem, ilo, ihi, st);
     } else {
       if (rem >= (1 << 24) || ihi >= (1u << 12) || seq >= (1u << 20)) loop_error(kErrDeepRange);  // 4-word slot
       int pk, pl;
-      if (s)
-        free_slot_t<1>(pk, pl);
-      else
-        free_slot_t<0>(pk, pl);
-      if (s)
-        ask.set_u(pk, lane == pl, m.price, rem, ilo, ihi, st);
-      else
-        bid.set_u(pk, lane == pl, m.price, rem, ilo, ihi, st);
+      free_slot_t<S>(pk, pl);
+      sd<S>().set_u(pk, lane == pl, m.price, rem, ilo, ihi, st);
     }
-    if (s) {
-      if (++live1 == 1 || m.price < best1) {
-        best1 = m.price;
-        moved = true;
-      }
-    } else {
-      if (++live0 == 1 || m.price > best0) {
-        best0 = m.price;
-        moved = true;
-      }
+    if (++live_<S>() == 1 || (S == 0 ? m.price > best_<S>() : m.price < best_<S>())) {
+      best_<S>() = m.price;
+      moved = true;
     }
   }
 
   // book.hpp:189-207 (reduce_order / remove_order); absent ids are no-ops.
-  __device__ __forceinline__ bool by_id(const MsgRef& m, bool remove) {
-    const int s = m.side;
+  template <int S>
+  __device__ __forceinline__ bool by_id_t(const MsgRef& m, bool remove) {
     const uint32_t lo = static_cast<uint32_t>(m.order_id()), hi = static_cast<uint32_t>(m.order_id() >> 32);
     if constexpr (!SMEM) {
       int32_t p = 0, q = 0;
       uint32_t st = 0;
-      const uint32_t tot = s ? id_gather_t<1>(lo, hi, p, q, st) : id_gather_t<0>(lo, hi, p, q, st);
+      const uint32_t tot = id_gather_t<S>(lo, hi, p, q, st);
       if (tot == 0) return false;
       if (MLOB_UNLIKELY(tot > 1)) {  // duplicate live ids: the first in storage order
-        st = s ? dup_st_t<1>(lo, hi, p) : dup_st_t<0>(lo, hi, p);
+        st = dup_st_t<S>(lo, hi, p);
         uint32_t ilo, ihi;
-        q = s ? q_of_st_t<1>(st, false, ilo, ihi) : q_of_st_t<0>(st, false, ilo, ihi);
+        q = q_of_st_t<S>(st, false, ilo, ihi);
       }
       const int32_t nq = remove ? 0 : q - min(q, m.qty);
       if (nq == 0) {
-        if (s) {
-          clear_st_t<1>(st);
-          if (--live1 > 0 && p == best1) best1 = side_best_t<1>();
-        } else {
-          clear_st_t<0>(st);
-          if (--live0 > 0 && p == best0) best0 = side_best_t<0>();
-        }
+        clear_st_t<S>(st);
+        if (--live_<S>() > 0 && p == best_<S>()) best_<S>() = side_best_t<S>();
         return true;
       }
-      if (s)
-        setq_st_t<1>(st, nq);
-      else
-        setq_st_t<0>(st, nq);
+      setq_st_t<S>(st, nq);
       return false;
     } else {  // shared-memory (deep) books
       int nm, lk;
-      if (s)
-        scan_id_t<1>(lo, hi, nm, lk);
-      else
-        scan_id_t<0>(lo, hi, nm, lk);
+      scan_id_t<S>(lo, hi, nm, lk);
       const uint32_t b = __ballot_sync(FULLMASK, nm > 0);
       if (b == 0) return false;
       int owner = __ffs(b) - 1;
-      if (__reduce_add_sync(FULLMASK, static_cast<uint32_t>(nm)) != 1)
-        owner = s ? dup_owner_t<1>(lo, hi, lk) : dup_owner_t<0>(lo, hi, lk);
+      if (__reduce_add_sync(FULLMASK, static_cast<uint32_t>(nm)) != 1) owner = dup_owner_t<S>(lo, hi, lk);
       int32_t p, q;
-      slot_get_pq(s, lk, p, q);
+      slot_get_pq(S, lk, p, q);
       p = __shfl_sync(FULLMASK, p, owner);
       q = __shfl_sync(FULLMASK, q, owner);
       const int32_t nq = remove ? 0 : q - min(q, m.qty);
       const bool me = lane == owner;
       if (nq == 0) {
-        slot_clear(s, lk, me);
-        if (s) {
-          if (--live1 > 0 && p == best1) best1 = side_best_t<1>();
-        } else {
-          if (--live0 > 0 && p == best0) best0 = side_best_t<0>();
-        }
+        slot_clear(S, lk, me);
+        if (--live_<S>() > 0 && p == best_<S>()) best_<S>() = side_best_t<S>();
         return true;
       }
-      slot_setq(s, lk, me, nq);
+      slot_setq(S, lk, me, nq);
       return false;
     }
   }
@@ -1365,11 +1330,15 @@ struct WarpEnv {
     if (m.kind == MLOB_NEW_LIMIT) {
       if (m.qty > 0) {
         moved = false;
-        new_limit(m);
+        if (m.side)
+          new_limit_t<1>(m);
+        else
+          new_limit_t<0>(m);
         if (moved) refresh_mid(m.a);
       }
     } else if (m.kind <= MLOB_EXECUTE_VISIBLE) {
-      if (by_id(m, m.kind == MLOB_DELETE)) refresh_mid(m.a);
+      const bool del = m.kind == MLOB_DELETE;
+      if (m.side ? by_id_t<1>(m, del) : by_id_t<0>(m, del)) refresh_mid(m.a);
     }
   }
 
