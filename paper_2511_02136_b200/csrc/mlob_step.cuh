@@ -374,7 +374,7 @@ __device__ __forceinline__ DevMsg lds_msg(const DevMsg* p) {
 struct MsgRef {
   uint32_t a;  // shared-window address of the record
   int32_t price, qty;
-  int32_t kind, side;  // widened once at the load (no per-use byte masks)
+  int32_t kind, side;  // kind widened once at the load; side: nonzero = ask
   int32_t trader;
   __device__ __forceinline__ uint64_t order_id() const {
     uint32_t lo, hi;
@@ -395,7 +395,7 @@ __device__ __forceinline__ MsgRef lds_hot_a(uint32_t a) {
   m.price = static_cast<int32_t>(x);
   m.qty = static_cast<int32_t>(y);
   m.kind = static_cast<int32_t>(z & 0xffu);
-  m.side = static_cast<int32_t>((z >> 8) & 0xffu);
+  m.side = static_cast<int32_t>(z & 0xff00u);  // only tested against zero (one LOP3 to a predicate)
   m.trader = static_cast<int32_t>(w);
   return m;
 }
@@ -999,7 +999,10 @@ struct WarpEnv {
       sv = c ? d.ST(k) : sv;
     }
     const uint32_t tot = __reduce_add_sync(FULLMASK, n);
-    if (tot == 1) {
+    // gathered whenever there is a match (duplicates are re-resolved by the
+    // caller): a two-way branch, where tot == 0 / 1 / > 1 compiled to a jump
+    // table (BRX through the constant bank)
+    if (tot != 0) {
       p = static_cast<int32_t>(__reduce_or_sync(FULLMASK, pv));
       q = static_cast<int32_t>(__reduce_or_sync(FULLMASK, qv));
       st = __reduce_or_sync(FULLMASK, sv);
