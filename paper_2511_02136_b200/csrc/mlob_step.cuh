@@ -1124,8 +1124,11 @@ struct WarpEnv {
     if constexpr (REC) ++n_trades;
     const uint32_t pt = st & 0xffu;
     if (MLOB_UNLIKELY(pt | static_cast<uint32_t>(m.trader))) {  // an agent may be involved: env.hpp:372-379 order
-      log_fill(price, qty, static_cast<int>(pt), 1 - aside);
-      log_fill(price, qty, m.trader, aside);
+      // passive side, then the aggressor: one copy of the (cold) append code
+      // per call site instead of two inside the message loop's code span
+      // (C +1 %, E +1.8 %: the loop is instruction-fetch sensitive)
+#pragma unroll 1
+      for (int e = 0; e < 2; ++e) log_fill(price, qty, e ? m.trader : static_cast<int>(pt), e ? aside : 1 - aside);
     }
   }
 
