@@ -79,14 +79,10 @@ __device__ inline uint32_t* book_region(char* base, const DevCfg& c) {
   return reinterpret_cast<uint32_t*>(base + b);
 }
 
-// Register-book book_kernel blocks: one block of kSyncWarps warps per SM walks
-// the envs in rounds with a block barrier at each round start, so the SM's
-// warps run the same phase's code together (the I-cache holds one phase).
-// Shared-memory (deep) books: blocks of as many warps as the shared memory
-// holds, one env per warp.
-#ifndef MLOB_ROUND_SYNC  // block barrier at each round start (measured -3 % since the split)
-#define MLOB_ROUND_SYNC 0
-#endif
+// Register-book book_kernel blocks: one persistent block per SM walks the
+// envs in rounds (no block barrier between rounds: measured -3 % once the step
+// was split).  Shared-memory (deep) books: blocks of as many warps as the
+// shared memory holds, one env per warp.
 // warps per register-book block and the register budget they leave: C <= 128
 // (SPL <= 4) 28 warps x 72 registers (+2.4 % on C over 24 x 80, after the
 // header fields left the loop's registers); SPL = 8 keeps 80 book registers,
@@ -185,7 +181,7 @@ __global__ void __launch_bounds__(kThreadBlock) reset_kernel(const __grid_consta
 }
 
 // book_kernel: stages (3)+(4) of the step, one warp per env.  Register books
-// (C <= 256): a grid of one phase-synchronised block per SM walks the envs in
+// (C <= 256): a grid of one persistent block per SM walks the envs in
 // rounds (env = first + r * stride), the next round's first replay chunk
 // staged while the current env finishes.  Deep books: one env per warp.
 // REC: the trade log is on (MLOB_VENV_RECORD_TRADES) — a separate
@@ -213,7 +209,7 @@ __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL
   const uint64_t first = static_cast<uint64_t>(blockIdx.x) * kWarps + warp;
   constexpr bool rounds = rounds_of<SPL>();
   bool idle = first >= kp.n_envs;
-  if (idle && !rounds) return;  // rounds: idle warps keep joining the block barriers
+  if (idle && !rounds) return;  // rounds: an idle warp skips every round below
   const DevCfg& cfg = sp_.cfg;
   char* wbase = smem + warp * warp_smem_bytes(cfg);
   WarpSmem sm{wbase};
@@ -235,9 +231,6 @@ __global__ void __launch_bounds__(warps_per_block<SPL>() * kWarp, min_blocks<SPL
   const uint64_t n_rounds = rounds ? (kp.n_envs + stride - 1) / stride : 1;
   uint64_t nenv = rounds ? first + stride : kp.n_envs;
   for (uint64_t env = first, round = 0; round < n_rounds; ++round) {
-    if constexpr (rounds && MLOB_ROUND_SYNC) {
-      if (round > 0) __syncthreads();
-    }
     if (!idle) {
       const bool has_next = nenv < kp.n_envs;
       w.bind(env);
