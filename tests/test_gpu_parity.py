@@ -695,3 +695,30 @@ def test_step_io_chunked_matches_oracle(orc, scenario, monkeypatch):
                     assert g.view(e).book(side).tobytes() == r.book(side).tobytes()
             else:
                 compare_env_state(g.view(e), r, trades=False)
+
+
+def test_trade_log_instantiation_gate():
+    """The trade log is its own book_kernel instantiation (REC = true when
+    MLOB_VENV_RECORD_TRADES is set): both instantiations evolve identical
+    books; the one without the log refuses mlob_venv_read_trades
+    (MarketEnv::step_trades, env.hpp:139-141), the other returns the step's
+    TradeRecords."""
+    cfg, synth_kw, _ = scenario_configs()["mm_fixed_exec"]
+    dev = dev_store(synth_kw)
+    n = 6
+    plain = MarketVecEnv(dev, cfg, seed=2, n_envs=n)
+    logged = MarketVecEnv(dev, cfg, seed=2, n_envs=n, record_trades=True)
+    for v in (plain, logged):
+        v.reset_all()
+    n_trades = 0
+    for t in range(cfg.steps_per_episode - 1):
+        for v in (plain, logged):
+            v.step_random(3, t)
+        for e in range(n):
+            for side in (0, 1):
+                assert plain.view(e).book(side).tobytes() == logged.view(e).book(side).tobytes()
+            n_trades += len(logged.view(e).trades())
+        assert plain.rewards().tobytes() == logged.rewards().tobytes()
+    assert n_trades > 0
+    with pytest.raises(LogicError, match="trade log disabled"):
+        plain.view(0).trades()
