@@ -143,6 +143,7 @@ def reference_arm(args) -> None:
     if rank != 0:
         return
     row, workers, n, label = cpu_reference_run(args.ref_envs, args.steps, args.warmup, args.workload)
+    cfg = workload(args.workload)[1]
     v = row.messages_per_sec
     sample = (f"{n} envs x {args.steps} timed steps (+{args.warmup} warm-up) of workload "
               f"{args.workload}, bench::run_throughput with {workers} worker threads")
@@ -150,8 +151,8 @@ def reference_arm(args) -> None:
            "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": 1e3 * row.wall_seconds / max(1, args.steps), "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-           "config": {"workload": label, "n_envs_sample": n, "messages_per_step": 100,
-                      "book_capacity": 100},
+           "config": {"workload": label, "n_envs_sample": n, "messages_per_step": cfg.messages_per_step,
+                      "book_capacity": cfg.book_capacity},
            "env_steps_per_s": row.steps_per_sec,
            "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "reference",
                             "sample": sample},
