@@ -36,7 +36,6 @@ constexpr int kMaxSpecs = MLOB_MAX_SPECS;
 constexpr int kMaxActive = MLOB_MAX_ACTIVE;
 constexpr int kMaxObsDepth = 64;
 constexpr int kChunk = 128;       // replay messages staged per bulk copy
-constexpr int kFillLog = 32;      // per-env exact fill log (MM rewards), smem
 constexpr uint32_t kEmptySt = 0xffffffffu;
 constexpr uint32_t kMaxSeq = 1u << 24;  // arrival_seq lives in the top 24 bits of `st`
 

@@ -1,19 +1,22 @@
-// mlob_step.cuh — the warp-per-environment state machine (K1+K2+K3 device code).
+// mlob_step.cuh — the warp-per-environment book state machine (book_kernel,
+// stages (3)+(4) of MarketEnv::step; the thread-per-env stages live in
+// mlob_thread.cuh).
 //
 // One warp owns one environment for a whole step:
 //   * the env's book is loaded from HBM into registers (SoA rows of 32 slots,
-//     lane l owns slots l, l+32, ...), processed, and stored back;
+//     lane l owns slots l, l+32, ...; C <= 256) or, for deep books, bulk-copied
+//     into shared memory in the HBM layout (4-word slots, C <= 1024);
 //   * the step's replay slice is staged global->shared with cp.async.bulk
-//     (TMA bulk copy, mbarrier completion), overlapped with the book load and
-//     the agent-order generation;
+//     (TMA bulk copy, mbarrier completion), overlapped with the book load;
 //   * every book operation is warp-cooperative: best price / oldest order by
-//     redux.sync min/max, order-id lookup by ballot, free-slot search by ballot;
-//   * step outcomes (rewards, infos, L2 top-D, observations) are computed in the
-//     same launch; terminal envs are reset in place (MarketVecEnv auto-reset).
-// The per-message loop is kept small (one copy shared by agent and replay
-// messages, runtime side, per-side code only in tiny scan primitives, agent
-// fill attribution deferred to a non-inlined routine): the v0 kernel was
-// instruction-cache bound (profiles/r1_v0_step_kernel_ncu.md).
+//     redux.sync min/max, order-id lookup by match counting, free-slot search
+//     by ballot;
+//   * the handlers are specialised on the message's side (one dispatch per
+//     message) and the trade log is a template parameter: the message loop is
+//     bound by instruction issue and fetch, and its register budget (72 at 28
+//     warps per SM) decides its speed;
+//   * agent fills are appended to the env's fill log in fill order for the
+//     outcome kernel; the L2 summary, active orders and header go back to HBM.
 // Reference semantics followed (paths under /root/reference/proj/include/marlob):
 //   lob/book.hpp:65-220, env/env.hpp:143-503, agents/*.hpp, core/rng.hpp,
 //   ippo/rollout.hpp:290-318, bench/bench.hpp:53-70.
