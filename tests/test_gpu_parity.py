@@ -697,15 +697,16 @@ def test_step_io_chunked_matches_oracle(orc, scenario, monkeypatch):
                 compare_env_state(g.view(e), r, trades=False)
 
 
-def test_trade_log_instantiation_gate():
+@pytest.mark.parametrize("n", [6, 5000])
+def test_trade_log_instantiation_gate(n):
     """The trade log is its own book_kernel instantiation (REC = true when
     MLOB_VENV_RECORD_TRADES is set): both instantiations evolve identical
-    books; the one without the log refuses mlob_venv_read_trades
-    (MarketEnv::step_trades, env.hpp:139-141), the other returns the step's
-    TradeRecords."""
+    books (one round of warps, and 5,000 envs: more envs than one round of
+    the persistent grid); the one without the log refuses
+    mlob_venv_read_trades (MarketEnv::step_trades, env.hpp:139-141), the
+    other returns the step's TradeRecords."""
     cfg, synth_kw, _ = scenario_configs()["mm_fixed_exec"]
     dev = dev_store(synth_kw)
-    n = 6
     plain = MarketVecEnv(dev, cfg, seed=2, n_envs=n)
     logged = MarketVecEnv(dev, cfg, seed=2, n_envs=n, record_trades=True)
     for v in (plain, logged):
@@ -714,7 +715,7 @@ def test_trade_log_instantiation_gate():
     for t in range(cfg.steps_per_episode - 1):
         for v in (plain, logged):
             v.step_random(3, t)
-        for e in range(n):
+        for e in (range(n) if n <= 64 else sorted({0, 1, 4143, 4144, n - 1, *range(0, n, 397)})):
             for side in (0, 1):
                 assert plain.view(e).book(side).tobytes() == logged.view(e).book(side).tobytes()
             n_trades += len(logged.view(e).trades())
