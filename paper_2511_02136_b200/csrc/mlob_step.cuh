@@ -473,11 +473,12 @@ struct WarpEnv {
   // them in registers); for shared-memory books the candidate-filter scans
   // (id, oldest at a price, best price) unroll fully — 32 independent
   // ld.shared in flight, D +17 % over groups of 4 — and every other row loop
-  // runs in groups of 2 (code size: 16 or a full unroll everywhere is slower).  An
-  // explicit `#pragma unroll N` on the row loops changes the register-book
-  // code (measured -11% on config C), hence the two-level loop below.
-#ifndef MLOB_SMEM_UNR  // shared-memory books: rows per unrolled group (measured: 2)
-#define MLOB_SMEM_UNR 2
+  // runs in groups of 4 (since the side-specialised handlers: +3 % on D over
+  // groups of 2, 8 no better; 1 is -3 %).  An explicit `#pragma unroll N` on
+  // the row loops changes the register-book code (measured -11% on config C),
+  // hence the two-level loop below.
+#ifndef MLOB_SMEM_UNR  // shared-memory books: rows per unrolled group (measured: 4)
+#define MLOB_SMEM_UNR 4
 #endif
   static constexpr int kUnr = (SMEM && SPL >= MLOB_SMEM_UNR) ? MLOB_SMEM_UNR : SPL;
   static constexpr int kScanUnr = (SMEM && SPL >= MLOB_SCAN_UNR) ? MLOB_SCAN_UNR : SPL;
