@@ -305,7 +305,8 @@ def measure(name, args, world, rank, local, dev, allreduce, barrier, cpu_group, 
     achieved = bb * (msgs / args.steps) / book_s / 1e9 if book_s > 0 else None
     inst = prof.get("inst_per_msg")
     out["roofline"] = {
-        "bound": "hbm", "kernel": f"book_kernel<{spl}, false>", "achieved": achieved, "peak": peak,
+        "bound": "hbm", "kernel": f"book_kernel<{spl}, false, {'true' if spl <= 4 and n_local >= 16384 else 'false'}>",
+        "achieved": achieved, "peak": peak,
         "unit": "GB/s", "frac": achieved / peak if achieved else None,
         "traffic": prof["dram_bytes_per_msg"] * (msgs / args.steps) if "dram_bytes_per_msg" in prof else None,
         "bytes_per_msg": round(bb, 1), "peak_kind": peak_kind,

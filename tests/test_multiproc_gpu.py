@@ -170,4 +170,4 @@ def test_bench_two_ranks_one_line():
     assert len(lines) == 1, p.stdout
     d = lines[0]
     assert d["n_gpus"] == 2 and d["config"]["envs_per_gpu"] == 4096 and d["value"] > 0
-    assert d["e2e"]["value"] > 0 and d["roofline"]["kernel"] == "book_kernel<4, false>"
+    assert d["e2e"]["value"] > 0 and d["roofline"]["kernel"] == "book_kernel<4, false, false>"

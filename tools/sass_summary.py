@@ -8,8 +8,8 @@ import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KERNELS = {
-    "_ZN4mlob11book_kernelILi4ELb0EEEvNS_7KParamsE": "book_kernel<4> (C <= 128, register book)",
-    "_ZN4mlob11book_kernelILi32ELb0EEEvNS_7KParamsE": "book_kernel<32> (C <= 1024, shared-memory book)",
+    "_ZN4mlob11book_kernelILi4ELb0ELb1EEEvNS_7KParamsE": "book_kernel<4, false, true> (C <= 128, register book, large batches)",
+    "_ZN4mlob11book_kernelILi32ELb0ELb0EEEvNS_7KParamsE": "book_kernel<32, false, false> (C <= 1024, shared-memory book)",
     "_ZN4mlob10act_kernelENS_7KParamsE": "act_kernel",
     "_ZN4mlob14outcome_kernelENS_7KParamsE": "outcome_kernel",
     "_ZN4mlob12reset_kernelENS_7KParamsE": "reset_kernel",
