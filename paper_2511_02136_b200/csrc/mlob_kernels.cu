@@ -350,7 +350,9 @@ static size_t book_staged_bytes(const DevCfg& c) {  // dynamic-smem prefix (deep
 static int book_warps(const DevCfg& c, bool waves) {
   const bool deep = deep_book(c);
   const int spl = spl_of(c.capacity);
-  const int want = waves ? kWaveWarps : deep ? 8 : spl <= 4 ? MLOB_SYNC_WARPS : 16;
+  // deep books: 3-warp blocks, two per SM (finer backfill than one 6-warp
+  // block: D +1.5 %; one-warp blocks fit only five per SM: -13 %)
+  const int want = waves ? kWaveWarps : deep ? 3 : spl <= 4 ? MLOB_SYNC_WARPS : 16;
   const size_t per = warp_smem_bytes(c);
   const size_t limit = deep ? 227 * 1024 - sizeof(SmemOff) - book_staged_bytes(c) - 256
                             : 227 * 1024 - sizeof(StagedParams) - sizeof(SmemOff) - 1024;
